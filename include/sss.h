@@ -1,0 +1,220 @@
+/* ===========================================================================
+ * sss.h — C ABI of the B200-native hot path of Student Splatting and Scooping
+ * (SSS, arXiv 2503.10148).  Citations "PAPER.md:l" are lines of the paper's
+ * text; "Rnn" are the readings listed in
+ * DESIGN.md §1 where the paper is silent or ambiguous.
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  - All array pointers are DEVICE pointers (CUDA global memory) unless the
+ *    argument is marked "host".  Every call is asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ *  - Ownership: the caller allocates and frees every buffer.  The library
+ *    allocates nothing and keeps no global mutable state, so calls on
+ *    different streams may run concurrently.  Workspaces are sized by the
+ *    matching *_workspace() query.
+ *  - Component parameters are SoA planes of stride n (sss_params): plane p of
+ *    component i is at base[p * n + i].  With K = (D+1)^2 SH coefficients per
+ *    channel: mean[3], log_scale[3], rot[4] (w,x,y,z, not necessarily unit),
+ *    raw_nu[1], raw_opacity[1], sh[3K] (plane 3k + channel).  When the six
+ *    pointers are consecutive slices of one allocation the whole set is a
+ *    single flat buffer of (12 + 3K) * n floats (used for the NCCL all-reduce).
+ *  - Errors: argument validation returns synchronously (SSS_ERR_ARG /
+ *    SSS_ERR_SHAPE) and launches nothing; a failed launch returns
+ *    SSS_ERR_CUDA; sss_last_error() gives a thread-local message.
+ *    Instance overflow in sss_bin_sort is reported on the device (see there).
+ * ======================================================================== */
+#ifndef SSS_H_
+#define SSS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SSS_API __attribute__((visibility("default")))
+#else
+#define SSS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SSS_OK = 0,
+  SSS_ERR_ARG = 1,      /* null pointer, n < 0, sh_degree outside [0,3], bad camera */
+  SSS_ERR_SHAPE = 2,    /* zero-size image, views of different sizes, too many bins */
+  SSS_ERR_CAPACITY = 3, /* bin capacity exceeded (sss_check_overflow) */
+  SSS_ERR_CUDA = 4      /* CUDA launch / runtime error */
+} sss_status;
+
+#define SSS_TILE 16          /* tile edge in pixels */
+#define SSS_MAX_BINS 6144    /* bins per view (tiles >> bin_shift) */
+#define SSS_REC_FLOATS 12    /* floats per projected record (48 B) */
+#define SSS_G2D_FLOATS 12    /* floats per screen-space gradient record (48 B) */
+
+/* Pinhole camera (host struct).  p_cam = rot * x + trans (rot row-major,
+ * world->camera; OpenCV axes x right, y down, z forward).  Pixel (i, j) has its
+ * centre at (i + 1/2, j + 1/2).  Eq. 4's W, t and the perspective Jacobian J
+ * (R4, R5); z_near culls components (R24). */
+typedef struct {
+  float rot[9];
+  float trans[3];
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float z_near;
+} sss_camera;
+
+/* Component parameters ("mean mu, covariance Sigma (S and R),
+ * colour c, opacity o, degree parameter nu"), device SoA planes, see above.
+ * nu = min(1 + softplus(raw_nu), 1e4) (R1); o = tanh(raw_opacity)
+ * (R2); S = diag(exp(log_scale)) (R3); R = R(q / |q|).
+ * The same struct describes gradients and Adam moments (same layout). */
+typedef struct {
+  int64_t n;
+  int32_t sh_degree;
+  int32_t reserved;
+  float* mean;
+  float* log_scale;
+  float* rot;
+  float* raw_nu;
+  float* raw_opacity;
+  float* sh;
+} sss_params;
+
+/* Per-(view, component) projection (output of sss_project).
+ *  rec   [V][n][12] floats: {mx, my, A, B2}, {C, hmax, o, inv_nu},
+ *        {e, r, g, b} with (A, B2/2, C) the conic (Sigma2D)^-1, hmax the L9
+ *        cutoff, e = -(nu+2)/2 and (r,g,b) the clamped SH colour.
+ *  depth [V][n] camera-space z of the mean, fp32 (the sort key source, R8).
+ *  rect  [V][n][4] int16 inclusive tile rect x0,y0,x1,y1; x0 > x1 = culled.
+ * Memory: 60 B per (view, component). */
+typedef struct {
+  int64_t n;
+  int32_t n_views;
+  int32_t reserved;
+  float* rec;
+  float* depth;
+  int16_t* rect;
+} sss_projected;
+
+/* Depth-ordered bin lists (output of sss_bin_sort).  A bin is a square of
+ * 2^bin_shift x 2^bin_shift tiles; bin_shift = 0 gives the classic per-tile
+ * lists.  For view v the entries of bin b are ids[v*capacity + ranges[2(v*nb+b)]
+ * ... + ranges[2(v*nb+b)+1]) in (depth, index) order (R8).
+ *  ids      [V][capacity] component indices
+ *  keys     nullable [V][capacity]: bin << 32 | float bits of depth
+ *  ranges   [V][n_bins][2] start, end (absolute offsets within the view)
+ *  totals   [V] instance count of the view (written even on overflow)
+ *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
+ *           scattered and every range is empty; grow and retry). */
+typedef struct {
+  int32_t bin_shift;
+  int32_t n_views;
+  int64_t capacity;
+  int32_t* ids;
+  uint64_t* keys;
+  int32_t* ranges;
+  int64_t* totals;
+  int32_t* overflow;
+} sss_bins;
+
+/* Rendered frames (output of sss_render_fwd; all views share one size).
+ *  rgb       [V][3][H][W]  C(u) of Eq. 7 + bg * W (unclamped, R21)
+ *  final_T   [V][H][W]     final transmittance W
+ *  n_contrib [V][H][W]     number of composited (included) components (R23)
+ *  last      [V][H][W]     private: bin-list offset one past the last
+ *                          composited entry (start of the backward replay) */
+typedef struct {
+  float* rgb;
+  float* final_T;
+  int32_t* n_contrib;
+  int32_t* last;
+} sss_frame;
+
+/* Hyper-parameters of one sampler step (host struct; PAPER.md:151-163,
+ * 1492-1523, R14-R19).  lr is eps of Eq. 10 (the mu step), noise the std eta
+ * of the pre-gate mu noise (R15), gate = sigmoid(-gate_k (|o| - gate_t)) (R16),
+ * grad_scale multiplies every gradient (1/V for the multi-view mean, R26). */
+typedef struct {
+  float lr, friction, noise, gate_k, gate_t;
+  int32_t burn_in; /* 1: F dropped, noise premultiplied by Sigma (R18) */
+  int32_t g_adam;  /* 1: use Adam's m^/(sqrt(v^)+eps) as g in the mu update (R17) */
+  float lr_scale, lr_rot, lr_nu, lr_opacity, lr_sh;
+  float beta1, beta2, adam_eps, grad_scale;
+  int64_t step;    /* 1-based step (Adam bias correction, noise counter) */
+  uint64_t seed;   /* Philox4x32-10 key */
+} sss_sghmc_hparams;
+
+/* flags for sss_render_bwd */
+#define SSS_BWD_NU_GRAD_PAPER 1 /* use the printed dT/dnu of PAPER.md:1301-1314 (R13) */
+
+/* a1 — projection of every component into V views (Eq. 4,
+ * 1116-1215 SM forward, 1077-1079 nu range / truncation / no low-pass).
+ * p: device params; cams: host array of n_views cameras (all the same size);
+ * out: device buffers sized as documented at sss_projected.
+ * Returns SSS_ERR_ARG / SSS_ERR_SHAPE on invalid input. */
+SSS_API sss_status sss_project(const sss_params* p, const sss_camera* cams, int32_t n_views,
+                       sss_projected* out, void* stream);
+
+/* Bytes of device scratch sss_bin_sort needs for n components, n_views views
+ * of cams[0]'s size and the given bin_shift.  0 on invalid input. */
+SSS_API size_t sss_bin_sort_workspace(int64_t n, int32_t n_views, const sss_camera* cams,
+                              int32_t bin_shift);
+
+/* a2 — bin every visible component into the bins its tile rect overlaps and
+ * order each bin's list by (fp32 depth, component index) (R8).  Implements a
+ * stable LSD radix sort of the depth keys followed by a stable counting
+ * scatter by bin.  ws: device scratch of at least sss_bin_sort_workspace()
+ * bytes.  out->bin_shift, capacity, ids, ranges, totals, overflow must be set
+ * (keys optional).  Overflow is device-side (see sss_bins). */
+SSS_API sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* cams, int32_t n_views,
+                        void* ws, size_t ws_bytes, sss_bins* out, void* stream);
+
+/* Synchronising helper: waits for `stream`, returns SSS_ERR_CAPACITY if the
+ * overflow flag of `bins` is set, SSS_OK otherwise. */
+SSS_API sss_status sss_check_overflow(const sss_bins* bins, void* stream);
+
+/* a3 — signed front-to-back compositing, Eq. 7:
+ * per pixel, components of its tile in bin order that pass the fp32 gate
+ * h <= hmax (R9) are composited with a = clamp(o T2D, -0.99, 0.99) (R10);
+ * a pixel stops after the component that makes W < 1e-4 (R11); bg (host[3])
+ * is added times the final W (R12). */
+SSS_API sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bins, const sss_camera* cams,
+                          int32_t n_views, const float* bg, sss_frame* out, void* stream);
+
+/* Bytes of device scratch sss_render_bwd needs (screen-space gradient records
+ * [V][n][12] floats).  The scratch must be ZERO before the first call; every
+ * call leaves it zero again (the projection-backward consumes and clears it). */
+SSS_API size_t sss_render_bwd_workspace(int64_t n, int32_t n_views);
+
+/* a4 + a5 (+ a6) — closed-form backward of
+ * sss_render_fwd with gating frozen (R22), accumulated (+=) into grad over all
+ * views.  Image gradient: d_rgb [V][3][H][W] if non-NULL, else the fused L1
+ * loss against target [V][3][H][W]: dL/dC = sign(C - target) / (3 H W) per
+ * view (Eq. 8's L1 term, R20); in that case loss_out (device float[1],
+ * nullable) is incremented by sum_v mean|C - target|.  fwd must be the
+ * output of sss_render_fwd for the same inputs.  flags: SSS_BWD_*. */
+SSS_API sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, const sss_bins* bins,
+                          const sss_camera* cams, int32_t n_views, const float* bg,
+                          const sss_frame* fwd, const float* d_rgb, const float* target,
+                          float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
+                          int32_t flags, void* stream);
+
+/* a7 — one sampler step in place (Eq. 10, 1492-1523; Adam on
+ * every non-mean group).  p, adam_m, adam_v: device
+ * planes (same n / sh_degree); grad read-only; momentum [3][n] device; hp host.
+ * Noise: Philox4x32-10 keyed by hp->seed, counter (i, hp->step) (R14). */
+SSS_API sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_params* adam_m,
+                          sss_params* adam_v, float* momentum, const sss_sghmc_hparams* hp,
+                          void* stream);
+
+SSS_API const char* sss_status_string(sss_status s);
+SSS_API const char* sss_last_error(void);
+/* Number of kernel launches issued by this thread since the last reset. */
+SSS_API int64_t sss_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSS_H_ */

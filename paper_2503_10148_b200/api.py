@@ -1,0 +1,281 @@
+"""Thin torch binding of the C ABI (include/sss.h), same names as the ABI.
+
+PyTorch supplies device memory and streams only; each function marshals
+pointers and calls one libsss.so entry point.  Shapes follow sss.h exactly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def n_planes(sh_degree: int) -> int:
+    return 12 + 3 * (sh_degree + 1) ** 2
+
+
+# ------------------------------------------------------------------ params
+class Params:
+    """Component parameters as one flat [P][n] fp32 device tensor (SoA planes).
+
+    Gradients and Adam moments use the same class (identical layout), so the
+    whole gradient is one contiguous buffer for the NCCL all-reduce."""
+
+    def __init__(self, planes: torch.Tensor, sh_degree: int):
+        assert planes.dtype == torch.float32 and planes.is_contiguous() and planes.dim() == 2
+        assert planes.shape[0] == n_planes(sh_degree), (planes.shape, sh_degree)
+        self.planes = planes
+        self.sh_degree = int(sh_degree)
+
+    @property
+    def n(self) -> int:
+        return int(self.planes.shape[1])
+
+    @classmethod
+    def zeros_like(cls, other: "Params") -> "Params":
+        return cls(torch.zeros_like(other.planes), other.sh_degree)
+
+    def c(self) -> L.sss_params:
+        b = self.planes.data_ptr()
+        n = self.n
+        off = lambda p: C.c_void_p(b + 4 * p * n)  # noqa: E731
+        return L.sss_params(n, self.sh_degree, 0, off(0), off(3), off(6), off(10), off(11), off(12))
+
+
+def camera_c(cam) -> L.sss_camera:
+    c = L.sss_camera()
+    R = [float(x) for x in torch.as_tensor(cam.R, dtype=torch.float32).reshape(9).tolist()]
+    t = [float(x) for x in torch.as_tensor(cam.t, dtype=torch.float32).reshape(3).tolist()]
+    for k in range(9):
+        c.rot[k] = R[k]
+    for k in range(3):
+        c.trans[k] = t[k]
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.z_near = float(cam.z_near)
+    return c
+
+
+def cameras_c(cams: Sequence) -> C.Array:
+    arr = (L.sss_camera * len(cams))()
+    for i, cam in enumerate(cams):
+        arr[i] = camera_c(cam)
+    return arr
+
+
+def tiles_of(width: int, height: int):
+    return (width + 15) // 16, (height + 15) // 16
+
+
+def n_bins_of(width: int, height: int, bin_shift: int) -> int:
+    tx, ty = tiles_of(width, height)
+    s = 1 << bin_shift
+    return ((tx + s - 1) // s) * ((ty + s - 1) // s)
+
+
+# ----------------------------------------------------------------- outputs
+@dataclass
+class Projected:
+    rec: torch.Tensor    # [V][n][12] f32
+    depth: torch.Tensor  # [V][n] f32
+    rect: torch.Tensor   # [V][n][4] i16
+
+    @classmethod
+    def empty(cls, n: int, V: int, device="cuda") -> "Projected":
+        return cls(torch.empty((V, n, L.SSS_REC_FLOATS), dtype=torch.float32, device=device),
+                   torch.empty((V, n), dtype=torch.float32, device=device),
+                   torch.empty((V, n, 4), dtype=torch.int16, device=device))
+
+    @property
+    def n(self):
+        return int(self.depth.shape[1])
+
+    @property
+    def n_views(self):
+        return int(self.depth.shape[0])
+
+    def c(self) -> L.sss_projected:
+        return L.sss_projected(self.n, self.n_views, 0, _ptr(self.rec), _ptr(self.depth),
+                               _ptr(self.rect))
+
+
+@dataclass
+class Bins:
+    bin_shift: int
+    capacity: int
+    ids: torch.Tensor               # [V][capacity] i32
+    keys: Optional[torch.Tensor]    # [V][capacity] i64 (bit pattern of u64) or None
+    ranges: torch.Tensor            # [V][n_bins][2] i32
+    totals: torch.Tensor            # [V] i64
+    overflow: torch.Tensor          # [1] i32
+
+    @classmethod
+    def empty(cls, V: int, n_bins: int, capacity: int, bin_shift: int, keys: bool,
+              device="cuda") -> "Bins":
+        cap = max(int(capacity), 1)
+        return cls(bin_shift, int(capacity),
+                   torch.empty((V, cap), dtype=torch.int32, device=device),
+                   torch.empty((V, cap), dtype=torch.int64, device=device) if keys else None,
+                   torch.empty((V, n_bins, 2), dtype=torch.int32, device=device),
+                   torch.zeros((V,), dtype=torch.int64, device=device),
+                   torch.zeros((1,), dtype=torch.int32, device=device))
+
+    def c(self) -> L.sss_bins:
+        return L.sss_bins(self.bin_shift, int(self.totals.shape[0]), self.capacity, _ptr(self.ids),
+                          _ptr(self.keys), _ptr(self.ranges), _ptr(self.totals),
+                          _ptr(self.overflow))
+
+
+@dataclass
+class Frame:
+    rgb: torch.Tensor        # [V][3][H][W] f32
+    final_T: torch.Tensor    # [V][H][W] f32
+    n_contrib: torch.Tensor  # [V][H][W] i32
+    last: torch.Tensor       # [V][H][W] i32
+
+    @classmethod
+    def empty(cls, V: int, H: int, W: int, device="cuda") -> "Frame":
+        return cls(torch.empty((V, 3, H, W), dtype=torch.float32, device=device),
+                   torch.empty((V, H, W), dtype=torch.float32, device=device),
+                   torch.empty((V, H, W), dtype=torch.int32, device=device),
+                   torch.empty((V, H, W), dtype=torch.int32, device=device))
+
+    def c(self) -> L.sss_frame:
+        return L.sss_frame(_ptr(self.rgb), _ptr(self.final_T), _ptr(self.n_contrib),
+                           _ptr(self.last))
+
+
+def hparams_c(hp) -> L.sss_sghmc_hparams:
+    return L.sss_sghmc_hparams(hp.lr, hp.friction, hp.noise, hp.gate_k, hp.gate_t,
+                               int(hp.burn_in), int(hp.g_adam), hp.lr_scale, hp.lr_rot, hp.lr_nu,
+                               hp.lr_opacity, hp.lr_sh, hp.beta1, hp.beta2, hp.adam_eps,
+                               hp.grad_scale, int(hp.step), int(hp.seed))
+
+
+# ------------------------------------------------------------- entry points
+def sss_project(params: Params, cams: Sequence, out: Optional[Projected] = None,
+                stream=None, cams_c=None) -> Projected:
+    lib = L.load()
+    V = len(cams)
+    out = out if out is not None else Projected.empty(params.n, V, params.planes.device)
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    p, o = params.c(), out.c()
+    L.check(lib.sss_project(C.byref(p), cc, V, C.byref(o), _stream_ptr(stream)), "sss_project")
+    return out
+
+
+def bin_sort_workspace_bytes(n: int, cams: Sequence, bin_shift: int, cams_c=None) -> int:
+    lib = L.load()
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    return int(lib.sss_bin_sort_workspace(n, len(cams), cc, bin_shift))
+
+
+def sss_bin_sort(proj: Projected, cams: Sequence, bin_shift: int = 0,
+                 capacity: Optional[int] = None, keys: bool = False,
+                 ws: Optional[torch.Tensor] = None, out: Optional[Bins] = None, stream=None,
+                 cams_c=None, headroom: float = 1.25) -> Bins:
+    """Bin and depth-sort.  With capacity=None the instance count is measured
+    first (one host sync) and the output sized with `headroom`."""
+    lib = L.load()
+    V = len(cams)
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    W, H = int(cams[0].width), int(cams[0].height)
+    nb = n_bins_of(W, H, bin_shift)
+    dev = proj.depth.device
+    need = bin_sort_workspace_bytes(proj.n, cams, bin_shift, cams_c=cc)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    if out is None:
+        if capacity is None:
+            probe = Bins.empty(V, nb, 0, bin_shift, False, dev)
+            pc, prc = probe.c(), proj.c()
+            L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(pc),
+                                     _stream_ptr(stream)), "sss_bin_sort(probe)")
+            capacity = int(int(probe.totals.max().item()) * headroom) + 1024
+        out = Bins.empty(V, nb, capacity, bin_shift, keys, dev)
+    bc, prc = out.c(), proj.c()
+    L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(bc),
+                             _stream_ptr(stream)), "sss_bin_sort")
+    return out
+
+
+def sss_check_overflow(bins: Bins, stream=None) -> bool:
+    lib = L.load()
+    b = bins.c()
+    st = lib.sss_check_overflow(C.byref(b), _stream_ptr(stream))
+    if st == L.SSS_ERR_CAPACITY:
+        return True
+    L.check(st, "sss_check_overflow")
+    return False
+
+
+def sss_render_fwd(proj: Projected, bins: Bins, cams: Sequence, bg=(0.0, 0.0, 0.0),
+                   out: Optional[Frame] = None, stream=None, cams_c=None) -> Frame:
+    lib = L.load()
+    V = len(cams)
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    H, W = int(cams[0].height), int(cams[0].width)
+    out = out if out is not None else Frame.empty(V, H, W, proj.depth.device)
+    bgc = (C.c_float * 3)(*[float(x) for x in bg])
+    prc, bc, fc = proj.c(), bins.c(), out.c()
+    L.check(lib.sss_render_fwd(C.byref(prc), C.byref(bc), cc, V, bgc, C.byref(fc),
+                               _stream_ptr(stream)), "sss_render_fwd")
+    return out
+
+
+def render_bwd_workspace_bytes(n: int, V: int) -> int:
+    return int(L.load().sss_render_bwd_workspace(n, V))
+
+
+def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, frame: Frame,
+                   bg=(0.0, 0.0, 0.0), d_rgb: Optional[torch.Tensor] = None,
+                   target: Optional[torch.Tensor] = None, grad: Optional[Params] = None,
+                   loss: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+                   nu_grad_paper: bool = False, stream=None, cams_c=None) -> Params:
+    """grad += d(L)/d(params).  `ws` (zeroed, reusable) holds the screen-space
+    gradient records; it is left zero by the call."""
+    lib = L.load()
+    V = len(cams)
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    grad = grad if grad is not None else Params.zeros_like(params)
+    need = render_bwd_workspace_bytes(params.n, V)
+    if ws is None:
+        ws = torch.zeros(max(need, 4), dtype=torch.uint8, device=params.planes.device)
+    assert ws.numel() >= need
+    for t in (d_rgb, target):
+        if t is not None:
+            assert t.is_contiguous() and t.dtype == torch.float32
+    bgc = (C.c_float * 3)(*[float(x) for x in bg])
+    pc, prc, bc, fc, gc = params.c(), proj.c(), bins.c(), frame.c(), grad.c()
+    flags = L.SSS_BWD_NU_GRAD_PAPER if nu_grad_paper else 0
+    L.check(lib.sss_render_bwd(C.byref(pc), C.byref(prc), C.byref(bc), cc, V, bgc, C.byref(fc),
+                               _ptr(d_rgb), _ptr(target), _ptr(loss), C.byref(gc), _ptr(ws),
+                               ws.numel(), flags, _stream_ptr(stream)), "sss_render_bwd")
+    return grad
+
+
+def sss_sghmc_step(params: Params, grad: Params, adam_m: Params, adam_v: Params,
+                   momentum: torch.Tensor, hp, stream=None) -> None:
+    lib = L.load()
+    h = hparams_c(hp)
+    pc, gc, mc, vc = params.c(), grad.c(), adam_m.c(), adam_v.c()
+    L.check(lib.sss_sghmc_step(C.byref(pc), C.byref(gc), C.byref(mc), C.byref(vc),
+                               _ptr(momentum), C.byref(h), _stream_ptr(stream)),
+            "sss_sghmc_step")
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(L.load().sss_launch_count(1 if reset else 0))

@@ -1,0 +1,43 @@
+// Shared device helpers of the SSS CUDA path (sm_100a).  Nothing here is
+// shared with oracle/ (the oracle is an independent fp64 CPU program).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sss.h"
+
+namespace sss {
+
+constexpr int kTile = SSS_TILE;
+constexpr int kMaxViewsPerLaunch = 128;
+constexpr float kAlphaMax = 0.99f;   // R10
+constexpr float kWStop = 1e-4f;      // R11
+constexpr double kNuMax = 1e4;
+
+struct DevCamera {  // a camera as the kernels see it
+  float R[9];
+  float t[3];
+  float fx, fy, cx, cy;
+  float center[3];  // -R^T t
+  float z_near;
+};
+
+struct CamPack {  // passed by value (kernel parameter space)
+  int n;
+  int width, height, tiles_x, tiles_y;
+  DevCamera cam[kMaxViewsPerLaunch];
+};
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// thread-local error plumbing (abi.cu)
+void set_error(const char* fmt, ...);
+sss_status check_launch(const char* what);
+void count_launch(int64_t k = 1);
+bool fill_campack(const sss_camera* cams, int first, int count, CamPack& cp);
+sss_status validate_params(const sss_params* p, const char* what);
+sss_status validate_cams(const sss_camera* cams, int n_views, const char* what);
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+}  // namespace sss

@@ -1,0 +1,559 @@
+// a4 + a5 (+ a6) — sss_render_bwd: closed-form backward of Eq. 7 (SM
+// "Backward Pass") to the six parameter groups
+// (PAPER.md:165).
+//
+// a4 raster backward.  One CTA per tile and view, one thread per pixel,
+// replaying the tile's bin list back to front from the last composited entry
+// (the forward's `last`).  Per pair (PAPER.md:1230-1268 chain, R10, R13):
+//   W_i = W_{i+1} / (1 - a_i),  dL/dc = g a_i W_i,
+//   dL/da = W_i sum_k g_k (c_k - S_k),  S <- c a + (1 - a) S,
+//   dL/do = dL/da T,  dL/dT = dL/da o,
+//   dT/dh = -(nu+2)/(2 nu) T / (1 + h/nu)
+//   dT/dnu = T [-1/2 ln(1 + h/nu) + (nu+2) h / (2 nu^2 (1 + h/nu))]  (R13)
+//   dh/dmu2D = -2 Q d,  dh/d(A, B, C) = (dx^2, 2 dx dy, dy^2).
+// The 10 per-pair values are reduced across the warp with a 16-lane
+// butterfly reduce-scatter (16 shuffles for 10 values instead of 50), warps
+// with no included lane skip it (vote.any), the 8 warps combine in shared
+// memory, and one vector RED per (component, tile) goes to the screen-space
+// gradient record g2d[v][i] (48 B) in the workspace.
+//
+// a6: with target != NULL the L1 image gradient sign(C - target)/(3HW) is
+// formed in the same kernel (no image-gradient buffer) and the loss summed.
+//
+// a5 projection backward.  One thread per component loops over the views
+// of the launch: it reads g2d[v][i] (and clears it), recomputes the view's
+// projection in fp32 and applies the chain of Eq. 4 (Sigma2D = J W Sigma W^T
+// J^T, mu2D = pinhole(W mu + t)), the SH view direction and colour clamp,
+// and finally the chain Sigma -> (R(q), S) -> (q, log_scale) and the
+// reparameterisations o = tanh(raw), nu = 1 + softplus(raw) once for all
+// views.  grad += result (one read-modify-write of the 240 B per component).
+#include "raster.cuh"
+
+namespace sss {
+namespace {
+
+// 16-value butterfly reduce-scatter: returns, in lane L, the warp sum of
+// value index (L >> 1) & 15.
+__device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const bool up = lane & 16;
+    const float send = up ? v[k] : v[k + 8];
+    const float keep = up ? v[k + 8] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool up = lane & 8;
+    const float send = up ? v[k] : v[k + 4];
+    const float keep = up ? v[k + 4] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool up = lane & 4;
+    const float send = up ? v[k] : v[k + 2];
+    const float keep = up ? v[k + 2] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const float send = up ? v[0] : v[1];
+    const float keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+template <bool FILTER, bool L1>
+__global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
+    const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
+    const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
+    const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
+    const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
+    float4* __restrict__ g2d, int flags) {
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
+  __shared__ int32_t spos[kBatch], sid[kBatch];
+  __shared__ __align__(16) float acc[kBatch * SSS_G2D_FLOATS];
+  __shared__ int32_t wcnt[kRasterThreads / 32];
+  __shared__ float wred[kRasterThreads / 32];
+  __shared__ int32_t smax;
+  const int v = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
+  const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
+  const int32_t start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
+  int lx, ly;
+  pixel_of(threadIdx.x, lx, ly);
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  const bool inside = x < G.width && y < G.height;
+  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t HW = (int64_t)G.width * G.height;
+  const int64_t pix = (int64_t)y * G.width + x;
+
+  float g0 = 0.f, g1 = 0.f, g2 = 0.f, W = 1.f, lsum = 0.f;
+  int32_t lastp = start;
+  const float inv3P = 1.0f / (3.0f * (float)HW);
+  if (inside) {
+    lastp = last[(int64_t)v * HW + pix];
+    W = final_T[(int64_t)v * HW + pix];
+    if (L1) {
+      const float* cimg = rgb + (int64_t)v * 3 * HW + pix;
+      const float* timg = target + (int64_t)v * 3 * HW + pix;
+      const float d0 = cimg[0] - timg[0], d1 = cimg[HW] - timg[HW], d2 = cimg[2 * HW] - timg[2 * HW];
+      g0 = (d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f));
+      g1 = (d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f));
+      g2 = (d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f));
+      lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
+    } else {
+      const float* gimg = d_rgb + (int64_t)v * 3 * HW + pix;
+      g0 = gimg[0];
+      g1 = gimg[HW];
+      g2 = gimg[2 * HW];
+    }
+  }
+  // tile end = max over pixels of `last`; loss partial sums
+  int32_t m = lastp;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (L1) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  }
+  if (threadIdx.x == 0) smax = start;
+  __syncthreads();
+  if (lane == 0) {
+    atomicMax(&smax, m);
+    if (L1) wred[w] = lsum;
+  }
+  __syncthreads();
+  const int32_t end = smax;
+  if (L1 && loss_out && threadIdx.x == 0) {
+    float s = 0.f;
+    for (int k = 0; k < kRasterThreads / 32; ++k) s += wred[k];
+    atomicAdd(loss_out, s * inv3P);
+  }
+
+  const int32_t* idv = ids + (int64_t)v * G.capacity;
+  const float4* rv = rec + (int64_t)v * G.n * 3;
+  const short4* rcv = rect + (int64_t)v * G.n;
+  float4* gv = g2d + (int64_t)v * G.n * 3;
+  const bool nu_paper = flags & SSS_BWD_NU_GRAD_PAPER;
+  float S0 = bg0, S1 = bg1, S2 = bg2;
+
+  for (int32_t hi = end; hi > start; hi -= kBatch) {
+    const int32_t lo = max(start, hi - kBatch);
+    __syncthreads();  // previous batch fully consumed and flushed
+    const int32_t pos = lo + (int32_t)threadIdx.x;
+    bool ok = pos < hi;
+    const int32_t id = ok ? idv[pos] : 0;
+    int slot, nb;
+    if (FILTER) {
+      if (ok) {
+        const short4 r = rcv[id];
+        ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) wcnt[w] = __popc(bal);
+      __syncthreads();
+      int off = 0, tot = 0;
+#pragma unroll
+      for (int k = 0; k < kRasterThreads / 32; ++k) {
+        const int c = wcnt[k];
+        off += k < w ? c : 0;
+        tot += c;
+      }
+      slot = off + __popc(bal & lt);
+      nb = tot;
+    } else {
+      slot = threadIdx.x;
+      nb = hi - lo;
+    }
+    if (ok) {
+      spos[slot] = pos;
+      sid[slot] = id;
+      sa[slot] = rv[(int64_t)id * 3 + 0];
+      sb[slot] = rv[(int64_t)id * 3 + 1];
+      sc[slot] = rv[(int64_t)id * 3 + 2];
+    }
+    for (int k = threadIdx.x; k < nb * SSS_G2D_FLOATS; k += kRasterThreads) acc[k] = 0.f;
+    __syncthreads();
+    for (int j = nb - 1; j >= 0; --j) {
+      const float4 a = sa[j];
+      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
+      bool incl = false;
+      float h = 0.f;
+      if (spos[j] < lastp) {
+        h = h_f32(px, py, a, b.x);
+        incl = h <= b.y;
+      }
+      if (!__any_sync(0xffffffffu, incl)) continue;
+      float vals[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) vals[k] = 0.f;
+      if (incl) {
+        const float4 c = sc[j];  // {e, r, g, b}
+        const float t = fmaxf(h, 0.f) * b.w;
+        const float opt = 1.f + t;
+        const float lg = log2_1p(t, b.w < (1.f / 32.f));
+        const float T = ex2_approx(c.x * lg);
+        const float araw = b.z * T;
+        const float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
+        const float Wi = __fdividef(W, 1.f - alpha);
+        const float aw = alpha * Wi;
+        vals[5] = g0 * aw;
+        vals[6] = g1 * aw;
+        vals[7] = g2 * aw;
+        float da = (g0 * (c.y - S0) + g1 * (c.z - S1) + g2 * (c.w - S2)) * Wi;
+        S0 = fmaf(c.y - S0, alpha, S0);
+        S1 = fmaf(c.z - S1, alpha, S1);
+        S2 = fmaf(c.w - S2, alpha, S2);
+        W = Wi;
+        if (fabsf(araw) > kAlphaMax) da = 0.f;
+        vals[8] = da * T;
+        const float dT = da * b.z;
+        const float Topt = __fdividef(T, opt);
+        const float dh = dT * c.x * b.w * Topt;
+        const float dTdnu = nu_paper ? -c.x * t * b.w * Topt
+                                     : T * (-0.34657359027997264f * lg - __fdividef(c.x * t * b.w, opt));
+        vals[9] = dT * dTdnu;
+        const float dx = px - a.x, dy = py - a.y;
+        vals[0] = -dh * (2.f * a.z * dx + a.w * dy);
+        vals[1] = -dh * (a.w * dx + 2.f * b.x * dy);
+        vals[2] = dh * dx * dx;
+        vals[3] = 2.f * dh * dx * dy;
+        vals[4] = dh * dy * dy;
+      }
+      const float r = warp_reduce16(vals, lane);
+      const int idx = (lane >> 1) & 15;
+      if (!(lane & 1) && idx < 10) atomicAdd(&acc[j * SSS_G2D_FLOATS + idx], r);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += kRasterThreads) {
+      const float4* q = reinterpret_cast<const float4*>(acc + k * SSS_G2D_FLOATS);
+      const float4 q0 = q[0], q1 = q[1], q2 = q[2];
+      const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) |
+                      (q1.y != 0.f) | (q1.z != 0.f) | (q1.w != 0.f) | (q2.x != 0.f) | (q2.y != 0.f);
+      if (nz) {
+        float4* dst = gv + (int64_t)sid[k] * 3;
+        atomicAdd(dst + 0, q0);
+        atomicAdd(dst + 1, q1);
+        atomicAdd(dst + 2, make_float4(q2.x, q2.y, 0.f, 0.f));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ a5
+__device__ __forceinline__ void sh_basis_f(int deg, float x, float y, float z, float* Y) {
+  Y[0] = 0.28209479177387814f;
+  if (deg >= 1) {
+    Y[1] = -0.4886025119029199f * y;
+    Y[2] = 0.4886025119029199f * z;
+    Y[3] = -0.4886025119029199f * x;
+  }
+  if (deg >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = 1.0925484305920792f * x * y;
+    Y[5] = -1.0925484305920792f * y * z;
+    Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * x * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
+  }
+  if (deg >= 3) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    Y[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+    Y[10] = 2.890611442640554f * x * y * z;
+    Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+    Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+    Y[14] = 1.445305721320277f * z * (xx - yy);
+    Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+  }
+}
+
+// sum_m coef_m * dY_m/d(x,y,z), coef_m = sum_c gdc_c sh_{m,c}
+__device__ __forceinline__ void sh_dir_grad(int deg, float x, float y, float z, const float* coef, float g[3]) {
+  g[0] = g[1] = g[2] = 0.f;
+  if (deg < 1) return;
+  const float c1 = 0.4886025119029199f;
+  g[1] += -c1 * coef[1];
+  g[2] += c1 * coef[2];
+  g[0] += -c1 * coef[3];
+  if (deg < 2) return;
+  const float c20 = 1.0925484305920792f, c22 = 0.31539156525252005f, c24 = 0.5462742152960396f;
+  g[0] += c20 * y * coef[4];  g[1] += c20 * x * coef[4];
+  g[1] += -c20 * z * coef[5]; g[2] += -c20 * y * coef[5];
+  g[0] += -2.f * c22 * x * coef[6]; g[1] += -2.f * c22 * y * coef[6]; g[2] += 4.f * c22 * z * coef[6];
+  g[0] += -c20 * z * coef[7]; g[2] += -c20 * x * coef[7];
+  g[0] += 2.f * c24 * x * coef[8]; g[1] += -2.f * c24 * y * coef[8];
+  if (deg < 3) return;
+  const float c30 = 0.5900435899266435f, c31 = 2.890611442640554f, c32 = 0.4570457994644658f;
+  const float c33 = 0.3731763325901154f, c35 = 1.445305721320277f;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  g[0] += -6.f * c30 * x * y * coef[9];
+  g[1] += -c30 * (3.f * xx - 3.f * yy) * coef[9];
+  g[0] += c31 * y * z * coef[10]; g[1] += c31 * x * z * coef[10]; g[2] += c31 * x * y * coef[10];
+  g[0] += 2.f * c32 * x * y * coef[11];
+  g[1] += -c32 * (4.f * zz - xx - 3.f * yy) * coef[11];
+  g[2] += -8.f * c32 * y * z * coef[11];
+  g[0] += -6.f * c33 * x * z * coef[12];
+  g[1] += -6.f * c33 * y * z * coef[12];
+  g[2] += c33 * (6.f * zz - 3.f * xx - 3.f * yy) * coef[12];
+  g[0] += -c32 * (4.f * zz - 3.f * xx - yy) * coef[13];
+  g[1] += 2.f * c32 * x * y * coef[13];
+  g[2] += -8.f * c32 * x * z * coef[13];
+  g[0] += 2.f * c35 * x * z * coef[14];
+  g[1] += -2.f * c35 * y * z * coef[14];
+  g[2] += c35 * (xx - yy) * coef[14];
+  g[0] += -c30 * (3.f * xx - 3.f * yy) * coef[15];
+  g[1] += 6.f * c30 * x * y * coef[15];
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(128) project_bwd_kernel(sss_params P, const __grid_constant__ CamPack cp,
+                                                           int nv, int v0, float4* __restrict__ g2d,
+                                                           sss_params Gd) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t n = P.n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float mu[3], s[3], q[4];
+  for (int k = 0; k < 3; ++k) mu[k] = P.mean[k * n + i];
+  for (int k = 0; k < 3; ++k) s[k] = P.log_scale[k * n + i];
+  for (int k = 0; k < 4; ++k) q[k] = P.rot[k * n + i];
+  const float raw_nu = P.raw_nu[i], raw_o = P.raw_opacity[i];
+  float sh[3 * K];
+#pragma unroll
+  for (int k = 0; k < 3 * K; ++k) sh[k] = P.sh[k * n + i];
+  // view-independent
+  const float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const float qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
+  float R[9];
+  R[0] = 1.f - 2.f * (qy * qy + qz * qz);
+  R[1] = 2.f * (qx * qy - qw * qz);
+  R[2] = 2.f * (qx * qz + qw * qy);
+  R[3] = 2.f * (qx * qy + qw * qz);
+  R[4] = 1.f - 2.f * (qx * qx + qz * qz);
+  R[5] = 2.f * (qy * qz - qw * qx);
+  R[6] = 2.f * (qx * qz - qw * qy);
+  R[7] = 2.f * (qy * qz + qw * qx);
+  R[8] = 1.f - 2.f * (qx * qx + qy * qy);
+  const float S[3] = {expf(s[0]), expf(s[1]), expf(s[2])};
+  float M[9], Sig[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) M[a * 3 + b] = R[a * 3 + b] * S[b];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      Sig[a * 3 + b] = M[a * 3 + 0] * M[b * 3 + 0] + M[a * 3 + 1] * M[b * 3 + 1] + M[a * 3 + 2] * M[b * 3 + 2];
+
+  float gSig[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float gmu[3] = {0.f, 0.f, 0.f};
+  float gsh[3 * K];
+#pragma unroll
+  for (int k = 0; k < 3 * K; ++k) gsh[k] = 0.f;
+  float g_o = 0.f, g_nu = 0.f;
+  bool any = false;
+
+  for (int vv = 0; vv < nv; ++vv) {
+    float4* gp = g2d + ((int64_t)(v0 + vv) * n + i) * 3;
+    const float4 G0 = gp[0], G1 = gp[1], G2 = gp[2];
+    const bool nz = (G0.x != 0.f) | (G0.y != 0.f) | (G0.z != 0.f) | (G0.w != 0.f) | (G1.x != 0.f) |
+                    (G1.y != 0.f) | (G1.z != 0.f) | (G1.w != 0.f) | (G2.x != 0.f) | (G2.y != 0.f);
+    if (!nz) continue;
+    any = true;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    gp[0] = z4; gp[1] = z4; gp[2] = z4;  // consume-and-clear (workspace stays zero)
+    const DevCamera& cam = cp.cam[vv];
+    float p[3];
+    for (int a = 0; a < 3; ++a) p[a] = cam.R[a * 3 + 0] * mu[0] + cam.R[a * 3 + 1] * mu[1] + cam.R[a * 3 + 2] * mu[2] + cam.t[a];
+    const float px = p[0], py = p[1], pz = p[2];
+    const float iz = 1.f / pz;
+    const float J00 = cam.fx * iz, J02 = -cam.fx * px * iz * iz, J11 = cam.fy * iz, J12 = -cam.fy * py * iz * iz;
+    // Sc = Rc Sig Rc^T
+    float T1[9], Sc[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        T1[a * 3 + b] = cam.R[a * 3 + 0] * Sig[0 * 3 + b] + cam.R[a * 3 + 1] * Sig[1 * 3 + b] + cam.R[a * 3 + 2] * Sig[2 * 3 + b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        Sc[a * 3 + b] = T1[a * 3 + 0] * cam.R[b * 3 + 0] + T1[a * 3 + 1] * cam.R[b * 3 + 1] + T1[a * 3 + 2] * cam.R[b * 3 + 2];
+    // J (2x3) with J01 = J10 = 0
+    const float J[6] = {J00, 0.f, J02, 0.f, J11, J12};
+    float K2[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) K2[a * 3 + b] = J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b] + J[a * 3 + 2] * Sc[2 * 3 + b];
+    const float cxx = K2[0] * J[0] + K2[2] * J[2];
+    const float cxy = K2[1] * J[4] + K2[2] * J[5];
+    const float cyy = K2[4] * J[4] + K2[5] * J[5];
+    const float idet = 1.f / (cxx * cyy - cxy * cxy);
+    const float QA = cyy * idet, QB = -cxy * idet, QC = cxx * idet;
+    // G_S = -Q G_Q Q with G_Q = [[dA, dB/2], [dB/2, dC]]
+    const float gA = G0.z, gB = 0.5f * G0.w, gC = G1.x;
+    const float QG00 = QA * gA + QB * gB, QG01 = QA * gB + QB * gC;
+    const float QG10 = QB * gA + QC * gB, QG11 = QB * gB + QC * gC;
+    const float GS00 = -(QG00 * QA + QG01 * QB);
+    const float GS01 = -(QG00 * QB + QG01 * QC);
+    const float GS11 = -(QG10 * QB + QG11 * QC);
+    const float GS[4] = {GS00, GS01, GS01, GS11};
+    // dL/dSc = J^T GS J ; dL/dJ = 2 GS J Sc
+    float GSc[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        float acc = 0.f;
+        for (int k = 0; k < 2; ++k)
+          for (int l = 0; l < 2; ++l) acc += J[k * 3 + a] * GS[k * 2 + l] * J[l * 3 + b];
+        GSc[a * 3 + b] = acc;
+      }
+    float JS[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) JS[a * 3 + b] = J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b] + J[a * 3 + 2] * Sc[2 * 3 + b];
+    float GJ[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) GJ[a * 3 + b] = 2.f * (GS[a * 2 + 0] * JS[0 * 3 + b] + GS[a * 2 + 1] * JS[1 * 3 + b]);
+    // dL/dSigma += Rc^T GSc Rc
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        float acc = 0.f;
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) acc += cam.R[k * 3 + a] * GSc[k * 3 + l] * cam.R[l * 3 + b];
+        gSig[a * 3 + b] += acc;
+      }
+    // camera-space mean through mean2d and J(p)
+    const float dmx = G0.x, dmy = G0.y;
+    const float iz2 = iz * iz, iz3 = iz2 * iz;
+    float dp0 = cam.fx * iz * dmx + GJ[2] * (-cam.fx * iz2);
+    float dp1 = cam.fy * iz * dmy + GJ[5] * (-cam.fy * iz2);
+    float dp2 = -cam.fx * px * iz2 * dmx - cam.fy * py * iz2 * dmy + GJ[0] * (-cam.fx * iz2) +
+                GJ[4] * (-cam.fy * iz2) + GJ[2] * (2.f * cam.fx * px * iz3) + GJ[5] * (2.f * cam.fy * py * iz3);
+    for (int a = 0; a < 3; ++a) gmu[a] += cam.R[0 * 3 + a] * dp0 + cam.R[1 * 3 + a] * dp1 + cam.R[2 * 3 + a] * dp2;
+    // SH colour (clamp mask) and view direction
+    float dvec[3] = {mu[0] - cam.center[0], mu[1] - cam.center[1], mu[2] - cam.center[2]};
+    const float dist = sqrtf(dvec[0] * dvec[0] + dvec[1] * dvec[1] + dvec[2] * dvec[2]);
+    const float idist = 1.f / dist;
+    const float dx = dvec[0] * idist, dy = dvec[1] * idist, dz = dvec[2] * idist;
+    float Y[16];
+    sh_basis_f(DEG, dx, dy, dz, Y);
+    float gdc[3] = {G1.y, G1.z, G1.w};
+    for (int c = 0; c < 3; ++c) {
+      float pre = 0.5f;
+      for (int mm = 0; mm < K; ++mm) pre += sh[mm * 3 + c] * Y[mm];
+      if (!(pre > 0.f)) gdc[c] = 0.f;
+    }
+#pragma unroll
+    for (int mm = 0; mm < K; ++mm)
+      for (int c = 0; c < 3; ++c) gsh[mm * 3 + c] += gdc[c] * Y[mm];
+    if (DEG > 0) {
+      float coef[16];
+      for (int mm = 0; mm < K; ++mm) coef[mm] = gdc[0] * sh[mm * 3 + 0] + gdc[1] * sh[mm * 3 + 1] + gdc[2] * sh[mm * 3 + 2];
+      float gd[3];
+      sh_dir_grad(DEG, dx, dy, dz, coef, gd);
+      const float dd = gd[0] * dx + gd[1] * dy + gd[2] * dz;
+      gmu[0] += (gd[0] - dx * dd) * idist;
+      gmu[1] += (gd[1] - dy * dd) * idist;
+      gmu[2] += (gd[2] - dz * dd) * idist;
+    }
+    g_o += G2.x;
+    g_nu += G2.y;
+  }
+  if (!any) return;
+  // Sigma = M M^T, M = R S
+  float GM[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) GM[a * 3 + b] = 2.f * (gSig[a * 3 + 0] * M[0 * 3 + b] + gSig[a * 3 + 1] * M[1 * 3 + b] + gSig[a * 3 + 2] * M[2 * 3 + b]);
+  float gls[3];
+  for (int b = 0; b < 3; ++b) gls[b] = (GM[0 * 3 + b] * R[0 * 3 + b] + GM[1 * 3 + b] * R[1 * 3 + b] + GM[2 * 3 + b] * R[2 * 3 + b]) * S[b];
+  float GR[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) GR[a * 3 + b] = GM[a * 3 + b] * S[b];
+  float gq[4];
+  gq[0] = 2.f * (-qz * GR[1] + qy * GR[2] + qz * GR[3] - qx * GR[5] - qy * GR[6] + qx * GR[7]);
+  gq[1] = 2.f * (qy * GR[1] + qz * GR[2] + qy * GR[3] - 2.f * qx * GR[4] - qw * GR[5] + qz * GR[6] + qw * GR[7] - 2.f * qx * GR[8]);
+  gq[2] = 2.f * (-2.f * qy * GR[0] + qx * GR[1] + qw * GR[2] + qx * GR[3] + qz * GR[5] - qw * GR[6] + qz * GR[7] - 2.f * qy * GR[8]);
+  gq[3] = 2.f * (-2.f * qz * GR[0] - qw * GR[1] + qx * GR[2] + qw * GR[3] - 2.f * qz * GR[4] + qy * GR[5] + qx * GR[6] + qy * GR[7]);
+  const float dotq = gq[0] * qw + gq[1] * qx + gq[2] * qy + gq[3] * qz;
+  const float qh[4] = {qw, qx, qy, qz};
+  // reparameterisations
+  const float o = tanhf(raw_o);
+  const float sp = raw_nu > 30.f ? raw_nu : log1pf(expf(raw_nu));
+  const float dnu = (1.f + sp >= (float)kNuMax) ? 0.f : 1.f / (1.f + expf(-raw_nu));
+  for (int a = 0; a < 3; ++a) Gd.mean[a * n + i] += gmu[a];
+  for (int a = 0; a < 3; ++a) Gd.log_scale[a * n + i] += gls[a];
+  for (int a = 0; a < 4; ++a) Gd.rot[a * n + i] += (gq[a] - qh[a] * dotq) / qn;
+  Gd.raw_nu[i] += g_nu * dnu;
+  Gd.raw_opacity[i] += g_o * (1.f - o * o);
+#pragma unroll
+  for (int k = 0; k < 3 * K; ++k) Gd.sh[k * n + i] += gsh[k];
+}
+
+}  // namespace
+}  // namespace sss
+
+using namespace sss;
+
+extern "C" size_t sss_render_bwd_workspace(int64_t n, int32_t n_views) {
+  if (n < 0 || n_views <= 0) return 0;
+  return (size_t)n * n_views * SSS_G2D_FLOATS * sizeof(float);
+}
+
+extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, const sss_bins* bins,
+                                     const sss_camera* cams, int32_t n_views, const float* bg,
+                                     const sss_frame* fwd, const float* d_rgb, const float* target,
+                                     float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
+                                     int32_t flags, void* stream) {
+  sss_status st;
+  if ((st = validate_params(p, "sss_render_bwd")) != SSS_OK) return st;
+  if ((st = validate_params(grad, "sss_render_bwd(grad)")) != SSS_OK) return st;
+  if ((st = validate_cams(cams, n_views, "sss_render_bwd")) != SSS_OK) return st;
+  if (!pr || !bins || !fwd || !bg) { set_error("sss_render_bwd: null argument"); return SSS_ERR_ARG; }
+  if (grad->n != p->n || grad->sh_degree != p->sh_degree || pr->n != p->n) {
+    set_error("sss_render_bwd: n / sh_degree mismatch");
+    return SSS_ERR_ARG;
+  }
+  if (!d_rgb && !target) { set_error("sss_render_bwd: need d_rgb or target"); return SSS_ERR_ARG; }
+  RasterGeom G;
+  if (!raster_geom(pr, bins, cams, n_views, G)) { set_error("sss_render_bwd: geometry mismatch"); return SSS_ERR_SHAPE; }
+  const size_t need = sss_render_bwd_workspace(p->n, n_views);
+  if (ws_bytes < need || (need > 0 && !ws)) {
+    set_error("sss_render_bwd: workspace %zu < %zu bytes", ws_bytes, need);
+    return SSS_ERR_ARG;
+  }
+  if (!fwd->rgb || !fwd->final_T || !fwd->last) { set_error("sss_render_bwd: null frame buffer"); return SSS_ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  float4* g2d = (float4*)ws;
+  const dim3 grid(G.tiles_x * G.tiles_y, n_views);
+  const float4* rec = (const float4*)pr->rec;
+  const short4* rect = (const short4*)pr->rect;
+#define SSS_BWD_LAUNCH(F, L)                                                                              \
+  render_bwd_kernel<F, L><<<grid, kRasterThreads, 0, s>>>(rec, rect, bins->ids, bins->ranges, G, bg[0], \
+                                                          bg[1], bg[2], fwd->rgb, fwd->final_T,         \
+                                                          fwd->last, d_rgb, target, loss_out, g2d, flags)
+  const bool l1 = d_rgb == nullptr;
+  if (G.shift > 0) {
+    if (l1) SSS_BWD_LAUNCH(true, true); else SSS_BWD_LAUNCH(true, false);
+  } else {
+    if (l1) SSS_BWD_LAUNCH(false, true); else SSS_BWD_LAUNCH(false, false);
+  }
+#undef SSS_BWD_LAUNCH
+  count_launch();
+  if ((st = check_launch("sss_render_bwd(raster)")) != SSS_OK) return st;
+  if (p->n == 0) return SSS_OK;
+  const int threads = 128;
+  const int blocks = div_up(p->n, threads);
+  for (int v0 = 0; v0 < n_views; v0 += kMaxViewsPerLaunch) {
+    const int nv = n_views - v0 < kMaxViewsPerLaunch ? n_views - v0 : kMaxViewsPerLaunch;
+    CamPack cp;
+    fill_campack(cams, v0, nv, cp);
+    switch (p->sh_degree) {
+      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
+      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
+      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
+      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
+    }
+    count_launch();
+    if ((st = check_launch("sss_render_bwd(projection)")) != SSS_OK) return st;
+  }
+  return SSS_OK;
+}

@@ -1,0 +1,147 @@
+// a7 — sss_sghmc_step: gated SGHMC on the means + Adam on every other group,
+// one fused elementwise pass over the parameter, gradient, moment and
+// momentum planes (Eq. 10; SM one-step form and sigmoid
+// switch PAPER.md:1502-1521; burn-in PAPER.md:163, 1523; Adam PAPER.md:152,
+// 1083, 1514).  Readings R14-R19:
+//   g     = grad * grad_scale
+//   r'    = (1 - eps C) r - eps g + (eta / eps) xi
+//   mu'   = mu - eps^2 g + gate (F + N),  F = eps (1 - eps C) r,  N = eta xi
+//   gate  = sigmoid(-k (|o| - t))
+//   burn-in: F = 0, N = eta Sigma xi (Sigma of the pre-update component)
+//   Adam: m' = b1 m + (1-b1) g, v' = b2 v + (1-b2) g^2,
+//         theta -= lr (m'/(1-b1^t)) / (sqrt(v'/(1-b2^t)) + eps_hat)
+// xi: three standard normals from Philox4x32-10 (cuRAND's device function),
+// key = seed, counter = (i, step); uniforms ((x >> 8) + 1/2) 2^-24 and
+// Box-Muller in fp64 (R14).  Identical on every rank, so data-parallel
+// replicas stay bit-identical without a broadcast.
+// HBM-bound: 4 x 240 B read + 3 x 240 B written + 24 B momentum per
+// component at SH degree 3 (~1.7 KB).
+#include <curand_philox4x32_x.h>
+
+#include "common.cuh"
+
+namespace sss {
+namespace {
+
+struct HP {
+  float lr, friction, noise, gate_k, gate_t;
+  int burn_in, g_adam;
+  float lr_group[5];  // log_scale, rot, nu, opacity, sh
+  float beta1, beta2, adam_eps, grad_scale;
+  float inv_b1t, inv_b2t;  // 1 / (1 - beta^t)
+  uint32_t ctr2, ctr3;     // step (lo, hi)
+  uint32_t key0, key1;     // seed (lo, hi)
+};
+
+__device__ __forceinline__ float adam_dir(float g, float* m, float* v, int64_t idx, const HP& hp) {
+  const float mm = hp.beta1 * m[idx] + (1.f - hp.beta1) * g;
+  const float vv = hp.beta2 * v[idx] + (1.f - hp.beta2) * g * g;
+  m[idx] = mm;
+  v[idx] = vv;
+  return (mm * hp.inv_b1t) / (sqrtf(vv * hp.inv_b2t) + hp.adam_eps);
+}
+
+__device__ __forceinline__ void adam_plane(float* theta, const float* grad, float* m, float* v, int64_t i,
+                                           float lr, const HP& hp) {
+  const float g = grad[i] * hp.grad_scale;
+  theta[i] -= lr * adam_dir(g, m, v, i, hp);
+}
+
+__global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr, sss_params Mo,
+                                                    sss_params Vo, float* __restrict__ r, HP hp) {
+  const int64_t n = P.n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int K = (P.sh_degree + 1) * (P.sh_degree + 1);
+  // gate and (burn-in) covariance from the pre-update state
+  const float o = tanhf(P.raw_opacity[i]);
+  const float gate = 1.f / (1.f + expf(hp.gate_k * (fabsf(o) - hp.gate_t)));
+  float Sig[9];
+  if (hp.burn_in) {
+    float q[4], s[3];
+    for (int k = 0; k < 4; ++k) q[k] = P.rot[k * n + i];
+    for (int k = 0; k < 3; ++k) s[k] = P.log_scale[k * n + i];
+    const float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const float w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    const float R[9] = {1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y),
+                        2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x),
+                        2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
+    const float e2[3] = {expf(2.f * s[0]), expf(2.f * s[1]), expf(2.f * s[2])};
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        Sig[a * 3 + b] = R[a * 3 + 0] * e2[0] * R[b * 3 + 0] + R[a * 3 + 1] * e2[1] * R[b * 3 + 1] +
+                         R[a * 3 + 2] * e2[2] * R[b * 3 + 2];
+  }
+  // noise xi ~ N(0, I3)
+  const uint4 x = curand_Philox4x32_10(make_uint4((uint32_t)i, (uint32_t)((uint64_t)i >> 32), hp.ctr2, hp.ctr3),
+                                       make_uint2(hp.key0, hp.key1));
+  const double u0 = ((double)(x.x >> 8) + 0.5) * (1.0 / 16777216.0);
+  const double u1 = ((double)(x.y >> 8) + 0.5) * (1.0 / 16777216.0);
+  const double u2 = ((double)(x.z >> 8) + 0.5) * (1.0 / 16777216.0);
+  const double u3 = ((double)(x.w >> 8) + 0.5) * (1.0 / 16777216.0);
+  const double r0 = sqrt(-2.0 * log(u0)), r1 = sqrt(-2.0 * log(u2));
+  double s1, c1, s3, c3;
+  sincospi(2.0 * u1, &s1, &c1);
+  sincospi(2.0 * u3, &s3, &c3);
+  const float xi[3] = {(float)(r0 * c1), (float)(r0 * s1), (float)(r1 * c3)};
+  // ---- mean: gated SGHMC
+  const float eps = hp.lr, Cf = hp.friction, eta = hp.noise;
+  float noise[3];
+  if (hp.burn_in) {
+    for (int a = 0; a < 3; ++a) noise[a] = eta * (Sig[a * 3 + 0] * xi[0] + Sig[a * 3 + 1] * xi[1] + Sig[a * 3 + 2] * xi[2]);
+  } else {
+    for (int a = 0; a < 3; ++a) noise[a] = eta * xi[a];
+  }
+  for (int a = 0; a < 3; ++a) {
+    const int64_t idx = a * n + i;
+    const float graw = Gr.mean[idx] * hp.grad_scale;
+    const float g = hp.g_adam ? adam_dir(graw, Mo.mean, Vo.mean, idx, hp) : graw;
+    const float ra = r[idx];
+    const float F = hp.burn_in ? 0.f : eps * (1.f - eps * Cf) * ra;
+    P.mean[idx] = P.mean[idx] - eps * eps * g + gate * (F + noise[a]);
+    r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
+  }
+  // ---- Adam on the other groups
+  for (int a = 0; a < 3; ++a) adam_plane(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, a * n + i, hp.lr_group[0], hp);
+  for (int a = 0; a < 4; ++a) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
+  adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
+  adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp);
+  for (int k = 0; k < 3 * K; ++k) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
+}
+
+}  // namespace
+}  // namespace sss
+
+using namespace sss;
+
+extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_params* adam_m,
+                                     sss_params* adam_v, float* momentum, const sss_sghmc_hparams* h,
+                                     void* stream) {
+  sss_status st;
+  if ((st = validate_params(p, "sss_sghmc_step")) != SSS_OK) return st;
+  if ((st = validate_params(grad, "sss_sghmc_step(grad)")) != SSS_OK) return st;
+  if ((st = validate_params(adam_m, "sss_sghmc_step(m)")) != SSS_OK) return st;
+  if ((st = validate_params(adam_v, "sss_sghmc_step(v)")) != SSS_OK) return st;
+  if (!h || (!momentum && p->n > 0)) { set_error("sss_sghmc_step: null hparams / momentum"); return SSS_ERR_ARG; }
+  if (grad->n != p->n || adam_m->n != p->n || adam_v->n != p->n || grad->sh_degree != p->sh_degree ||
+      adam_m->sh_degree != p->sh_degree || adam_v->sh_degree != p->sh_degree) {
+    set_error("sss_sghmc_step: n / sh_degree mismatch");
+    return SSS_ERR_ARG;
+  }
+  if (h->step < 1 || !(h->lr > 0.f)) { set_error("sss_sghmc_step: step must be >= 1 and lr > 0"); return SSS_ERR_ARG; }
+  if (p->n == 0) return SSS_OK;
+  HP hp;
+  hp.lr = h->lr; hp.friction = h->friction; hp.noise = h->noise; hp.gate_k = h->gate_k; hp.gate_t = h->gate_t;
+  hp.burn_in = h->burn_in; hp.g_adam = h->g_adam;
+  hp.lr_group[0] = h->lr_scale; hp.lr_group[1] = h->lr_rot; hp.lr_group[2] = h->lr_nu;
+  hp.lr_group[3] = h->lr_opacity; hp.lr_group[4] = h->lr_sh;
+  hp.beta1 = h->beta1; hp.beta2 = h->beta2; hp.adam_eps = h->adam_eps; hp.grad_scale = h->grad_scale;
+  hp.inv_b1t = (float)(1.0 / (1.0 - pow((double)h->beta1, (double)h->step)));
+  hp.inv_b2t = (float)(1.0 / (1.0 - pow((double)h->beta2, (double)h->step)));
+  hp.ctr2 = (uint32_t)h->step; hp.ctr3 = (uint32_t)((uint64_t)h->step >> 32);
+  hp.key0 = (uint32_t)h->seed; hp.key1 = (uint32_t)(h->seed >> 32);
+  cudaStream_t s = (cudaStream_t)stream;
+  sghmc_kernel<<<div_up(p->n, 256), 256, 0, s>>>(*p, *grad, *adam_m, *adam_v, momentum, hp);
+  count_launch();
+  return check_launch("sss_sghmc_step");
+}

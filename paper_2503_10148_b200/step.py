@@ -1,0 +1,124 @@
+"""One SSS training iteration on the CUDA path (SURVEY.md §3 call stack 2).
+
+For each batch of this rank's views: sss_project -> sss_bin_sort ->
+sss_render_fwd -> sss_render_bwd (fused L1, gradients accumulated over
+views); then the NCCL all-reduce of the flat gradient buffer (R > 1) and
+sss_sghmc_step with grad_scale = 1/V (R26).  All calls are asynchronous on
+one stream; the only host synchronisation is the loss / overflow read-back
+the caller asks for.  Buffers are allocated once and reused (the bin
+capacity is sized from a measured instance count with headroom; an
+overflow is detected from the device flag and the iteration replayed with a
+larger buffer).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import api as A
+from . import dist as D
+
+
+class TrainStep:
+    def __init__(self, planes: torch.Tensor, sh_degree: int, cameras: Sequence, hp,
+                 total_views: Optional[int] = None, bin_shift: int = 0,
+                 views_per_batch: int = 16, bg=(0.0, 0.0, 0.0), headroom: float = 1.25,
+                 group=None, momentum: Optional[torch.Tensor] = None,
+                 adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None):
+        dev = planes.device
+        self.params = A.Params(planes, sh_degree)
+        self.grad = A.Params.zeros_like(self.params)
+        self.m = A.Params(adam_m if adam_m is not None else torch.zeros_like(planes), sh_degree)
+        self.v = A.Params(adam_v if adam_v is not None else torch.zeros_like(planes), sh_degree)
+        n = self.params.n
+        self.r = momentum if momentum is not None else torch.zeros((3, n), device=dev)
+        self.hp = hp
+        self.cams = list(cameras)
+        self.total_views = int(total_views if total_views is not None else len(self.cams))
+        self.bin_shift = int(bin_shift)
+        self.bg = tuple(float(x) for x in bg)
+        self.headroom = headroom
+        self.group = group
+        self.t = int(getattr(hp, "step", 1))
+        vb = max(1, min(int(views_per_batch), len(self.cams)))
+        self.batches: List[List[int]] = [list(range(i, min(i + vb, len(self.cams))))
+                                         for i in range(0, len(self.cams), vb)]
+        self.cams_c = [A.cameras_c([self.cams[v] for v in b]) for b in self.batches]
+        W, H = int(self.cams[0].width), int(self.cams[0].height)
+        self.W, self.H = W, H
+        self.proj = A.Projected.empty(n, vb, dev)
+        self.frame = A.Frame.empty(vb, H, W, dev)
+        self.n_bins = A.n_bins_of(W, H, self.bin_shift)
+        need = max(A.bin_sort_workspace_bytes(n, [self.cams[0]] * vb, self.bin_shift), 1)
+        self.ws_bin = torch.empty(need, dtype=torch.uint8, device=dev)
+        self.ws_g2d = torch.zeros(max(A.render_bwd_workspace_bytes(n, vb), 4), dtype=torch.uint8,
+                                  device=dev)
+        self.loss = torch.zeros(1, device=dev)
+        self.bins: List[A.Bins] = []
+        self._size_bins()
+
+    # -- bin capacity ------------------------------------------------------
+    def _size_bins(self, factor: float = 1.0):
+        """Measure the per-view instance count of every batch (host sync)."""
+        cap = 0
+        for bi, b in enumerate(self.batches):
+            cams = [self.cams[v] for v in b]
+            pv = self._proj_view(len(b))
+            A.sss_project(self.params, cams, out=pv, cams_c=self.cams_c[bi])
+            probe = A.Bins.empty(len(b), self.n_bins, 0, self.bin_shift, False, self.params.planes.device)
+            A.sss_bin_sort(pv, cams, bin_shift=self.bin_shift, ws=self.ws_bin, out=probe,
+                           cams_c=self.cams_c[bi])
+            cap = max(cap, int(probe.totals.max().item()))
+        cap = int(cap * self.headroom * factor) + 4096
+        vb = len(self.batches[0])
+        self.bins = [A.Bins.empty(vb, self.n_bins, cap, self.bin_shift, False,
+                                  self.params.planes.device)]
+        self.capacity = cap
+
+    def _proj_view(self, nv: int) -> A.Projected:
+        return A.Projected(self.proj.rec[:nv], self.proj.depth[:nv], self.proj.rect[:nv])
+
+    def _frame_view(self, nv: int) -> A.Frame:
+        f = self.frame
+        return A.Frame(f.rgb[:nv], f.final_T[:nv], f.n_contrib[:nv], f.last[:nv])
+
+    def _bins_view(self, nv: int) -> A.Bins:
+        b = self.bins[0]
+        return A.Bins(b.bin_shift, b.capacity, b.ids[:nv], None, b.ranges[:nv], b.totals[:nv],
+                      b.overflow)
+
+    # -- the iteration -----------------------------------------------------
+    def forward_backward(self, targets: torch.Tensor) -> None:
+        """Render this rank's views and accumulate grad (no optimizer step).
+        targets: [V_local][3][H][W] fp32 device tensor."""
+        self.grad.planes.zero_()
+        self.loss.zero_()
+        for bi, b in enumerate(self.batches):
+            nv = len(b)
+            cams = [self.cams[v] for v in b]
+            cc = self.cams_c[bi]
+            pv, fv, bv = self._proj_view(nv), self._frame_view(nv), self._bins_view(nv)
+            A.sss_project(self.params, cams, out=pv, cams_c=cc)
+            A.sss_bin_sort(pv, cams, bin_shift=self.bin_shift, ws=self.ws_bin, out=bv, cams_c=cc)
+            A.sss_render_fwd(pv, bv, cams, bg=self.bg, out=fv, cams_c=cc)
+            A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg,
+                             target=targets[b[0]:b[-1] + 1], grad=self.grad, loss=self.loss,
+                             ws=self.ws_g2d, cams_c=cc)
+
+    def step(self, targets: torch.Tensor) -> torch.Tensor:
+        """One full iteration; returns the (device) loss of this rank."""
+        self.forward_backward(targets)
+        D.allreduce_sum_(self.grad.planes, self.group)
+        self.hp.step = self.t
+        self.hp.grad_scale = 1.0 / self.total_views
+        A.sss_sghmc_step(self.params, self.grad, self.m, self.v, self.r, self.hp)
+        self.t += 1
+        return self.loss
+
+    def overflowed(self) -> bool:
+        """Synchronising check of the bin overflow flag."""
+        return bool(self.bins[0].overflow.item())
+
+    def grow(self):
+        self._size_bins(factor=1.5)

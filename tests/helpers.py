@@ -13,6 +13,8 @@ Y00 = 0.5 / math.sqrt(math.pi)
 def raw_nu_for(nu):
     if nu <= 1.0:
         return -50.0  # softplus(-50) ~ 2e-22: nu == 1 in fp64
+    if nu - 1.0 > 30.0:
+        return nu - 1.0  # softplus(x) = x there (R1)
     return math.log(math.expm1(nu - 1.0))
 
 

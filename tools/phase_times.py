@@ -1,0 +1,48 @@
+"""Per-phase CUDA-event timing of the hot path on one config (dev tool)."""
+import argparse, json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2503_10148_b200 as P
+from paper_2503_10148_b200 import api as A
+from sss_synth import make_scene, make_targets
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--views", type=int, default=None)
+ap.add_argument("--shift", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+sc = make_scene(a.config, n_views=a.views)
+cams = sc.cameras
+V = len(cams)
+params = P.Params(torch.from_numpy(sc.params).cuda(), sc.sh_degree)
+tgt = torch.from_numpy(make_targets(sc)).cuda()
+pr = P.sss_project(params, cams)
+bins = P.sss_bin_sort(pr, cams, bin_shift=a.shift)
+fr = P.sss_render_fwd(pr, bins, cams)
+ws_g2d = torch.zeros(A.render_bwd_workspace_bytes(params.n, V), dtype=torch.uint8, device="cuda")
+ws_bin = torch.empty(A.bin_sort_workspace_bytes(params.n, cams, a.shift), dtype=torch.uint8, device="cuda")
+grad = P.Params.zeros_like(params)
+loss = torch.zeros(1, device="cuda")
+cc = A.cameras_c(cams)
+phases = {
+  "project": lambda: P.sss_project(params, cams, out=pr, cams_c=cc),
+  "bin_sort": lambda: P.sss_bin_sort(pr, cams, bin_shift=a.shift, ws=ws_bin, out=bins, cams_c=cc),
+  "render_fwd": lambda: P.sss_render_fwd(pr, bins, cams, out=fr, cams_c=cc),
+  "render_bwd": lambda: P.sss_render_bwd(params, pr, bins, cams, fr, target=tgt, grad=grad, loss=loss, ws=ws_g2d, cams_c=cc),
+}
+res = {}
+for name, f in phases.items():
+    f(); torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); f(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    res[name] = min(ts)
+tot = bins.totals.cpu().numpy()
+nc = fr.n_contrib.float()
+out = dict(config=a.config, views=V, shift=a.shift, ms=res, total_ms=sum(res.values()),
+           instances_per_view=float(tot.mean()), capacity=bins.capacity,
+           pairs_per_view=float(nc.sum().item()/V), mean_contrib=float(nc.mean().item()),
+           mpix_per_s=V*cams[0].width*cams[0].height/sum(res.values())/1e3)
+print(json.dumps(out))
