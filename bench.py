@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""SSS hot-path benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (default): BASELINE config 5, the full training-step loop:
+3,000,000 components (SH degree 3), 64 views at 1297x840 on a hemisphere,
+per iteration project -> bin/sort -> composite -> fused-L1 backward over all
+views, NCCL all-reduce of the parameter gradients (N > 1), SGHMC/Adam step.
+A "step" is one such iteration.  `value` is whole-job training iterations/s
+with inputs resident in HBM; `e2e` is the same metric through the public API
+with the step's target images copied host->device (pinned) and the loss read
+back every step.  Views are sharded round-robin over ranks (strong scaling:
+the 64-view iteration is fixed, R ranks share it).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd Mpixel/s and train iters/s at 1/2/4/8 B200; % of FP32/HBM roofline"
+
+# Algorithmic work per unit: FP32 lane-ops per composited
+# pair (forward / backward raster) and bytes per component-view (HBM kernels).
+FWD_OPS_PER_PAIR = 19
+BWD_OPS_PER_PAIR = 62
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--bin-shift", type=int, default=2)
+    ap.add_argument("--views-per-batch", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = {}
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+    return {"hbm_gbs": float(d.get("hbm_gbs", 6650.0)), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+            "source": "measured" if d else "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def roofline_for(phase_ms, counts, n, views, pk, steps):
+    """Roofline entry of the dominant kernel (largest share of the timed step)."""
+    lane_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6  # FP32 lane-ops/s
+    hbm_peak = pk["hbm_gbs"] * 1e9
+    table = {}
+    pairs = counts["pairs"]
+    table["render_fwd"] = ("alu", pairs * FWD_OPS_PER_PAIR, lane_peak, "Glane-op/s")
+    table["render_bwd_raster"] = ("alu", pairs * BWD_OPS_PER_PAIR, lane_peak, "Glane-op/s")
+    P = counts["planes"]
+    # projection: params read once per launch (<=views_per_batch views) + 60 B/view written
+    table["project"] = ("hbm", counts["launches_per_step"] * n * 4 * P + views * n * 60, hbm_peak, "GB/s")
+    # bin/sort: lower bound = 4 B id written per instance + 4 B depth key read per comp-view
+    table["bin_sort"] = ("hbm", counts["instances"] * 4 + views * n * 4, hbm_peak, "GB/s")
+    # projection backward: g2d 48 B read per comp-view + params 240 B + grad RMW 480 B per launch
+    table["render_bwd_projection"] = ("hbm", views * n * 48 + counts["launches_per_step"] * n * 4 * P * 3,
+                                      hbm_peak, "GB/s")
+    table["sghmc"] = ("hbm", n * 4 * (P * 7 + 6), hbm_peak, "GB/s")
+    dom = max((k for k in phase_ms if k in table), key=lambda k: phase_ms[k])
+    bound, work, peak, unit = table[dom]
+    t = phase_ms[dom] / 1e3 / steps  # seconds per step in that kernel (all its launches)
+    achieved = work / t
+    return dom, {"kernel": dom, "bound": bound, "achieved": round(achieved / 1e9, 2),
+                 "peak": round(peak / 1e9, 2), "unit": unit, "frac": round(achieved / peak, 4),
+                 "traffic": None, "peak_source": pk["source"] + (" (148 SMs x 128 FP32 lanes x sm_max_mhz)" if bound == "alu" else " hbm_gbs"),
+                 "share_of_step": round(phase_ms[dom] / sum(phase_ms.values()), 3)}
+
+
+def cpu_baseline_sample(scene, targets_np, budget_s, views_total):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload
+    on this host's cores and extrapolate to it/s (rank 0 only)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    cam = scene.cameras[0]
+    n = scene.n
+    P_ = cam.width * cam.height
+    import ctypes
+
+    t0 = time.time()
+    pp = O._P(scene.params, scene.sh_degree)
+    cc = O._cam(cam)
+    tw, th = O.tiles_of(cam)
+    counts = np.zeros(tw * th, np.int32)
+    O.lib().orc_bin(pp.ref, ctypes.byref(cc), O._ptr(counts), None, None)  # project + bin
+    t_bin = time.time() - t0
+    rng = np.random.default_rng(0)
+    npx = 8192
+    px = rng.choice(P_, npx, replace=False).astype(np.int32)
+    t0 = time.time()
+    fr = O.render(scene.params, scene.sh_degree, cam, mode="tiled", pixels=px)
+    t_fwd = time.time() - t0 - t_bin  # the call re-projects and re-bins the view
+    tgt = targets_np[:, px // cam.width, px % cam.width]
+    d = np.sign(fr.rgb - tgt) / (3 * P_)
+    t0 = time.time()
+    O.backward(scene.params, scene.sh_degree, cam, d, mode="tiled", pixels=px)
+    t_bwd = time.time() - t0 - t_bin
+    t_raster = max(t_fwd, 0.0) + max(t_bwd, 0.0)
+    nsub = min(n, 100000)
+    from sss_synth import make_optimizer_state, sghmc_params_for
+
+    sub = scene.params[:, :nsub]
+    r, m, v = make_optimizer_state(scene, zero=True)
+    t0 = time.time()
+    O.sghmc_step(sub, scene.sh_degree, np.zeros_like(sub), m[:, :nsub], v[:, :nsub], r[:, :nsub],
+                 sghmc_params_for(scene))
+    t_sg = (time.time() - t0) * n / nsub
+    t_iter = views_total * (t_bin + t_raster * P_ / npx) + t_sg
+    return {"value": round(1.0 / t_iter, 8), "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": (f"fp64 C++ oracle on host cores: project+bin of 1 view ({t_bin:.1f}s), "
+                       f"fwd+bwd of {npx} random pixels of that view ({t_raster:.1f}s, scaled x{P_ // npx}), "
+                       f"SGHMC on {nsub} comps (scaled x{n / nsub:.0f}); x{views_total} views; extrapolated"),
+            "seconds_per_iter": round(t_iter, 1)}
+
+
+def run_reference(a):
+    """--impl reference: the oracle, timed as it stands, on bounded samples."""
+    rank, world, local = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+    if rank != 0:
+        return 0
+    from sss_synth import CONFIG_NAMES, make_scene, make_targets
+
+    sc = make_scene(a.config)
+    tg = make_targets(sc, [0])[0]
+    vals = []
+    for k in range(a.warmup + a.steps):
+        cb = cpu_baseline_sample(sc, tg, a.cpu_budget_s, sc.n_views)
+        if k >= a.warmup:
+            vals.append(cb["value"])
+    v = sum(vals) / len(vals)
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "it/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 / v, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": CONFIG_NAMES[a.config]},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import numpy as np
+    import torch
+
+    import paper_2503_10148_b200 as P
+    from paper_2503_10148_b200 import dist as D
+    from paper_2503_10148_b200.step import TrainStep
+    from sss_synth import CONFIG_NAMES, make_scene, make_targets, sghmc_params_for
+
+    rank, world, local = D.init()
+    torch.cuda.set_device(local)
+    P.load()
+    sc = make_scene(a.config)
+    V = sc.n_views
+    mine = D.shard_views(V, rank, world)
+    cams = [sc.cameras[v] for v in mine]
+    tg_np = make_targets(sc, mine)
+    targets = torch.from_numpy(tg_np).cuda()
+    planes = torch.from_numpy(sc.params).cuda()
+    hp = sghmc_params_for(sc)
+    ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
+                   views_per_batch=a.views_per_batch)
+    for _ in range(a.warmup):
+        ts.step(targets)
+        if ts.overflowed():
+            ts.grow()
+    torch.cuda.synchronize()
+    D.barrier()
+    # ---- timed region: device-resident inputs
+    cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip().isdigit()]
+    clk = ClockSampler(int(cvd[local]) if local < len(cvd) else local)
+    clk.start()
+    P.launch_count(reset=True)
+    ts.prof = []
+    torch.cuda.synchronize()
+    D.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        ts.step(targets)
+    e1.record()
+    torch.cuda.synchronize()
+    D.barrier()
+    launches = P.launch_count(reset=True)
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    ms_max = D.allreduce_max(ms, device=torch.device("cuda", local))
+    phases = ts.phase_ms()
+    ts.prof = None
+    overflow = ts.overflowed()
+    it_s = a.steps / (ms_max / 1e3)
+    H, W = sc.cameras[0].height, sc.cameras[0].width
+    mpix = it_s * V * H * W / 1e6
+    # ---- counts for the roofline (one extra untimed forward, same state)
+    dev = torch.device("cuda", local)
+    ts.stats = {"pairs": torch.zeros((), dtype=torch.int64, device=dev),
+                "instances": torch.zeros((), dtype=torch.int64, device=dev)}
+    ts.forward_backward(targets)
+    pairs, inst = float(ts.stats["pairs"].item()), float(ts.stats["instances"].item())
+    ts.stats = None
+    counts = {"pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
+              "launches_per_step": len(ts.batches) * a.steps}
+    pk = peaks()
+    dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1)
+    # ---- end to end through the public API: H2D targets + loss read back
+    e2e_steps = a.e2e_steps or a.steps
+    host_t = torch.from_numpy(tg_np).pin_memory()
+    dev_t = torch.empty_like(targets)
+    torch.cuda.synchronize()
+    D.barrier()
+    t0 = time.perf_counter()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(e2e_steps):
+        dev_t.copy_(host_t, non_blocking=True)
+        loss = ts.step(dev_t)
+        _ = float(loss.item())
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_ms = D.allreduce_max(s0.elapsed_time(s1), device=torch.device("cuda", local))
+    e2e = {"value": round(e2e_steps / (e2e_ms / 1e3), 4), "unit": "it/s",
+           "h2d_bytes_per_step": int(host_t.numel() * 4), "d2h_bytes_per_step": 4}
+    del dev_t, host_t
+    if rank == 0:
+        cb = None
+        if world == 1 and not a.no_cpu_baseline:
+            try:
+                cb = cpu_baseline_sample(sc, tg_np[0], a.cpu_budget_s, V)
+            except Exception as ex:  # noqa: BLE001
+                cb = {"error": str(ex)}
+        line = {
+            "metric": METRIC, "value": round(it_s, 4), "unit": "it/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max / a.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": V,
+                       "width": W, "height": H, "sh_degree": sc.sh_degree,
+                       "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch,
+                       "parallelism": f"view-dp{world}",
+                       "l2": "no flush: inputs > L2 (params 720 MB, targets 837 MB, bins GBs)"},
+            "mpix_per_s_fwd_bwd": round(mpix, 2),
+            "phase_ms_per_step": {k: round(v / a.steps, 3) for k, v in phases.items()},
+            "roofline": roof,
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "bin_overflow": bool(overflow),
+        }
+        print(json.dumps(line), flush=True)
+    D.barrier()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -148,6 +148,8 @@ typedef struct {
 
 /* flags for sss_render_bwd */
 #define SSS_BWD_NU_GRAD_PAPER 1 /* use the printed dT/dnu of PAPER.md:1301-1314 (R13) */
+#define SSS_BWD_RASTER_ONLY 2   /* run only the a4 raster half (fills the workspace) */
+#define SSS_BWD_PROJECTION_ONLY 4 /* run only the a5 projection half (consumes it) */
 
 /* a1 — projection of every component into V views (Eq. 4,
  * 1116-1215 SM forward, 1077-1079 nu range / truncation / no low-pass).

@@ -75,7 +75,7 @@ def lib():
             ("orc_bin", i64, [p, p, p, p, p]),
             ("orc_tile_lists", i64, [p, p, i32, p, p, p, i64]),
             ("orc_render", C.c_int, [p, p, p, i32, p, p, p, p, p, p, i32, i32, p]),
-            ("orc_backward", C.c_int, [p, p, p, p, i32, i32, p, p, p, i32]),
+            ("orc_backward", C.c_int, [p, p, p, p, i32, i32, p, p, p, i32, i32, p]),
             ("orc_philox4x32_10", None, [p, p, p]),
             ("orc_normals3", None, [C.c_uint64, i64, i64, p]),
             ("orc_sghmc_step", C.c_int, [i64, i32, p, p, p, p, p, p]),
@@ -291,8 +291,9 @@ def render(planes, sh_degree, cam, bg=(0.0, 0.0, 0.0), mode="tiled", lists_in=No
 
 
 def backward(planes, sh_degree, cam, d_rgb, bg=(0.0, 0.0, 0.0), mode="tiled", lists_in=None,
-             nu_grad_paper=False, want_g2d=False):
-    """Reverse mode of render(): (grad planes [P][n] fp64, g2d [n][10] or None)."""
+             nu_grad_paper=False, want_g2d=False, pixels=None):
+    """Reverse mode of render(): (grad planes [P][n] fp64, g2d [n][10] or None).
+    `pixels`: optional flat pixel indices; then d_rgb is [3][len(pixels)]."""
     P = _P(planes, sh_degree)
     c = _cam(cam)
     n = P.arr.shape[1]
@@ -305,9 +306,11 @@ def backward(planes, sh_degree, cam, d_rgb, bg=(0.0, 0.0, 0.0), mode="tiled", li
     if mode == "frozen":
         lin = np.ascontiguousarray(lists_in, dtype=np.int32)
         cap = lin.shape[-1]
+    sel = None if pixels is None else np.ascontiguousarray(np.asarray(pixels, np.int32))
     lib().orc_backward(P.ref, C.byref(c), _ptr(bgv), _ptr(d), MODES[mode], int(nu_grad_paper),
                        _ptr(grads), _ptr(g2d) if g2d is not None else None,
-                       _ptr(lin) if lin is not None else None, cap)
+                       _ptr(lin) if lin is not None else None, cap,
+                       len(sel) if sel is not None else 0, _ptr(sel) if sel is not None else None)
     return grads, g2d
 
 

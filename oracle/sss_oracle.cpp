@@ -591,23 +591,26 @@ int orc_render(const orc_params* P, const orc_cam* cam, const double* bg, int32_
 // groups ("dL/dmu, dL/dS, dL/dR, dL/dc, dL/do, dL/dnu").
 // grad_planes [P][n] is accumulated (+=); g2d [n][10] (+=, nullable) holds
 // dL/d{mean2d x,y, conic A,B,C, colour r,g,b, o, nu} per component.
+// If pix_sel != NULL only the n_sel listed pixels (y*W+x) contribute and
+// d_rgb is compact ([3][n_sel]).
 int orc_backward(const orc_params* P, const orc_cam* cam, const double* bg, const double* d_rgb,
                  int32_t mode, int32_t nu_grad_paper, double* grad_planes, double* g2d_out,
-                 const int32_t* lists_in, int32_t cap) {
+                 const int32_t* lists_in, int32_t cap, int32_t n_sel, const int32_t* pix_sel) {
   View v;
   build_view(P, *cam, v, mode == 1);
   const int64_t n = P->n;
-  const int64_t npx = (int64_t)v.W * v.H;
+  const int64_t npx = pix_sel ? (int64_t)n_sel : (int64_t)v.W * v.H;
   std::vector<double> g2d((size_t)n * 10, 0.0);
 #pragma omp parallel
   {
     std::vector<Entry> L;
 #pragma omp for schedule(dynamic, 64)
-    for (int64_t pix = 0; pix < npx; ++pix) {
+    for (int64_t s = 0; s < npx; ++s) {
+      const int64_t pix = pix_sel ? (int64_t)pix_sel[s] : s;
       const int x = (int)(pix % v.W), y = (int)(pix / v.W);
       pixel_list(v, x, y, mode, lists_in, cap, L, nullptr);
       if (L.empty()) continue;
-      const double g[3] = {d_rgb[0 * npx + pix], d_rgb[1 * npx + pix], d_rgb[2 * npx + pix]};
+      const double g[3] = {d_rgb[0 * npx + s], d_rgb[1 * npx + s], d_rgb[2 * npx + s]};
       // suffix S_i: colour behind i normalised by W_{i+1}; S_n = bg
       double S[3] = {bg[0], bg[1], bg[2]};
       for (int k = (int)L.size() - 1; k >= 0; --k) {

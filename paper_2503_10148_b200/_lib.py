@@ -18,6 +18,8 @@ SSS_MAX_BINS = 6144
 SSS_REC_FLOATS = 12
 SSS_G2D_FLOATS = 12
 SSS_BWD_NU_GRAD_PAPER = 1
+SSS_BWD_RASTER_ONLY = 2
+SSS_BWD_PROJECTION_ONLY = 4
 
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",

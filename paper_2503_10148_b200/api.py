@@ -244,9 +244,11 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
                    bg=(0.0, 0.0, 0.0), d_rgb: Optional[torch.Tensor] = None,
                    target: Optional[torch.Tensor] = None, grad: Optional[Params] = None,
                    loss: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
-                   nu_grad_paper: bool = False, stream=None, cams_c=None) -> Params:
+                   nu_grad_paper: bool = False, stream=None, cams_c=None,
+                   half: Optional[str] = None) -> Params:
     """grad += d(L)/d(params).  `ws` (zeroed, reusable) holds the screen-space
-    gradient records; it is left zero by the call."""
+    gradient records; it is left zero by the call.  half = "raster" /
+    "projection" runs one of the two kernels (timing instrumentation)."""
     lib = L.load()
     V = len(cams)
     cc = cams_c if cams_c is not None else cameras_c(cams)
@@ -261,6 +263,10 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
     bgc = (C.c_float * 3)(*[float(x) for x in bg])
     pc, prc, bc, fc, gc = params.c(), proj.c(), bins.c(), frame.c(), grad.c()
     flags = L.SSS_BWD_NU_GRAD_PAPER if nu_grad_paper else 0
+    if half == "raster":
+        flags |= L.SSS_BWD_RASTER_ONLY
+    elif half == "projection":
+        flags |= L.SSS_BWD_PROJECTION_ONLY
     L.check(lib.sss_render_bwd(C.byref(pc), C.byref(prc), C.byref(bc), cc, V, bgc, C.byref(fc),
                                _ptr(d_rgb), _ptr(target), _ptr(loss), C.byref(gc), _ptr(ws),
                                ws.numel(), flags, _stream_ptr(stream)), "sss_render_bwd")

@@ -512,7 +512,10 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
     set_error("sss_render_bwd: n / sh_degree mismatch");
     return SSS_ERR_ARG;
   }
-  if (!d_rgb && !target) { set_error("sss_render_bwd: need d_rgb or target"); return SSS_ERR_ARG; }
+  if (!(flags & SSS_BWD_PROJECTION_ONLY) && !d_rgb && !target) {
+    set_error("sss_render_bwd: need d_rgb or target");
+    return SSS_ERR_ARG;
+  }
   RasterGeom G;
   if (!raster_geom(pr, bins, cams, n_views, G)) { set_error("sss_render_bwd: geometry mismatch"); return SSS_ERR_SHAPE; }
   const size_t need = sss_render_bwd_workspace(p->n, n_views);
@@ -531,15 +534,17 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
                                                           bg[1], bg[2], fwd->rgb, fwd->final_T,         \
                                                           fwd->last, d_rgb, target, loss_out, g2d, flags)
   const bool l1 = d_rgb == nullptr;
-  if (G.shift > 0) {
-    if (l1) SSS_BWD_LAUNCH(true, true); else SSS_BWD_LAUNCH(true, false);
-  } else {
-    if (l1) SSS_BWD_LAUNCH(false, true); else SSS_BWD_LAUNCH(false, false);
+  if (!(flags & SSS_BWD_PROJECTION_ONLY)) {
+    if (G.shift > 0) {
+      if (l1) SSS_BWD_LAUNCH(true, true); else SSS_BWD_LAUNCH(true, false);
+    } else {
+      if (l1) SSS_BWD_LAUNCH(false, true); else SSS_BWD_LAUNCH(false, false);
+    }
+    count_launch();
+    if ((st = check_launch("sss_render_bwd(raster)")) != SSS_OK) return st;
   }
 #undef SSS_BWD_LAUNCH
-  count_launch();
-  if ((st = check_launch("sss_render_bwd(raster)")) != SSS_OK) return st;
-  if (p->n == 0) return SSS_OK;
+  if (p->n == 0 || (flags & SSS_BWD_RASTER_ONLY)) return SSS_OK;
   const int threads = 128;
   const int blocks = div_up(p->n, threads);
   for (int v0 = 0; v0 < n_views; v0 += kMaxViewsPerLaunch) {

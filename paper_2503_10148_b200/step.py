@@ -56,7 +56,15 @@ class TrainStep:
                                   device=dev)
         self.loss = torch.zeros(1, device=dev)
         self.bins: List[A.Bins] = []
+        self.prof = None  # list of (phase, cuda event) when timing phases
+        self.stats = None  # dict of device counters (pairs, instances) when counting
         self._size_bins()
+
+    def _mark(self, name: str):
+        if self.prof is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.prof.append((name, e))
 
     # -- bin capacity ------------------------------------------------------
     def _size_bins(self, factor: float = 1.0):
@@ -94,27 +102,60 @@ class TrainStep:
         targets: [V_local][3][H][W] fp32 device tensor."""
         self.grad.planes.zero_()
         self.loss.zero_()
+        self._mark("start")
         for bi, b in enumerate(self.batches):
             nv = len(b)
             cams = [self.cams[v] for v in b]
             cc = self.cams_c[bi]
             pv, fv, bv = self._proj_view(nv), self._frame_view(nv), self._bins_view(nv)
+            tg = targets[b[0]:b[-1] + 1]
             A.sss_project(self.params, cams, out=pv, cams_c=cc)
+            self._mark("project")
             A.sss_bin_sort(pv, cams, bin_shift=self.bin_shift, ws=self.ws_bin, out=bv, cams_c=cc)
+            self._mark("bin_sort")
             A.sss_render_fwd(pv, bv, cams, bg=self.bg, out=fv, cams_c=cc)
-            A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg,
-                             target=targets[b[0]:b[-1] + 1], grad=self.grad, loss=self.loss,
-                             ws=self.ws_g2d, cams_c=cc)
+            self._mark("render_fwd")
+            if self.stats is not None:
+                self.stats["pairs"] += fv.n_contrib.sum(dtype=torch.int64)
+                self.stats["instances"] += bv.totals.sum()
+            if self.prof is None:
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
+                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
+            else:  # same two kernels, split so each can be timed
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
+                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc,
+                                 half="raster")
+                self._mark("render_bwd_raster")
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
+                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc,
+                                 half="projection")
+                self._mark("render_bwd_projection")
 
     def step(self, targets: torch.Tensor) -> torch.Tensor:
         """One full iteration; returns the (device) loss of this rank."""
         self.forward_backward(targets)
         D.allreduce_sum_(self.grad.planes, self.group)
+        self._mark("allreduce")
         self.hp.step = self.t
         self.hp.grad_scale = 1.0 / self.total_views
         A.sss_sghmc_step(self.params, self.grad, self.m, self.v, self.r, self.hp)
+        self._mark("sghmc")
         self.t += 1
         return self.loss
+
+    def phase_ms(self) -> dict:
+        """Per-phase milliseconds of the recorded events (after a sync)."""
+        out = {}
+        if not self.prof:
+            return out
+        prev = self.prof[0][1]
+        for name, e in self.prof[1:]:
+            if name == "start":
+                prev = e
+                continue
+            out[name] = out.get(name, 0.0) + prev.elapsed_time(e)
+            prev = e
+        return out
 
     def overflowed(self) -> bool:
         """Synchronising check of the bin overflow flag."""
