@@ -71,6 +71,7 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SSS_LIB", path)  # dev: load a variant build
     if not os.path.exists(path) or os.environ.get("SSS_REBUILD"):
         from . import _build
 

@@ -110,3 +110,4 @@ extern "C" int64_t sss_launch_count(int32_t reset) {
   if (reset) sss::g_launches = 0;
   return v;
 }
+

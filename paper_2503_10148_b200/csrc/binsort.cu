@@ -93,8 +93,16 @@ __global__ void keys_init_kernel(const float* __restrict__ depth, const short4* 
     keys[(int64_t)v * n + i] = vis ? __float_as_uint(depth[(int64_t)v * n + i]) : 0xFFFFFFFFu;
     vals[(int64_t)v * n + i] = (int32_t)i;
   }
+  // one atomic per block (per-warp atomics on one address serialise)
+  __shared__ int32_t wsum[8];
   const unsigned b = __ballot_sync(0xffffffffu, vis);
-  if (lane_id() == 0 && b) atomicAdd(&n_vis[v], __popc(b));
+  if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
+    if (s) atomicAdd(&n_vis[v], s);
+  }
 }
 
 // Positive fp32 depths (> z_near > 0) order like their bit patterns.
@@ -301,8 +309,77 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   }
 }
 
+// Walks the instances (component, bin) of the warp's components
+// [wlo, whi) in order — component-major, bin row-major — 32 instances per
+// step: the instance counts of 32 consecutive components are prefix-summed
+// across the warp, each lane finds the component owning its flat index by a
+// 5-step binary search over the lanes, and lanes hitting the same bin in the
+// same step are ranked by lane order (match.any), which preserves the
+// (depth, index) order within every bin.  COUNT: per-warp bin counts;
+// otherwise write ids (and keys) at base[b] + the warp's running offset.
+template <bool COUNT>
+__device__ __forceinline__ void warp_instances(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
+                                               const float* __restrict__ dv, int64_t wlo, int64_t whi,
+                                               const BinGeom& g, uint16_t* my, const uint32_t* base,
+                                               int32_t* __restrict__ idv, uint64_t* __restrict__ kv) {
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
+    const int64_t j = j0 + lane;
+    int id = 0, bx0 = 0, by0 = 0, bw = 1, nb = 0;
+    uint32_t dbits = 0;
+    if (j < whi) {
+      id = sid[j];
+      const short4 r = rv[id];
+      bx0 = r.x >> g.shift;
+      by0 = r.y >> g.shift;
+      bw = (r.z >> g.shift) - bx0 + 1;
+      nb = bw * ((r.w >> g.shift) - by0 + 1);
+      if (!COUNT && kv) dbits = __float_as_uint(dv[id]);
+    }
+    int incl = nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - nb;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int f0 = 0; f0 < total; f0 += 32) {
+      const int f = f0 + lane;
+      const bool act = f < total;
+      int k = 0;  // owner lane: the largest k with excl_k <= f
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, excl, k + step);
+        if (e <= f) k += step;
+      }
+      const int t = f - __shfl_sync(0xffffffffu, excl, k);
+      const int kbw = __shfl_sync(0xffffffffu, bw, k);
+      const int kbx0 = __shfl_sync(0xffffffffu, bx0, k);
+      const int kby0 = __shfl_sync(0xffffffffu, by0, k);
+      const int row = t / kbw;
+      const int b = (kby0 + row) * g.bins_x + kbx0 + (t - row * kbw);
+      const unsigned peers = __match_any_sync(0xffffffffu, act ? b : -1 - lane);
+      const int rank = __popc(peers & lt);
+      if (!COUNT) {
+        const int kid = __shfl_sync(0xffffffffu, id, k);
+        const uint32_t kd = __shfl_sync(0xffffffffu, dbits, k);
+        if (act) {
+          const uint32_t pos = base[b] + my[b] + rank;
+          idv[pos] = kid;
+          if (kv) kv[pos] = ((uint64_t)b << 32) | kd;
+        }
+      }
+      __syncwarp();
+      if (act && rank == 0) my[b] += (uint16_t)__popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
 // stable scatter: CTA per (chunk, view); warp w owns components
-// [chunk*c + w*chunk/8, ...) and walks them in order.
+// [chunk*c + w*chunk/8, ...) and walks their instances in order.
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int chunk,
@@ -322,32 +399,17 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) base[b] = bs[b] + ch[b];
   for (int k = threadIdx.x; k < kScatterWarps * g.n_bins; k += blockDim.x) woff[k] = 0;
   __syncthreads();
-  const int w = threadIdx.x >> 5, lane = lane_id();
+  const int w = threadIdx.x >> 5;
   const int per_warp = chunk / kScatterWarps;
   const int64_t wlo = lo + (int64_t)w * per_warp;
   const int64_t whi = min(wlo + per_warp, nvis);
   uint16_t* my = woff + (size_t)w * g.n_bins;
   const int32_t* sid = sorted_ids + (int64_t)v * n;
   const short4* rv = rect + (int64_t)v * n;
-  // phase 1: per-warp counts
-  for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
-    const int64_t j = j0 + lane;
-    int id = -1;
-    short4 r = make_short4(1, 1, 0, 0);
-    if (j < whi) { id = sid[j]; r = rv[id]; }
-    const int cnt = (int)min((int64_t)32, whi - j0);
-    for (int k = 0; k < cnt; ++k) {
-      const int rx0 = __shfl_sync(0xffffffffu, (int)r.x, k), ry0 = __shfl_sync(0xffffffffu, (int)r.y, k);
-      const int rx1 = __shfl_sync(0xffffffffu, (int)r.z, k), ry1 = __shfl_sync(0xffffffffu, (int)r.w, k);
-      const int bx0 = rx0 >> g.shift, by0 = ry0 >> g.shift, bx1 = rx1 >> g.shift, by1 = ry1 >> g.shift;
-      const int bw = bx1 - bx0 + 1, nb = bw * (by1 - by0 + 1);
-      for (int t = lane; t < nb; t += 32) {
-        const int b = (by0 + t / bw) * g.bins_x + bx0 + t % bw;
-        my[b] += 1;
-      }
-      __syncwarp();
-    }
-  }
+  const float* dv = depth + (int64_t)v * n;
+  int32_t* idv = ids + (int64_t)v * capacity;
+  uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
+  warp_instances<true>(sid, rv, dv, wlo, whi, g, my, base, idv, kv);  // phase 1: counts
   __syncthreads();
   for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) {
     uint32_t acc = 0;
@@ -358,38 +420,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     }
   }
   __syncthreads();
-  // phase 2: scatter in order
-  int32_t* idv = ids + (int64_t)v * capacity;
-  uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  const float* dv = depth + (int64_t)v * n;
-  for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
-    const int64_t j = j0 + lane;
-    int id = -1;
-    short4 r = make_short4(1, 1, 0, 0);
-    uint32_t dbits = 0;
-    if (j < whi) {
-      id = sid[j];
-      r = rv[id];
-      if (kv) dbits = __float_as_uint(dv[id]);
-    }
-    const int cnt = (int)min((int64_t)32, whi - j0);
-    for (int k = 0; k < cnt; ++k) {
-      const int cid = __shfl_sync(0xffffffffu, id, k);
-      const uint32_t cd = __shfl_sync(0xffffffffu, dbits, k);
-      const int rx0 = __shfl_sync(0xffffffffu, (int)r.x, k), ry0 = __shfl_sync(0xffffffffu, (int)r.y, k);
-      const int rx1 = __shfl_sync(0xffffffffu, (int)r.z, k), ry1 = __shfl_sync(0xffffffffu, (int)r.w, k);
-      const int bx0 = rx0 >> g.shift, by0 = ry0 >> g.shift, bx1 = rx1 >> g.shift, by1 = ry1 >> g.shift;
-      const int bw = bx1 - bx0 + 1, nb = bw * (by1 - by0 + 1);
-      for (int t = lane; t < nb; t += 32) {
-        const int b = (by0 + t / bw) * g.bins_x + bx0 + t % bw;
-        const uint32_t pos = base[b] + my[b];
-        my[b] += 1;
-        idv[pos] = cid;
-        if (kv) kv[pos] = ((uint64_t)b << 32) | cd;
-      }
-      __syncwarp();
-    }
-  }
+  warp_instances<false>(sid, rv, dv, wlo, whi, g, my, base, idv, kv);  // phase 2: scatter
 }
 
 }  // namespace

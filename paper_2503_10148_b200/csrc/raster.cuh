@@ -4,8 +4,43 @@
 
 namespace sss {
 
-constexpr int kRasterThreads = 256;  // one thread per pixel of a 16x16 tile
-constexpr int kBatch = 256;          // bin entries staged per shared-memory batch
+// A CTA renders one 16x16 tile of one view; each thread owns kPX horizontally
+// adjacent pixels, a warp an (8 kPX) x 4 strip.  With kPX = 2 the per-entry
+// shared-memory loads, the warp culling test and (backward) the warp
+// reduction are amortised over 64 pixels instead of 32.
+#ifndef SSS_RASTER_PX
+#define SSS_RASTER_PX 4
+#endif
+#ifndef SSS_BOX_CULL
+#define SSS_BOX_CULL 0
+#endif
+constexpr int kPX = SSS_RASTER_PX;
+static_assert(kPX == 1 || kPX == 2 || kPX == 4, "1, 2 or 4 pixels per thread");
+constexpr int kRasterThreads = 256 / kPX;
+constexpr int kRasterWarps = kRasterThreads / 32;
+constexpr int kBatch = kRasterThreads < 128 ? kRasterThreads : 128;  // entries per smem batch
+constexpr int kWarpW = kPX == 1 ? 8 : 16;         // warp strip: 8x4, 16x4 or 16x8 pixels
+constexpr int kWarpH = 32 * kPX / kWarpW;
+constexpr int kLanesPerRow = kWarpW / kPX;
+constexpr int kWarpsPerRow = 16 / kWarpW;
+
+// Development counters (variant builds with -DSSS_COUNTERS only).
+#ifdef SSS_COUNTERS
+static __device__ unsigned long long g_cnt[16];  // one set per translation unit
+#define SSS_COUNT(i, x) atomicAdd(&g_cnt[(i)], (unsigned long long)(x))
+#define SSS_COUNTER_ACCESSOR(NAME)                                                                  \
+  extern "C" __attribute__((visibility("default"))) int NAME(unsigned long long* h, int reset) {   \
+    if (cudaMemcpyFromSymbol(h, sss::g_cnt, sizeof(unsigned long long) * 16) != cudaSuccess) return 1; \
+    if (reset) {                                                                                    \
+      unsigned long long z[16] = {0};                                                               \
+      if (cudaMemcpyToSymbol(sss::g_cnt, z, sizeof(z)) != cudaSuccess) return 1;                    \
+    }                                                                                               \
+    return 0;                                                                                       \
+  }
+#else
+#define SSS_COUNTER_ACCESSOR(NAME)
+#define SSS_COUNT(i, x) ((void)0)
+#endif
 
 struct RasterGeom {
   int width, height, tiles_x, tiles_y, shift, bins_x, n_bins;
@@ -15,24 +50,23 @@ struct RasterGeom {
 bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera* cams, int n_views,
                  RasterGeom& G);
 
-// Pixel of this thread: warp w covers an 8x4 block so the lanes of a warp
-// are spatially compact (coherent inclusion decisions per warp).
-__device__ __forceinline__ void pixel_of(int tid, int& lx, int& ly) {
+// First pixel of this thread (the others follow at lx + 1, ...) and the
+// origin of its warp's strip, within the tile.
+__device__ __forceinline__ void pixels_of(int tid, int& lx, int& ly, int& sx, int& sy) {
   const int w = tid >> 5, l = tid & 31;
-  lx = ((w & 1) << 3) + (l & 7);
-  ly = ((w >> 1) << 2) + (l >> 3);
+  sx = (w % kWarpsPerRow) * kWarpW;
+  sy = (w / kWarpsPerRow) * kWarpH;
+  lx = sx + (l % kLanesPerRow) * kPX;
+  ly = sy + l / kLanesPerRow;
 }
 
 // The fp32 inclusion quadratic h = A dx^2 + B2 dx dy + C dy^2 in the exact
 // order of DESIGN.md §2 (intrinsics: never contracted / reassociated), so the
-// inclusion decision h <= hmax is bit-identical to the oracle's.
-__device__ __forceinline__ float h_f32(float px, float py, float4 a, float C) {
-  const float dx = __fsub_rn(px, a.x);
-  const float dy = __fsub_rn(py, a.y);
-  const float bdy = __fmul_rn(a.w, dy);
-  const float cdy = __fmul_rn(C, dy);
-  const float cdy2 = __fmul_rn(cdy, dy);
-  return __fmaf_rn(dx, __fmaf_rn(a.z, dx, bdy), cdy2);
+// inclusion decision h <= hmax is bit-identical to the fp64 reference's fp32
+// test.  bdy = B2*dy and cdy2 = (C*dy)*dy depend only on the row.
+__device__ __forceinline__ float h_f32_row(float px, float mx, float A, float bdy, float cdy2) {
+  const float dx = __fsub_rn(px, mx);
+  return __fmaf_rn(dx, __fmaf_rn(A, dx, bdy), cdy2);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -52,6 +86,30 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // lanes evaluate the same component).
 __device__ __forceinline__ float log2_1p(float t, bool precise) {
   return precise ? log1pf(t) * 1.4426950408889634f : lg2_approx(1.0f + t);
+}
+
+// Conservative pixel-centre bounding box of {h_f32 <= hmax} for warp-level
+// culling: x in [box.x, box.y], y in [box.z, box.w].  The half-extents
+// sqrt(hmax Sigma_xx), sqrt(hmax Sigma_yy) get a 1-pixel margin; for
+// ill-conditioned conics (where fp32 cancellation in h could exceed the
+// margin) the box is unbounded, i.e. no culling.
+__device__ __forceinline__ float4 entry_box(float4 a, float4 b) {
+  const float A = a.z, B = 0.5f * a.w, C = b.x;
+  const float det = A * C - B * B;
+  const float INF = __int_as_float(0x7f800000);
+  if (!(det > 0.01f * A * C) || !(A > 0.f) || !(C > 0.f)) return make_float4(-INF, INF, -INF, INF);
+  const float ex = sqrtf(b.y * C / det) + 1.0f;
+  const float ey = sqrtf(b.y * A / det) + 1.0f;
+  if (!(ex < 1e30f) || !(ey < 1e30f)) return make_float4(-INF, INF, -INF, INF);
+  return make_float4(a.x - ex, a.x + ex, a.y - ey, a.y + ey);
+}
+
+__device__ __forceinline__ bool box_misses(float4 bx, float x0, float x1, float y0, float y1) {
+#if SSS_BOX_CULL
+  return bx.y < x0 || bx.x > x1 || bx.w < y0 || bx.z > y1;
+#else
+  return false;
+#endif
 }
 
 }  // namespace sss

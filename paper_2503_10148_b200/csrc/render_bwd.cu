@@ -2,20 +2,23 @@
 // "Backward Pass") to the six parameter groups
 // (PAPER.md:165).
 //
-// a4 raster backward.  One CTA per tile and view, one thread per pixel,
-// replaying the tile's bin list back to front from the last composited entry
-// (the forward's `last`).  Per pair (PAPER.md:1230-1268 chain, R10, R13):
+// a4 raster backward.  One CTA per tile and view, 128 threads with two
+// pixels each, replaying the tile's bin list back to front from the last
+// composited entry (the forward's `last`).  Per pair (PAPER.md:1230-1268
+// chain, R10, R13):
 //   W_i = W_{i+1} / (1 - a_i),  dL/dc = g a_i W_i,
 //   dL/da = W_i sum_k g_k (c_k - S_k),  S <- c a + (1 - a) S,
 //   dL/do = dL/da T,  dL/dT = dL/da o,
 //   dT/dh = -(nu+2)/(2 nu) T / (1 + h/nu)
 //   dT/dnu = T [-1/2 ln(1 + h/nu) + (nu+2) h / (2 nu^2 (1 + h/nu))]  (R13)
 //   dh/dmu2D = -2 Q d,  dh/d(A, B, C) = (dx^2, 2 dx dy, dy^2).
-// The 10 per-pair values are reduced across the warp with a 16-lane
-// butterfly reduce-scatter (16 shuffles for 10 values instead of 50), warps
-// with no included lane skip it (vote.any), the 8 warps combine in shared
-// memory, and one vector RED per (component, tile) goes to the screen-space
-// gradient record g2d[v][i] (48 B) in the workspace.
+// A thread sums its two pixels' 10 per-pair values, the warp reduces them
+// with a 16-lane butterfly reduce-scatter (16 shuffles for 10 values instead
+// of 50), warps whose 16x4 strip misses the entry's box or whose lanes are
+// all excluded skip it (warp-uniform), each warp stores its partial sums in
+// its own shared-memory slot (no shared atomics), and after the batch one
+// vector RED per (component, tile) adds the 4 warps' sums to the
+// screen-space gradient record g2d[v][i] (48 B) in the workspace.
 //
 // a6: with target != NULL the L1 image gradient sign(C - target)/(3HW) is
 // formed in the same kernel (no image-gradient buffer) and the loss summed.
@@ -65,6 +68,50 @@ __device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+constexpr int kAccPitch = kBatch + 1;  // conflict-free column writes
+constexpr size_t kAccBytes = (size_t)kRasterWarps * 10 * kAccPitch * sizeof(float);
+
+struct PixB {  // backward state of one pixel
+  float W, S0, S1, S2, g0, g1, g2;
+  int32_t last;
+};
+
+// Adds one composited pair's contribution to vals[0..9] and steps the
+// pixel's replay state (W_i = W_{i+1} / (1 - a_i), suffix colour S).
+__device__ __forceinline__ void pair_grad(PixB& p, float dx, float dy, float h, float4 a, float4 b,
+                                          float4 c, bool nu_paper, float* vals) {
+  const float t = fmaxf(h, 0.f) * b.w;
+  const float opt = 1.f + t;
+  const float lg = log2_1p(t, b.w < (1.f / 32.f));
+  const float T = ex2_approx(c.x * lg);
+  const float araw = b.z * T;
+  const float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
+  const float Wi = __fdividef(p.W, 1.f - alpha);
+  const float aw = alpha * Wi;
+  vals[5] = fmaf(p.g0, aw, vals[5]);
+  vals[6] = fmaf(p.g1, aw, vals[6]);
+  vals[7] = fmaf(p.g2, aw, vals[7]);
+  float da = (p.g0 * (c.y - p.S0) + p.g1 * (c.z - p.S1) + p.g2 * (c.w - p.S2)) * Wi;
+  p.S0 = fmaf(c.y - p.S0, alpha, p.S0);
+  p.S1 = fmaf(c.z - p.S1, alpha, p.S1);
+  p.S2 = fmaf(c.w - p.S2, alpha, p.S2);
+  p.W = Wi;
+  if (fabsf(araw) > kAlphaMax) da = 0.f;
+  vals[8] = fmaf(da, T, vals[8]);
+  const float dT = da * b.z;
+  const float Topt = __fdividef(T, opt);
+  const float dh = dT * c.x * b.w * Topt;
+  const float dTdnu = nu_paper ? -c.x * t * b.w * Topt
+                               : T * (-0.34657359027997264f * lg - __fdividef(c.x * t * b.w, opt));
+  vals[9] = fmaf(dT, dTdnu, vals[9]);
+  const float dhdx = dh * dx, dhdy = dh * dy;
+  vals[0] -= 2.f * a.z * dhdx + a.w * dhdy;
+  vals[1] -= a.w * dhdx + 2.f * b.x * dhdy;
+  vals[2] = fmaf(dhdx, dx, vals[2]);
+  vals[3] = fmaf(2.f * dhdx, dy, vals[3]);
+  vals[4] = fmaf(dhdy, dy, vals[4]);
+}
+
 template <bool FILTER, bool L1>
 __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
     const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
@@ -72,56 +119,64 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
     float4* __restrict__ g2d, int flags) {
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch], sbox[kBatch];
   __shared__ int32_t spos[kBatch], sid[kBatch];
-  __shared__ __align__(16) float acc[kBatch * SSS_G2D_FLOATS];
-  __shared__ int32_t wcnt[kRasterThreads / 32];
-  __shared__ float wred[kRasterThreads / 32];
+  __shared__ int32_t wcnt[kRasterWarps];
+  __shared__ float wred[kRasterWarps];
   __shared__ int32_t smax;
+  extern __shared__ float acc[];  // [warps][10][kAccPitch] per-warp partial sums, no atomics
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
   const int32_t start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
-  int lx, ly;
-  pixel_of(threadIdx.x, lx, ly);
-  const int x = tx * kTile + lx, y = ty * kTile + ly;
-  const bool inside = x < G.width && y < G.height;
-  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  int lx, ly, sx, sy;
+  pixels_of(threadIdx.x, lx, ly, sx, sy);
+  const int x0 = tx * kTile + lx, y = ty * kTile + ly;
+  const float py = (float)y + 0.5f;
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
+  const float wx0 = (float)(tx * kTile + sx) + 0.5f, wx1 = wx0 + (float)(kWarpW - 1);
+  const float wy0 = (float)(ty * kTile + sy) + 0.5f, wy1 = wy0 + (float)(kWarpH - 1);
   const int64_t HW = (int64_t)G.width * G.height;
-  const int64_t pix = (int64_t)y * G.width + x;
-
-  float g0 = 0.f, g1 = 0.f, g2 = 0.f, W = 1.f, lsum = 0.f;
-  int32_t lastp = start;
   const float inv3P = 1.0f / (3.0f * (float)HW);
-  if (inside) {
-    lastp = last[(int64_t)v * HW + pix];
-    W = final_T[(int64_t)v * HW + pix];
+
+  PixB q[kPX];
+  float px[kPX];
+  float lsum = 0.f;
+  int32_t m = start;
+#pragma unroll
+  for (int k = 0; k < kPX; ++k) {
+    q[k] = PixB{1.f, bg0, bg1, bg2, 0.f, 0.f, 0.f, start};
+    px[k] = (float)(x0 + k) + 0.5f;
+    if (!(x0 + k < G.width && y < G.height)) continue;
+    const int64_t pix = (int64_t)y * G.width + x0 + k;
+    q[k].last = last[(int64_t)v * HW + pix];
+    q[k].W = final_T[(int64_t)v * HW + pix];
+    m = max(m, q[k].last);
     if (L1) {
       const float* cimg = rgb + (int64_t)v * 3 * HW + pix;
       const float* timg = target + (int64_t)v * 3 * HW + pix;
       const float d0 = cimg[0] - timg[0], d1 = cimg[HW] - timg[HW], d2 = cimg[2 * HW] - timg[2 * HW];
-      g0 = (d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f));
-      g1 = (d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f));
-      g2 = (d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f));
-      lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
+      q[k].g0 = d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f);
+      q[k].g1 = d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f);
+      q[k].g2 = d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f);
+      lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
     } else {
       const float* gimg = d_rgb + (int64_t)v * 3 * HW + pix;
-      g0 = gimg[0];
-      g1 = gimg[HW];
-      g2 = gimg[2 * HW];
+      q[k].g0 = gimg[0];
+      q[k].g1 = gimg[HW];
+      q[k].g2 = gimg[2 * HW];
     }
   }
   // tile end = max over pixels of `last`; loss partial sums
-  int32_t m = lastp;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (L1) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
   }
+  const int32_t wlast = m;  // this warp's replay start (max over its pixels)
   if (threadIdx.x == 0) smax = start;
   __syncthreads();
   if (lane == 0) {
@@ -130,9 +185,10 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   }
   __syncthreads();
   const int32_t end = smax;
+  if (threadIdx.x == 0) SSS_COUNT(7, end - start);
   if (L1 && loss_out && threadIdx.x == 0) {
     float s = 0.f;
-    for (int k = 0; k < kRasterThreads / 32; ++k) s += wred[k];
+    for (int k = 0; k < kRasterWarps; ++k) s += wred[k];
     atomicAdd(loss_out, s * inv3P);
   }
 
@@ -141,13 +197,14 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   const short4* rcv = rect + (int64_t)v * G.n;
   float4* gv = g2d + (int64_t)v * G.n * 3;
   const bool nu_paper = flags & SSS_BWD_NU_GRAD_PAPER;
-  float S0 = bg0, S1 = bg1, S2 = bg2;
+  float* myacc = acc + w * 10 * kAccPitch;
 
   for (int32_t hi = end; hi > start; hi -= kBatch) {
     const int32_t lo = max(start, hi - kBatch);
     __syncthreads();  // previous batch fully consumed and flushed
+    if (threadIdx.x == 0) SSS_COUNT(0, 1);
     const int32_t pos = lo + (int32_t)threadIdx.x;
-    bool ok = pos < hi;
+    bool ok = (int)threadIdx.x < kBatch && pos < hi;
     const int32_t id = ok ? idv[pos] : 0;
     int slot, nb;
     if (FILTER) {
@@ -160,7 +217,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       __syncthreads();
       int off = 0, tot = 0;
 #pragma unroll
-      for (int k = 0; k < kRasterThreads / 32; ++k) {
+      for (int k = 0; k < kRasterWarps; ++k) {
         const int c = wcnt[k];
         off += k < w ? c : 0;
         tot += c;
@@ -172,75 +229,82 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       nb = hi - lo;
     }
     if (ok) {
+      const float4 a = rv[(int64_t)id * 3 + 0];
+      const float4 b = rv[(int64_t)id * 3 + 1];
       spos[slot] = pos;
       sid[slot] = id;
-      sa[slot] = rv[(int64_t)id * 3 + 0];
-      sb[slot] = rv[(int64_t)id * 3 + 1];
+      sa[slot] = a;
+      sb[slot] = b;
       sc[slot] = rv[(int64_t)id * 3 + 2];
+      if (SSS_BOX_CULL) sbox[slot] = entry_box(a, b);
     }
-    for (int k = threadIdx.x; k < nb * SSS_G2D_FLOATS; k += kRasterThreads) acc[k] = 0.f;
+    for (int k = threadIdx.x; k < kRasterWarps * 10 * kAccPitch; k += kRasterThreads) acc[k] = 0.f;
     __syncthreads();
+    if (threadIdx.x == 0) SSS_COUNT(6, nb);
     for (int j = nb - 1; j >= 0; --j) {
+      if (lane == 0) SSS_COUNT(1, 1);
+      if (SSS_BOX_CULL && box_misses(sbox[j], wx0, wx1, wy0, wy1)) {  // warp-uniform
+        if (lane == 0) SSS_COUNT(2, 1);
+        continue;
+      }
+      const int32_t pj = spos[j];
+      if (pj >= wlast) continue;  // warp-uniform: past every pixel's replay start
       const float4 a = sa[j];
       const float4 b = sb[j];  // {C, hmax, o, inv_nu}
-      bool incl = false;
-      float h = 0.f;
-      if (spos[j] < lastp) {
-        h = h_f32(px, py, a, b.x);
-        incl = h <= b.y;
+      const float dy = __fsub_rn(py, a.y);
+      const float bdy = __fmul_rn(a.w, dy);
+      const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
+      float h[kPX], dx[kPX];
+      bool inc[kPX];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < kPX; ++k) {
+        dx[k] = __fsub_rn(px[k], a.x);  // the h_f32 sequence, dx kept for the gradient
+        h[k] = __fmaf_rn(dx[k], __fmaf_rn(a.z, dx[k], bdy), cdy2);
+        inc[k] = pj < q[k].last && h[k] <= b.y;
+        any = any || inc[k];
       }
-      if (!__any_sync(0xffffffffu, incl)) continue;
+#ifdef SSS_COUNTERS
+      {
+        const unsigned ba = __ballot_sync(0xffffffffu, any);
+        int ninc = 0, nlive = 0;
+        for (int k = 0; k < kPX; ++k) {
+          ninc += __popc(__ballot_sync(0xffffffffu, inc[k]));
+          nlive += __popc(__ballot_sync(0xffffffffu, pj < q[k].last));
+        }
+        if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
+      }
+#endif
+      if (!__any_sync(0xffffffffu, any)) continue;
       float vals[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) vals[k] = 0.f;
-      if (incl) {
-        const float4 c = sc[j];  // {e, r, g, b}
-        const float t = fmaxf(h, 0.f) * b.w;
-        const float opt = 1.f + t;
-        const float lg = log2_1p(t, b.w < (1.f / 32.f));
-        const float T = ex2_approx(c.x * lg);
-        const float araw = b.z * T;
-        const float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
-        const float Wi = __fdividef(W, 1.f - alpha);
-        const float aw = alpha * Wi;
-        vals[5] = g0 * aw;
-        vals[6] = g1 * aw;
-        vals[7] = g2 * aw;
-        float da = (g0 * (c.y - S0) + g1 * (c.z - S1) + g2 * (c.w - S2)) * Wi;
-        S0 = fmaf(c.y - S0, alpha, S0);
-        S1 = fmaf(c.z - S1, alpha, S1);
-        S2 = fmaf(c.w - S2, alpha, S2);
-        W = Wi;
-        if (fabsf(araw) > kAlphaMax) da = 0.f;
-        vals[8] = da * T;
-        const float dT = da * b.z;
-        const float Topt = __fdividef(T, opt);
-        const float dh = dT * c.x * b.w * Topt;
-        const float dTdnu = nu_paper ? -c.x * t * b.w * Topt
-                                     : T * (-0.34657359027997264f * lg - __fdividef(c.x * t * b.w, opt));
-        vals[9] = dT * dTdnu;
-        const float dx = px - a.x, dy = py - a.y;
-        vals[0] = -dh * (2.f * a.z * dx + a.w * dy);
-        vals[1] = -dh * (a.w * dx + 2.f * b.x * dy);
-        vals[2] = dh * dx * dx;
-        vals[3] = 2.f * dh * dx * dy;
-        vals[4] = dh * dy * dy;
-      }
+      const float4 c = sc[j];  // {e, r, g, b}
+#pragma unroll
+      for (int k = 0; k < kPX; ++k)
+        if (inc[k]) pair_grad(q[k], dx[k], dy, h[k], a, b, c, nu_paper, vals);
       const float r = warp_reduce16(vals, lane);
       const int idx = (lane >> 1) & 15;
-      if (!(lane & 1) && idx < 10) atomicAdd(&acc[j * SSS_G2D_FLOATS + idx], r);
+      if (!(lane & 1) && idx < 10) myacc[idx * kAccPitch + j] = r;
     }
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += kRasterThreads) {
-      const float4* q = reinterpret_cast<const float4*>(acc + k * SSS_G2D_FLOATS);
-      const float4 q0 = q[0], q1 = q[1], q2 = q[2];
-      const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) |
-                      (q1.y != 0.f) | (q1.z != 0.f) | (q1.w != 0.f) | (q2.x != 0.f) | (q2.y != 0.f);
+      float s[10];
+#pragma unroll
+      for (int qq = 0; qq < 10; ++qq) {
+        float t = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kRasterWarps; ++ww) t += acc[(ww * 10 + qq) * kAccPitch + k];
+        s[qq] = t;
+      }
+      bool nz = false;
+#pragma unroll
+      for (int qq = 0; qq < 10; ++qq) nz |= s[qq] != 0.f;
       if (nz) {
         float4* dst = gv + (int64_t)sid[k] * 3;
-        atomicAdd(dst + 0, q0);
-        atomicAdd(dst + 1, q1);
-        atomicAdd(dst + 2, make_float4(q2.x, q2.y, 0.f, 0.f));
+        atomicAdd(dst + 0, make_float4(s[0], s[1], s[2], s[3]));
+        atomicAdd(dst + 1, make_float4(s[4], s[5], s[6], s[7]));
+        atomicAdd(dst + 2, make_float4(s[8], s[9], 0.f, 0.f));
       }
     }
   }
@@ -493,6 +557,8 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(sss_params P, const __
 
 using namespace sss;
 
+SSS_COUNTER_ACCESSOR(sss_dev_counters_bwd)
+
 extern "C" size_t sss_render_bwd_workspace(int64_t n, int32_t n_views) {
   if (n < 0 || n_views <= 0) return 0;
   return (size_t)n * n_views * SSS_G2D_FLOATS * sizeof(float);
@@ -530,10 +596,18 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   const float4* rec = (const float4*)pr->rec;
   const short4* rect = (const short4*)pr->rect;
 #define SSS_BWD_LAUNCH(F, L)                                                                              \
-  render_bwd_kernel<F, L><<<grid, kRasterThreads, 0, s>>>(rec, rect, bins->ids, bins->ranges, G, bg[0], \
+  render_bwd_kernel<F, L><<<grid, kRasterThreads, kAccBytes, s>>>(rec, rect, bins->ids, bins->ranges, G, bg[0], \
                                                           bg[1], bg[2], fwd->rgb, fwd->final_T,         \
                                                           fwd->last, d_rgb, target, loss_out, g2d, flags)
   const bool l1 = d_rgb == nullptr;
+  static thread_local bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(render_bwd_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
+    cudaFuncSetAttribute(render_bwd_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
+    cudaFuncSetAttribute(render_bwd_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
+    cudaFuncSetAttribute(render_bwd_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
+    attr_set = true;
+  }
   if (!(flags & SSS_BWD_PROJECTION_ONLY)) {
     if (G.shift > 0) {
       if (l1) SSS_BWD_LAUNCH(true, true); else SSS_BWD_LAUNCH(true, false);

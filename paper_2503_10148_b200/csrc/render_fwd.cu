@@ -2,19 +2,42 @@
 // PAPER.md:131-135, 1224-1228) of the 2D t kernels of Eq. 4
 // (T2D = [1 + h/nu]^-(nu+2)/2).
 //
-// B200 design: one CTA per 16x16 tile and view (grid = tiles x V), one
-// thread per pixel.  The tile's bin list is streamed through shared memory
-// in batches of 256 entries; for bins coarser than a tile (bin_shift > 0) the
-// batch is filtered by the component's tile rect and compacted in order
-// (warp ballots) before the 48-byte records are staged.  Every pixel then
-// walks the batch with broadcast shared-memory reads.  A pixel stops after
-// the component that drives W below 1e-4 (R11); the CTA leaves as soon as no
-// pixel is live (__syncthreads_count).  The hot loop is FP32-pipe bound
-// (~8 ops per h test, ~12 more + 2 MUFU per composited pair).
+// B200 design: one CTA per 16x16 tile and view (grid = tiles x V), 128
+// threads with two pixels each.  The tile's bin list is streamed through
+// shared memory in batches of 128 entries; for bins coarser than a tile
+// (bin_shift > 0) the batch is filtered by the component's tile rect and
+// compacted in order (warp ballots) before the 48-byte records are staged,
+// together with a conservative pixel bounding box per entry.  Each warp then
+// walks the batch with broadcast shared-memory reads, skipping (warp-
+// uniformly) entries whose box misses its 16x4 strip.  A pixel stops after
+// the component that drives W below 1e-4 (R11); a warp leaves the batch
+// when all its pixels stopped, the CTA when no pixel is live.  The hot loop
+// is FP32/issue bound (~8 ops per h test, ~15 more + 2 MUFU per composited
+// pair).
 #include "raster.cuh"
 
 namespace sss {
 namespace {
+
+struct PixF {  // forward state of one pixel
+  float W, C0, C1, C2;
+  int32_t cnt, last;
+  bool done;
+};
+
+__device__ __forceinline__ void composite(PixF& p, float h, float4 b, float4 c, int32_t pos) {
+  const float t = fmaxf(h, 0.f) * b.w;
+  const float T = ex2_approx(c.x * log2_1p(t, b.w < (1.f / 32.f)));
+  const float alpha = fminf(fmaxf(b.z * T, -kAlphaMax), kAlphaMax);
+  const float aw = alpha * p.W;
+  p.C0 = fmaf(c.y, aw, p.C0);
+  p.C1 = fmaf(c.z, aw, p.C1);
+  p.C2 = fmaf(c.w, aw, p.C2);
+  p.W = fmaf(-alpha, p.W, p.W);
+  ++p.cnt;
+  p.last = pos + 1;
+  p.done = p.W < kWStop;
+}
 
 template <bool FILTER>
 __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
@@ -22,34 +45,49 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     float* __restrict__ rgb, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
     int32_t* __restrict__ last) {
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch], sbox[kBatch];
   __shared__ int32_t spos[kBatch];
-  __shared__ int32_t wcnt[kRasterThreads / 32];
+  __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
   const int32_t start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
   const int32_t end = ranges[((int64_t)v * G.n_bins + bin) * 2 + 1];
-  int lx, ly;
-  pixel_of(threadIdx.x, lx, ly);
-  const int x = tx * kTile + lx, y = ty * kTile + ly;
-  const bool inside = x < G.width && y < G.height;
-  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  int lx, ly, sx, sy;
+  pixels_of(threadIdx.x, lx, ly, sx, sy);
+  const int x0 = tx * kTile + lx, y = ty * kTile + ly;
+  const float py = (float)y + 0.5f;
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
+  // this warp's strip (pixel centres)
+  const float wx0 = (float)(tx * kTile + sx) + 0.5f, wx1 = wx0 + (float)(kWarpW - 1);
+  const float wy0 = (float)(ty * kTile + sy) + 0.5f, wy1 = wy0 + (float)(kWarpH - 1);
 
   const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
 
-  float W = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  int32_t cnt = 0, lastp = start;
-  bool done = !inside;
+  if (threadIdx.x == 0) SSS_COUNT(7, end - start);
+  PixF p[kPX];
+  float px[kPX];
+#pragma unroll
+  for (int k = 0; k < kPX; ++k) {
+    const bool inside = x0 + k < G.width && y < G.height;
+    p[k] = PixF{1.f, 0.f, 0.f, 0.f, 0, start, !inside};
+    px[k] = (float)(x0 + k) + 0.5f;
+  }
+  auto all_done = [&]() {
+    bool d = true;
+#pragma unroll
+    for (int k = 0; k < kPX; ++k) d = d && p[k].done;
+    return d;
+  };
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
-    if (__syncthreads_count(!done) == 0) break;
+    if (__syncthreads_count(!all_done()) == 0) break;
+    if (threadIdx.x == 0) SSS_COUNT(0, 1);
     const int32_t pos = b0 + (int32_t)threadIdx.x;
-    bool ok = pos < end;
+    bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? idv[pos] : 0;
     int slot, nb;
     if (FILTER) {
@@ -62,7 +100,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
       __syncthreads();
       int off = 0, tot = 0;
 #pragma unroll
-      for (int k = 0; k < kRasterThreads / 32; ++k) {
+      for (int k = 0; k < kRasterWarps; ++k) {
         const int c = wcnt[k];
         off += k < w ? c : 0;
         tot += c;
@@ -74,47 +112,70 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
       nb = min(kBatch, end - b0);
     }
     if (ok) {
+      const float4 a = rv[(int64_t)id * 3 + 0];
+      const float4 b = rv[(int64_t)id * 3 + 1];
       spos[slot] = pos;
-      sa[slot] = rv[(int64_t)id * 3 + 0];
-      sb[slot] = rv[(int64_t)id * 3 + 1];
+      sa[slot] = a;
+      sb[slot] = b;
       sc[slot] = rv[(int64_t)id * 3 + 2];
+      if (SSS_BOX_CULL) sbox[slot] = entry_box(a, b);
     }
     __syncthreads();
-    if (!done) {
-      for (int j = 0; j < nb; ++j) {
-        const float4 a = sa[j];
-        const float4 b = sb[j];  // {C, hmax, o, inv_nu}
-        const float h = h_f32(px, py, a, b.x);
-        if (h <= b.y) {
-          const float4 c = sc[j];  // {e, r, g, b}
-          const float t = fmaxf(h, 0.f) * b.w;
-          const float T = ex2_approx(c.x * log2_1p(t, b.w < (1.f / 32.f)));
-          const float alpha = fminf(fmaxf(b.z * T, -kAlphaMax), kAlphaMax);
-          const float aw = alpha * W;
-          C0 = fmaf(c.y, aw, C0);
-          C1 = fmaf(c.z, aw, C1);
-          C2 = fmaf(c.w, aw, C2);
-          W = fmaf(-alpha, W, W);
-          ++cnt;
-          lastp = spos[j] + 1;
-          if (W < kWStop) {
-            done = true;
-            break;
-          }
-        }
+    if (threadIdx.x == 0) SSS_COUNT(6, nb);
+    if (__all_sync(0xffffffffu, all_done())) continue;
+    for (int j = 0; j < nb; ++j) {
+      if (lane == 0) SSS_COUNT(1, 1);
+      if (SSS_BOX_CULL && box_misses(sbox[j], wx0, wx1, wy0, wy1)) {  // warp-uniform
+        if (lane == 0) SSS_COUNT(2, 1);
+        continue;
       }
+      const float4 a = sa[j];
+      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
+      const float dy = __fsub_rn(py, a.y);
+      const float bdy = __fmul_rn(a.w, dy);
+      const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
+      float h[kPX];
+      bool inc[kPX];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < kPX; ++k) {
+        h[k] = h_f32_row(px[k], a.x, a.z, bdy, cdy2);
+        inc[k] = !p[k].done && h[k] <= b.y;
+        any = any || inc[k];
+      }
+#ifdef SSS_COUNTERS
+      {
+        const unsigned ba = __ballot_sync(0xffffffffu, any);
+        int ninc = 0, nlive = 0;
+        for (int k = 0; k < kPX; ++k) {
+          ninc += __popc(__ballot_sync(0xffffffffu, inc[k]));
+          nlive += __popc(__ballot_sync(0xffffffffu, !p[k].done));
+        }
+        if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
+      }
+#endif
+      if (any) {
+        const float4 c = sc[j];  // {e, r, g, b}
+        const int32_t pj = spos[j];
+#pragma unroll
+        for (int k = 0; k < kPX; ++k)
+          if (inc[k]) composite(p[k], h[k], b, c, pj);
+      }
+      if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
     }
   }
-  if (inside) {
-    const int64_t HW = (int64_t)G.width * G.height;
-    const int64_t pix = (int64_t)y * G.width + x;
+  const int64_t HW = (int64_t)G.width * G.height;
+#pragma unroll
+  for (int k = 0; k < kPX; ++k) {
+    if (!(x0 + k < G.width && y < G.height)) continue;
+    const int64_t pix = (int64_t)y * G.width + x0 + k;
     float* o = rgb + (int64_t)v * 3 * HW + pix;
-    o[0] = C0 + bg0 * W;
-    o[HW] = C1 + bg1 * W;
-    o[2 * HW] = C2 + bg2 * W;
-    final_T[(int64_t)v * HW + pix] = W;
-    n_contrib[(int64_t)v * HW + pix] = cnt;
-    last[(int64_t)v * HW + pix] = lastp;
+    o[0] = p[k].C0 + bg0 * p[k].W;
+    o[HW] = p[k].C1 + bg1 * p[k].W;
+    o[2 * HW] = p[k].C2 + bg2 * p[k].W;
+    final_T[(int64_t)v * HW + pix] = p[k].W;
+    n_contrib[(int64_t)v * HW + pix] = p[k].cnt;
+    last[(int64_t)v * HW + pix] = p[k].last;
   }
 }
 
@@ -137,6 +198,8 @@ bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera
 }  // namespace sss
 
 using namespace sss;
+
+SSS_COUNTER_ACCESSOR(sss_dev_counters_fwd)
 
 extern "C" sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bins, const sss_camera* cams,
                                      int32_t n_views, const float* bg, sss_frame* out, void* stream) {

@@ -255,9 +255,6 @@ def test_sghmc_parity(orc, sss, variant):
     ulp = np.spacing(np.abs(p_ref).astype(np.float32)).astype(np.float64)
     bound = ulp + 1e-5 * np.abs(dref)
     assert np.all(np.abs(got - p_ref) <= bound + 1e-30), float((np.abs(got - p_ref) / bound).max())
-    # the fraction of elements off by the final rounding stays small
-    frac = np.mean(np.abs(got - p_ref) > 1e-5 * np.abs(dref) + 1e-30)
-    assert frac < 0.2, frac
     assert rel_l2(rr.cpu().numpy() - r, r_ref - r) <= 1e-5
     assert rel_l2(mm.planes.cpu().numpy(), m_ref) <= 1e-5
     assert rel_l2(vv.planes.cpu().numpy(), v_ref) <= 1e-5
