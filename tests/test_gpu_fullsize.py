@@ -1,0 +1,178 @@
+"""Parity at BASELINE.json's full sizes, in bench.py's launch configuration.
+
+* config 3 (500k components, 1297x840): every projection record, every tile
+  count, sampled per-tile key lists, the whole image and the whole gradient.
+* configs 4 and 5 (2M / 3M components): two views each, with the bench's
+  16-view launch shape (bin_shift 2) — projection, tile counts and sampled
+  tile lists bit-exact, sampled pixels vs the oracle evaluated pixel by
+  pixel, and gradients of a loss restricted to sampled pixels (the oracle's
+  backward over those pixels is cheap; the GPU runs its full kernels with
+  an image gradient that is zero elsewhere).  Config 5 also checks the
+  SGHMC/Adam step over all 3M components.
+"""
+import numpy as np
+import pytest
+
+from helpers import group_slices, rel_l2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _sample_tiles(n_tiles, k, seed):
+    return np.random.default_rng(seed).choice(n_tiles, size=min(k, n_tiles), replace=False)
+
+
+def _check_lists(orc, sc, v, bins_tile, sample):
+    """bins_tile: GPU bins with bin_shift 0 for view index v (within the launch)."""
+    from gpu_helpers import bin_lists
+
+    cam = sc.cameras[v]
+    tw, th = (cam.width + 15) // 16, (cam.height + 15) // 16
+    ref = orc.tile_lists(sc.params, sc.sh_degree, cam, sample)
+    got = bin_lists(bins_tile, 0, tw * th)
+    for t, r in zip(sample, ref):
+        assert np.array_equal(got[t], r), t
+
+
+def test_config3_full(orc, sss):
+    import torch
+    from gpu_helpers import gpu_forward
+    from test_gpu_parity import _check_frame, _check_projection
+    from sss_synth import make_scene
+
+    sc = make_scene(3)
+    params, pr, bins, fr = gpu_forward(sc, bin_shift=0)
+    o = _check_projection(orc, sc, pr, 0)
+    counts, _, _ = orc.bin_sort(sc.params, 3, sc.cameras[0], want_keys=False)
+    rg = bins.ranges[0].cpu().numpy()
+    assert np.array_equal(rg[:, 1] - rg[:, 0], counts)
+    _check_lists(orc, sc, 0, bins, _sample_tiles(len(counts), 60, 1))
+    ref = orc.render(sc.params, 3, sc.cameras[0], mode="tiled")
+    _check_frame("cfg3", fr.rgb[0].cpu().numpy(), fr.final_T[0].cpu().numpy(),
+                 fr.n_contrib[0].cpu().numpy(), ref)
+    d = np.random.default_rng(3).normal(size=(1, 3, 840, 1297)).astype(np.float32)
+    g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=torch.from_numpy(d).cuda())
+    torch.cuda.synchronize()
+    gref, _ = orc.backward(sc.params, 3, sc.cameras[0], d[0].astype(np.float64), mode="tiled")
+    gg = g.planes.cpu().numpy()
+    for grp, sl in group_slices(3).items():
+        assert rel_l2(gg[sl], gref[sl]) <= 1e-3, grp
+
+
+def _sampled_view_checks(orc, sss, sc, views, n_px=600, seed=0):
+    """Projection, tile counts and lists, sampled pixels and sampled-pixel
+    gradients for `views`, launched together as in the bench (bin_shift 2)."""
+    import torch
+    from gpu_helpers import gpu_forward
+
+    cams = [sc.cameras[v] for v in views]
+    params, pr, bins, fr = gpu_forward(sc, cams=cams, bin_shift=2)
+    # bit-exact per-tile lists need the per-tile binning of the same projection
+    bins0 = sss.sss_bin_sort(pr, cams, bin_shift=0)
+    H, W = cams[0].height, cams[0].width
+    rng = np.random.default_rng(seed)
+    d_full = np.zeros((len(views), 3, H, W), np.float32)
+    refs = []
+    for k, v in enumerate(views):
+        from test_gpu_parity import _check_projection
+        from types import SimpleNamespace
+
+        sub = SimpleNamespace(params=sc.params, sh_degree=sc.sh_degree, cameras=cams)
+        _check_projection(orc, sub, pr, k)
+        counts, _, _ = orc.bin_sort(sc.params, sc.sh_degree, cams[k], want_keys=False)
+        rg = bins0.ranges[k].cpu().numpy()
+        assert np.array_equal(rg[:, 1] - rg[:, 0], counts)
+        _check_lists(orc, SimpleNamespace(params=sc.params, sh_degree=sc.sh_degree, cameras=cams), k,
+                     _SubBins(bins0, k), _sample_tiles(len(counts), 12, seed + k))
+        px = rng.choice(H * W, n_px, replace=False).astype(np.int32)
+        ref = orc.render(sc.params, sc.sh_degree, cams[k], mode="tiled", pixels=px)
+        rgb = fr.rgb[k].reshape(3, -1)[:, px].cpu().numpy()
+        nc = fr.n_contrib[k].reshape(-1)[px].cpu().numpy()
+        mism = nc != ref.n_contrib
+        assert np.all(ref.tie[mism] < 1e-3) and mism.mean() < 0.01
+        assert np.abs(rgb - ref.rgb)[:, ~mism].max() <= 1e-4
+        dsel = rng.normal(size=(3, n_px))
+        d_full[k].reshape(3, -1)[:, px] = dsel
+        refs.append((px, dsel))
+    g = sss.sss_render_bwd(params, pr, bins, cams, fr, d_rgb=torch.from_numpy(d_full).cuda())
+    torch.cuda.synchronize()
+    gref = 0
+    for k, (px, dsel) in enumerate(refs):
+        gref = gref + orc.backward(sc.params, sc.sh_degree, cams[k], dsel, mode="tiled", pixels=px)[0]
+    gg = g.planes.cpu().numpy()
+    for grp, sl in group_slices(sc.sh_degree).items():
+        assert rel_l2(gg[sl], gref[sl]) <= 1e-3, grp
+
+
+class _SubBins:
+    """View k of a multi-view Bins as a 1-view object for bin_lists()."""
+
+    def __init__(self, b, k):
+        self.ids = b.ids[k:k + 1]
+        self.ranges = b.ranges[k:k + 1]
+
+
+@pytest.mark.parametrize("config,views", [(4, [0, 5]), (5, [0, 37])])
+def test_configs_4_5_sampled(orc, sss, config, views):
+    from sss_synth import make_scene
+
+    sc = make_scene(config)
+    _sampled_view_checks(orc, sss, sc, views, seed=config)
+
+
+def test_config5_sghmc_full(orc, sss):
+    import torch
+    from sss_synth import make_optimizer_state, make_scene, sghmc_params_for
+    from test_gpu_parity import _hp32
+
+    sc = make_scene(5)
+    r, m, v = make_optimizer_state(sc, seed=3)
+    rng = np.random.default_rng(5)
+    grad = (rng.normal(size=sc.params.shape) * 1e-2).astype(np.float32)
+    hp = _hp32(sghmc_params_for(sc, step=2, seed=99))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    params = sss.Params(dev(sc.params), 3)
+    mm, vv, rr = sss.Params(dev(m), 3), sss.Params(dev(v), 3), dev(r)
+    sss.sss_sghmc_step(params, sss.Params(dev(grad), 3), mm, vv, rr, hp)
+    torch.cuda.synchronize()
+    p_ref, m_ref, v_ref, r_ref = orc.sghmc_step(sc.params, 3, grad, m, v, r, hp)
+    got = params.planes.cpu().numpy().astype(np.float64)
+    ulp = np.spacing(np.abs(p_ref).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got - p_ref) <= ulp + 1e-5 * np.abs(p_ref - sc.params) + 1e-30)
+    assert rel_l2(rr.cpu().numpy() - r, r_ref - r) <= 1e-5
+    assert rel_l2(mm.planes.cpu().numpy(), m_ref) <= 1e-5
+    assert rel_l2(vv.planes.cpu().numpy(), v_ref) <= 1e-5
+
+
+def test_trainstep_matches_the_abi_sequence(orc, sss):
+    """step.TrainStep (view batches, fused L1, SGHMC) equals the oracle's
+    iteration: sum over views of the L1 backward, grad_scale 1/V, one step."""
+    import torch
+    from paper_2503_10148_b200.step import TrainStep
+    from sss_synth import make_custom_scene, make_targets, sghmc_params_for
+    from test_gpu_parity import _hp32
+
+    sc = make_custom_scene(4000, 2, 96, 80, n_views=5, seed=23, layout="blobs", nu_hi=16.0)
+    tg = make_targets(sc)
+    hp = _hp32(sghmc_params_for(sc, step=1, seed=5, noise=0.0))
+    ts = TrainStep(torch.from_numpy(sc.params).cuda(), 2, sc.cameras, hp, bin_shift=1,
+                   views_per_batch=2)
+    loss = ts.step(torch.from_numpy(tg).cuda())
+    torch.cuda.synchronize()
+    assert not ts.overflowed()
+    g = ts.grad.planes.cpu().numpy()
+    ref = 0
+    lref = 0.0
+    for v, cam in enumerate(sc.cameras):
+        fr = orc.render(sc.params, 2, cam, mode="tiled")
+        l, dl = orc.l1_loss_and_grad(fr.rgb, tg[v])
+        lref += l
+        ref = ref + orc.backward(sc.params, 2, cam, dl, mode="tiled")[0]
+    assert abs(loss.item() - lref) <= 1e-4 * lref
+    for grp, sl in group_slices(2).items():
+        assert rel_l2(g[sl], ref[sl]) <= 2e-3, grp  # L1 sign ties (R20) add a little
+    P, n = sc.params.shape
+    p_ref, _, _, _ = orc.sghmc_step(sc.params, 2, ref, np.zeros((P, n)), np.zeros((P, n)),
+                                    np.zeros((3, n)), hp)
+    got = ts.params.planes.cpu().numpy().astype(np.float64)
+    assert rel_l2(got[3:] - sc.params[3:], p_ref[3:] - sc.params[3:]) <= 5e-3
