@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--bin-shift", type=int, default=2)
-    ap.add_argument("--views-per-batch", type=int, default=16)
+    ap.add_argument("--views-per-batch", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -117,7 +117,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def roofline_for(phase_ms, counts, n, views, pk, steps):
+def ncu_traffic(kernel, views_per_launch):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    capture (profiles/traffic.json), scaled to this run's launch size."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    b = d.get("bytes_per_launch", {}).get(kernel)
+    if b is None:
+        return None
+    return int(b * views_per_launch / d.get("views_per_launch", views_per_launch))
+
+
+def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16):
     """Roofline entry of the dominant kernel (largest share of the timed step)."""
     lane_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6  # FP32 lane-ops/s (DESIGN.md §5)
     hbm_peak = pk["hbm_gbs"] * 1e9
@@ -140,7 +154,9 @@ def roofline_for(phase_ms, counts, n, views, pk, steps):
     achieved = work / t
     return dom, {"kernel": dom, "bound": bound, "achieved": round(achieved / 1e9, 2),
                  "peak": round(peak / 1e9, 2), "unit": unit, "frac": round(achieved / peak, 4),
-                 "traffic": None, "peak_source": pk["source"] + (" (148 SMs x 128 FP32 lanes x sm_max_mhz)" if bound == "alu" else " hbm_gbs"),
+                 "traffic": ncu_traffic(dom, views_per_launch),
+                 "traffic_unit": "dram bytes per launch (ncu --set full, profiles/traffic.json)",
+                 "peak_source": pk["source"] + (" (148 SMs x 128 FP32 lanes x sm_max_mhz)" if bound == "alu" else " hbm_gbs"),
                  "share_of_step": round(phase_ms[dom] / sum(phase_ms.values()), 3)}
 
 
@@ -294,7 +310,8 @@ def main():
     counts = {"pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
               "launches_per_step": len(ts.batches) * a.steps}
     pk = peaks()
-    dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1)
+    dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
+                             views_per_launch=len(ts.batches[0]))
     # ---- end to end through the public API: H2D targets + loss read back
     e2e_steps = a.e2e_steps or a.steps
     host_t = torch.from_numpy(tg_np).pin_memory()

@@ -78,14 +78,18 @@ struct PixB {  // backward state of one pixel
 
 // Adds one composited pair's contribution to vals[0..9] and steps the
 // pixel's replay state (W_i = W_{i+1} / (1 - a_i), suffix colour S).
+// Predicated on `inc`: with a = 0 the replay state is bit-unchanged
+// (W / (1 - 0) = W, S + (c - S) 0 = S) and every contribution is zero, so a
+// warp runs its pixels' chains branch-free.
 __device__ __forceinline__ void pair_grad(PixB& p, float dx, float dy, float h, float4 a, float4 b,
-                                          float4 c, bool nu_paper, float* vals) {
+                                          float4 c, bool nu_paper, float* vals, bool inc) {
   const float t = fmaxf(h, 0.f) * b.w;
   const float opt = 1.f + t;
   const float lg = log2_1p(t, b.w < (1.f / 32.f));
   const float T = ex2_approx(c.x * lg);
   const float araw = b.z * T;
-  const float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
+  float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
+  alpha = inc ? alpha : 0.f;
   const float Wi = __fdividef(p.W, 1.f - alpha);
   const float aw = alpha * Wi;
   vals[5] = fmaf(p.g0, aw, vals[5]);
@@ -96,13 +100,15 @@ __device__ __forceinline__ void pair_grad(PixB& p, float dx, float dy, float h, 
   p.S1 = fmaf(c.z - p.S1, alpha, p.S1);
   p.S2 = fmaf(c.w - p.S2, alpha, p.S2);
   p.W = Wi;
-  if (fabsf(araw) > kAlphaMax) da = 0.f;
+  da = (inc && fabsf(araw) <= kAlphaMax) ? da : 0.f;  // R10: no gradient through the clamp
   vals[8] = fmaf(da, T, vals[8]);
   const float dT = da * b.z;
-  const float Topt = __fdividef(T, opt);
-  const float dh = dT * c.x * b.w * Topt;
-  const float dTdnu = nu_paper ? -c.x * t * b.w * Topt
-                               : T * (-0.34657359027997264f * lg - __fdividef(c.x * t * b.w, opt));
+  const float ropt = rcp_approx(opt);
+  const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
+  const float Topt = T * ropt;
+  const float dh = dT * einu * Topt;
+  const float dTdnu = nu_paper ? -einu * t * Topt
+                               : T * fmaf(-einu * t, ropt, -0.34657359027997264f * lg);
   vals[9] = fmaf(dT, dTdnu, vals[9]);
   const float dhdx = dh * dx, dhdy = dh * dy;
   vals[0] -= 2.f * a.z * dhdx + a.w * dhdy;
@@ -281,8 +287,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       for (int k = 0; k < 16; ++k) vals[k] = 0.f;
       const float4 c = sc[j];  // {e, r, g, b}
 #pragma unroll
-      for (int k = 0; k < kPX; ++k)
-        if (inc[k]) pair_grad(q[k], dx[k], dy, h[k], a, b, c, nu_paper, vals);
+      for (int k = 0; k < kPX; ++k) pair_grad(q[k], dx[k], dy, h[k], a, b, c, nu_paper, vals, inc[k]);
       const float r = warp_reduce16(vals, lane);
       const int idx = (lane >> 1) & 15;
       if (!(lane & 1) && idx < 10) myacc[idx * kAccPitch + j] = r;

@@ -25,17 +25,20 @@ struct PixF {  // forward state of one pixel
   bool done;
 };
 
-__device__ __forceinline__ void composite(PixF& p, float h, float4 b, float4 c, int32_t pos) {
+// One pair of Eq. 7, predicated on `inc` (a = 0 leaves C and W bit-unchanged:
+// C + c*0 = C, W - 0*W = W), so a warp runs its pixels' chains branch-free.
+__device__ __forceinline__ void composite(PixF& p, float h, float4 b, float4 c, int32_t pos, bool inc) {
   const float t = fmaxf(h, 0.f) * b.w;
   const float T = ex2_approx(c.x * log2_1p(t, b.w < (1.f / 32.f)));
-  const float alpha = fminf(fmaxf(b.z * T, -kAlphaMax), kAlphaMax);
+  float alpha = fminf(fmaxf(b.z * T, -kAlphaMax), kAlphaMax);
+  alpha = inc ? alpha : 0.f;
   const float aw = alpha * p.W;
   p.C0 = fmaf(c.y, aw, p.C0);
   p.C1 = fmaf(c.z, aw, p.C1);
   p.C2 = fmaf(c.w, aw, p.C2);
   p.W = fmaf(-alpha, p.W, p.W);
-  ++p.cnt;
-  p.last = pos + 1;
+  p.cnt += inc ? 1 : 0;
+  p.last = inc ? pos + 1 : p.last;
   p.done = p.W < kWStop;
 }
 
@@ -154,12 +157,11 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
         if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
       }
 #endif
-      if (any) {
+      if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
         const float4 c = sc[j];  // {e, r, g, b}
         const int32_t pj = spos[j];
 #pragma unroll
-        for (int k = 0; k < kPX; ++k)
-          if (inc[k]) composite(p[k], h[k], b, c, pj);
+        for (int k = 0; k < kPX; ++k) composite(p[k], h[k], b, c, pj, inc[k]);
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
     }

@@ -1,0 +1,28 @@
+"""Key metrics of an ncu --set full report (raw page) as a small table."""
+import csv, subprocess, sys
+WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
+        ("dram__bytes_write.sum", "dram write"), ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
+        ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
+        ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+        ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+        ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+        ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
+        ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
+        ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+        ("smsp__inst_executed.sum", "warp instructions"),
+        ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads / instr"),
+        ("sm__warps_active.avg.per_cycle_active", "warps active / SM"),
+        ("launch__registers_per_thread", "registers / thread"),
+        ("launch__grid_size", "grid"), ("launch__block_size", "block")]
+for rep in sys.argv[1:]:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    h, u, v = r[0], r[1], r[2]
+    name = v[h.index("Kernel Name")][:90]
+    print(f"### {rep}\n{name}\n")
+    print("| metric | value |\n|---|---|")
+    for k, lab in WANT:
+        if k in h:
+            i = h.index(k)
+            print(f"| {lab} (`{k}`) | {v[i]} {u[i]} |")
+    print()
