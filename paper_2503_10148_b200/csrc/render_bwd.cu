@@ -71,18 +71,30 @@ __device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
 constexpr int kAccPitch = kBatch + 1;  // conflict-free column writes
 constexpr size_t kAccBytes = (size_t)kRasterWarps * 10 * kAccPitch * sizeof(float);
 
-struct PixB {  // backward state of one pixel
-  float W, S0, S1, S2, g0, g1, g2;
+// Backward state of one pixel.  Only the scalar gS = g . S of the suffix
+// colour S is needed: dL/da_i = W_i (g.c_i - g.S_i) and
+// g.S_{i-1} = a_i g.c_i + (1 - a_i) g.S_i.
+struct PixB {
+  float W, gS, g0, g1, g2;
   int32_t last;
 };
 
-// Adds one composited pair's contribution to vals[0..9] and steps the
-// pixel's replay state (W_i = W_{i+1} / (1 - a_i), suffix colour S).
+// Per-thread sums over its pixels for one entry.  The thread's pixels share
+// a row (one dy), so the five screen-space geometry gradients follow from
+// sum dh, sum dh dx and sum dh dx^2:
+//   d mu2D = -(2A sum dh dx + B2 dy sum dh, B2 sum dh dx + 2C dy sum dh),
+//   d(A, B, C) = (sum dh dx^2, 2 dy sum dh dx, dy^2 sum dh).
+struct EntrySums {
+  float sdh, sdhdx, sdhdx2, dc0, dc1, dc2, dO, dnu;
+};
+
+// Adds one composited pair's contribution to the thread's entry sums and
+// steps the pixel's replay state (W_i = W_{i+1} / (1 - a_i), g.S).
 // Predicated on `inc`: with a = 0 the replay state is bit-unchanged
-// (W / (1 - 0) = W, S + (c - S) 0 = S) and every contribution is zero, so a
-// warp runs its pixels' chains branch-free.
-__device__ __forceinline__ void pair_grad(PixB& p, float dx, float dy, float h, float4 a, float4 b,
-                                          float4 c, bool nu_paper, float* vals, bool inc) {
+// (W / (1 - 0) = W, gS + (gc - gS) 0 = gS) and every contribution is zero,
+// so a warp runs its pixels' chains branch-free.
+__device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, float4 c, float einu,
+                                          bool nu_paper, EntrySums& e, bool inc) {
   const float t = fmaxf(h, 0.f) * b.w;
   const float opt = 1.f + t;
   const float lg = log2_1p(t, b.w < (1.f / 32.f));
@@ -92,30 +104,27 @@ __device__ __forceinline__ void pair_grad(PixB& p, float dx, float dy, float h, 
   alpha = inc ? alpha : 0.f;
   const float Wi = __fdividef(p.W, 1.f - alpha);
   const float aw = alpha * Wi;
-  vals[5] = fmaf(p.g0, aw, vals[5]);
-  vals[6] = fmaf(p.g1, aw, vals[6]);
-  vals[7] = fmaf(p.g2, aw, vals[7]);
-  float da = (p.g0 * (c.y - p.S0) + p.g1 * (c.z - p.S1) + p.g2 * (c.w - p.S2)) * Wi;
-  p.S0 = fmaf(c.y - p.S0, alpha, p.S0);
-  p.S1 = fmaf(c.z - p.S1, alpha, p.S1);
-  p.S2 = fmaf(c.w - p.S2, alpha, p.S2);
+  e.dc0 = fmaf(p.g0, aw, e.dc0);
+  e.dc1 = fmaf(p.g1, aw, e.dc1);
+  e.dc2 = fmaf(p.g2, aw, e.dc2);
+  const float gc = fmaf(p.g0, c.y, fmaf(p.g1, c.z, p.g2 * c.w));
+  const float diff = gc - p.gS;
+  float da = diff * Wi;
+  p.gS = fmaf(diff, alpha, p.gS);
   p.W = Wi;
   da = (inc && fabsf(araw) <= kAlphaMax) ? da : 0.f;  // R10: no gradient through the clamp
-  vals[8] = fmaf(da, T, vals[8]);
+  e.dO = fmaf(da, T, e.dO);
   const float dT = da * b.z;
   const float ropt = rcp_approx(opt);
-  const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
   const float Topt = T * ropt;
   const float dh = dT * einu * Topt;
   const float dTdnu = nu_paper ? -einu * t * Topt
                                : T * fmaf(-einu * t, ropt, -0.34657359027997264f * lg);
-  vals[9] = fmaf(dT, dTdnu, vals[9]);
-  const float dhdx = dh * dx, dhdy = dh * dy;
-  vals[0] -= 2.f * a.z * dhdx + a.w * dhdy;
-  vals[1] -= a.w * dhdx + 2.f * b.x * dhdy;
-  vals[2] = fmaf(dhdx, dx, vals[2]);
-  vals[3] = fmaf(2.f * dhdx, dy, vals[3]);
-  vals[4] = fmaf(dhdy, dy, vals[4]);
+  e.dnu = fmaf(dT, dTdnu, e.dnu);
+  const float dhdx = dh * dx;
+  e.sdh += dh;
+  e.sdhdx += dhdx;
+  e.sdhdx2 = fmaf(dhdx, dx, e.sdhdx2);
 }
 
 template <bool FILTER, bool L1>
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   int32_t m = start;
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
-    q[k] = PixB{1.f, bg0, bg1, bg2, 0.f, 0.f, 0.f, start};
+    q[k] = PixB{1.f, 0.f, 0.f, 0.f, 0.f, start};
     px[k] = (float)(x0 + k) + 0.5f;
     if (!(x0 + k < G.width && y < G.height)) continue;
     const int64_t pix = (int64_t)y * G.width + x0 + k;
@@ -174,6 +183,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       q[k].g1 = gimg[HW];
       q[k].g2 = gimg[2 * HW];
     }
+    q[k].gS = fmaf(q[k].g0, bg0, fmaf(q[k].g1, bg1, q[k].g2 * bg2));  // S_n = bg (R12)
   }
   // tile end = max over pixels of `last`; loss partial sums
 #pragma unroll
@@ -282,12 +292,25 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       }
 #endif
       if (!__any_sync(0xffffffffu, any)) continue;
-      float vals[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) vals[k] = 0.f;
       const float4 c = sc[j];  // {e, r, g, b}
+      const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
+      EntrySums es{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k = 0; k < kPX; ++k) pair_grad(q[k], dx[k], dy, h[k], a, b, c, nu_paper, vals, inc[k]);
+      for (int k = 0; k < kPX; ++k) pair_grad(q[k], dx[k], h[k], b, c, einu, nu_paper, es, inc[k]);
+      const float dysdh = dy * es.sdh;
+      float vals[16];
+      vals[0] = -fmaf(2.f * a.z, es.sdhdx, a.w * dysdh);   // d mu2D_x
+      vals[1] = -fmaf(a.w, es.sdhdx, 2.f * b.x * dysdh);   // d mu2D_y
+      vals[2] = es.sdhdx2;                                  // d A
+      vals[3] = 2.f * dy * es.sdhdx;                        // d B (conic_xy)
+      vals[4] = dy * dysdh;                                 // d C
+      vals[5] = es.dc0;
+      vals[6] = es.dc1;
+      vals[7] = es.dc2;
+      vals[8] = es.dO;
+      vals[9] = es.dnu;
+#pragma unroll
+      for (int k = 10; k < 16; ++k) vals[k] = 0.f;
       const float r = warp_reduce16(vals, lane);
       const int idx = (lane >> 1) & 15;
       if (!(lane & 1) && idx < 10) myacc[idx * kAccPitch + j] = r;
