@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
     const bool inside = x0 + k < G.width && y < G.height;
-    p[k] = PixF{1.f, 0.f, 0.f, 0.f, 0, start, !inside};
+    // pixels outside the image start with W = 0: done, and the predicated
+    // composite (done = W < 1e-4) keeps them done (their outputs are unused)
+    p[k] = PixF{inside ? 1.f : 0.f, 0.f, 0.f, 0.f, 0, start, !inside};
     px[k] = (float)(x0 + k) + 0.5f;
   }
   auto all_done = [&]() {
