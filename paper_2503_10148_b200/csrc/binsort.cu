@@ -22,6 +22,9 @@
 namespace sss {
 namespace {
 
+#ifndef SSS_RADIX_MATCH
+#define SSS_RADIX_MATCH 0  // warp peers of a digit: 0 = 8 ballots, 1 = match.any
+#endif
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 keys per CTA
@@ -107,6 +110,9 @@ __global__ void keys_init_kernel(const float* __restrict__ depth, const short4* 
 
 // Positive fp32 depths (> z_near > 0) order like their bit patterns.
 __device__ __forceinline__ unsigned peers_of(unsigned d) {
+#if SSS_RADIX_MATCH
+  return __match_any_sync(0xffffffffu, d);
+#endif
   unsigned m = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
