@@ -182,7 +182,7 @@ def cpu_baseline_sample(scene, targets_np, budget_s, views_total):
     O.lib().orc_bin(pp.ref, ctypes.byref(cc), O._ptr(counts), None, None)  # project + bin
     t_bin = time.time() - t0
     rng = np.random.default_rng(0)
-    npx = 8192
+    npx = 65536  # ~6% of the view: enough pixel work to rise above the re-binning noise
     px = rng.choice(P_, npx, replace=False).astype(np.int32)
     # each oracle call re-projects and re-bins the view; subtract a 1-pixel call
     one = px[:1]
