@@ -449,15 +449,26 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(sss_params P, const __
   float g_o = 0.f, g_nu = 0.f;
   bool any = false;
 
+  // software pipeline: the next view's 48-byte record is in flight while this
+  // view's chain runs (streaming loads: each record is read once)
+  float4 N0 = make_float4(0.f, 0.f, 0.f, 0.f), N1 = N0, N2 = N0;
+  if (nv > 0) {
+    const float4* gp0 = g2d + ((int64_t)v0 * n + i) * 3;
+    N0 = __ldcs(gp0); N1 = __ldcs(gp0 + 1); N2 = __ldcs(gp0 + 2);
+  }
   for (int vv = 0; vv < nv; ++vv) {
     float4* gp = g2d + ((int64_t)(v0 + vv) * n + i) * 3;
-    const float4 G0 = gp[0], G1 = gp[1], G2 = gp[2];
+    const float4 G0 = N0, G1 = N1, G2 = N2;
+    if (vv + 1 < nv) {
+      const float4* gq = gp + (int64_t)n * 3;
+      N0 = __ldcs(gq); N1 = __ldcs(gq + 1); N2 = __ldcs(gq + 2);
+    }
     const bool nz = (G0.x != 0.f) | (G0.y != 0.f) | (G0.z != 0.f) | (G0.w != 0.f) | (G1.x != 0.f) |
                     (G1.y != 0.f) | (G1.z != 0.f) | (G1.w != 0.f) | (G2.x != 0.f) | (G2.y != 0.f);
     if (!nz) continue;
     any = true;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    gp[0] = z4; gp[1] = z4; gp[2] = z4;  // consume-and-clear (workspace stays zero)
+    __stcs(gp, z4); __stcs(gp + 1, z4); __stcs(gp + 2, z4);  // consume-and-clear (workspace stays zero)
     const DevCamera& cam = cp.cam[vv];
     float p[3];
     for (int a = 0; a < 3; ++a) p[a] = cam.R[a * 3 + 0] * mu[0] + cam.R[a * 3 + 1] * mu[1] + cam.R[a * 3 + 2] * mu[2] + cam.t[a];
