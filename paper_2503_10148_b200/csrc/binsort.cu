@@ -32,7 +32,7 @@ constexpr int kScatterThreads = 256;
 constexpr int kScatterWarps = kScatterThreads / 32;
 
 struct BinGeom {
-  int tiles_x, tiles_y, shift, bins_x, bins_y, n_bins;
+  int tiles_x, tiles_y, shift, bins_x, bins_y, n_bins, bits;  // bits: ceil(log2(n_bins))
 };
 
 inline BinGeom bin_geom(const sss_camera& c, int shift) {
@@ -43,6 +43,8 @@ inline BinGeom bin_geom(const sss_camera& c, int shift) {
   g.bins_x = div_up(g.tiles_x, 1 << shift);
   g.bins_y = div_up(g.tiles_y, 1 << shift);
   g.n_bins = g.bins_x * g.bins_y;
+  g.bits = 1;
+  while ((1 << g.bits) < g.n_bins) ++g.bits;
   return g;
 }
 
@@ -330,13 +332,25 @@ __device__ __forceinline__ void warp_instances(const int32_t* __restrict__ sid, 
                                                int32_t* __restrict__ idv, uint64_t* __restrict__ kv) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
+  // software pipeline: the next group's (id, rect) gathers are in flight
+  // while the current group's instances are placed
+  int id_n = 0;
+  short4 r_n = make_short4(1, 1, 0, 0);
+  if (wlo + lane < whi) {
+    id_n = sid[wlo + lane];
+    r_n = rv[id_n];
+  }
   for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
     const int64_t j = j0 + lane;
-    int id = 0, bx0 = 0, by0 = 0, bw = 1, nb = 0;
+    const int id = id_n;
+    const short4 r = r_n;
+    if (j + 32 < whi) {
+      id_n = sid[j + 32];
+      r_n = rv[id_n];
+    }
+    int bx0 = 0, by0 = 0, bw = 1, nb = 0;
     uint32_t dbits = 0;
     if (j < whi) {
-      id = sid[j];
-      const short4 r = rv[id];
       bx0 = r.x >> g.shift;
       by0 = r.y >> g.shift;
       bw = (r.z >> g.shift) - bx0 + 1;
@@ -366,7 +380,14 @@ __device__ __forceinline__ void warp_instances(const int32_t* __restrict__ sid, 
       const int kby0 = __shfl_sync(0xffffffffu, by0, k);
       const int row = t / kbw;
       const int b = (kby0 + row) * g.bins_x + kbx0 + (t - row * kbw);
-      const unsigned peers = __match_any_sync(0xffffffffu, act ? b : -1 - lane);
+      // lanes of this step with the same bin (ballots on its bits; cheaper
+      // than match.any on sm_100)
+      unsigned peers = __ballot_sync(0xffffffffu, act);
+      for (int i = 0; i < g.bits; ++i) {
+        const bool bit = (b >> i) & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+      }
       const int rank = __popc(peers & lt);
       if (!COUNT) {
         const int kid = __shfl_sync(0xffffffffu, id, k);
@@ -511,13 +532,13 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
                                             out->overflow);
   count_launch();
   if (n > 0) {
-    const size_t ssm = (size_t)g.n_bins * 4 + (size_t)kScatterWarps * g.n_bins * 2;
     static thread_local bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_set = true;
     }
+    const size_t ssm = (size_t)g.n_bins * 4 + (size_t)kScatterWarps * g.n_bins * 2;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
         vals_a, n_vis, rect, pr->depth, n, L.chunk, L.n_chunks, g, chist, bstart, out->totals,
         out->capacity, out->ids, out->keys);
