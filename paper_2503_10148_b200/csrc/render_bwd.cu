@@ -35,37 +35,30 @@
 namespace sss {
 namespace {
 
-// 16-value butterfly reduce-scatter: returns, in lane L, the warp sum of
-// value index (L >> 1) & 15.
-__device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
+// 10-value butterfly reduce-scatter (12 shuffles): returns, in lane L, the
+// warp sum of value index idx (idx < 0: L holds nothing).  Both lanes of an
+// even/odd pair hold the same sum.
+__device__ __forceinline__ float warp_reduce10(const float* v, int lane, int& idx) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  float a[5];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const bool up = lane & 16;
-    const float send = up ? v[k] : v[k + 8];
-    const float keep = up ? v[k + 8] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  for (int k = 0; k < 5; ++k) {  // xor 16: keep index k + 5 b4
+    const float send = b4 ? v[k] : v[k + 5];
+    const float keep = b4 ? v[k + 5] : v[k];
+    a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const bool up = lane & 8;
-    const float send = up ? v[k] : v[k + 4];
-    const float keep = up ? v[k + 4] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const bool up = lane & 4;
-    const float send = up ? v[k] : v[k + 2];
-    const float keep = up ? v[k + 2] : v[k];
-    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const bool up = lane & 2;
-    const float send = up ? v[0] : v[1];
-    const float keep = up ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  // xor 8: b3 = 0 keeps (0, 1, 2), b3 = 1 keeps (3, 4)
+  const float c0 = (b3 ? a[3] : a[0]) + __shfl_xor_sync(0xffffffffu, b3 ? a[0] : a[3], 8);
+  const float c1 = (b3 ? a[4] : a[1]) + __shfl_xor_sync(0xffffffffu, b3 ? a[1] : a[4], 8);
+  const float c2 = (b3 ? 0.f : a[2]) + __shfl_xor_sync(0xffffffffu, b3 ? a[2] : 0.f, 8);
+  // xor 4: b2 = 0 keeps (c0, c1), b2 = 1 keeps (c2)
+  const float d0 = (b2 ? c2 : c0) + __shfl_xor_sync(0xffffffffu, b2 ? c0 : c2, 4);
+  const float d1 = (b2 ? 0.f : c1) + __shfl_xor_sync(0xffffffffu, b2 ? c1 : 0.f, 4);
+  // xor 2, xor 1
+  const float e = (b1 ? d1 : d0) + __shfl_xor_sync(0xffffffffu, b1 ? d0 : d1, 2);
+  const int sub = b3 ? (b2 ? -1 : 3 + (b1 ? 1 : 0)) : (b2 ? (b1 ? -1 : 2) : (b1 ? 1 : 0));
+  idx = sub < 0 ? -1 : 5 * (b4 ? 1 : 0) + sub;
+  return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
 constexpr int kAccPitch = kBatch + 1;  // conflict-free column writes
@@ -93,8 +86,9 @@ struct EntrySums {
 // Predicated on `inc`: with a = 0 the replay state is bit-unchanged
 // (W / (1 - 0) = W, gS + (gc - gS) 0 = gS) and every contribution is zero,
 // so a warp runs its pixels' chains branch-free.
+template <bool NU_PAPER>
 __device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, float4 c, float einu,
-                                          bool nu_paper, EntrySums& e, bool inc) {
+                                          EntrySums& e, bool inc) {
   const float t = fmaxf(h, 0.f) * b.w;
   const float opt = 1.f + t;
   const float lg = log2_1p(t, b.w < (1.f / 32.f));
@@ -102,7 +96,7 @@ __device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, 
   const float araw = b.z * T;
   float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
   alpha = inc ? alpha : 0.f;
-  const float Wi = __fdividef(p.W, 1.f - alpha);
+  const float Wi = p.W * rcp_approx(1.f - alpha);  // 1 - a >= 0.01 (R10): no range fix-up
   const float aw = alpha * Wi;
   e.dc0 = fmaf(p.g0, aw, e.dc0);
   e.dc1 = fmaf(p.g1, aw, e.dc1);
@@ -118,7 +112,7 @@ __device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, 
   const float ropt = rcp_approx(opt);
   const float Topt = T * ropt;
   const float dh = dT * einu * Topt;
-  const float dTdnu = nu_paper ? -einu * t * Topt
+  const float dTdnu = NU_PAPER ? -einu * t * Topt
                                : T * fmaf(-einu * t, ropt, -0.34657359027997264f * lg);
   e.dnu = fmaf(dT, dTdnu, e.dnu);
   const float dhdx = dh * dx;
@@ -127,13 +121,13 @@ __device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, 
   e.sdhdx2 = fmaf(dhdx, dx, e.sdhdx2);
 }
 
-template <bool FILTER, bool L1>
+template <bool FILTER, bool L1, bool NUP>
 __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
     const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
-    float4* __restrict__ g2d, int flags) {
+    float4* __restrict__ g2d) {
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch], sbox[kBatch];
   __shared__ int32_t spos[kBatch], sid[kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
@@ -212,7 +206,6 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
   float4* gv = g2d + (int64_t)v * G.n * 3;
-  const bool nu_paper = flags & SSS_BWD_NU_GRAD_PAPER;
   float* myacc = acc + w * 10 * kAccPitch;
 
   for (int32_t hi = end; hi > start; hi -= kBatch) {
@@ -296,9 +289,9 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
       EntrySums es{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k = 0; k < kPX; ++k) pair_grad(q[k], dx[k], h[k], b, c, einu, nu_paper, es, inc[k]);
+      for (int k = 0; k < kPX; ++k) pair_grad<NUP>(q[k], dx[k], h[k], b, c, einu, es, inc[k]);
       const float dysdh = dy * es.sdh;
-      float vals[16];
+      float vals[10];
       vals[0] = -fmaf(2.f * a.z, es.sdhdx, a.w * dysdh);   // d mu2D_x
       vals[1] = -fmaf(a.w, es.sdhdx, 2.f * b.x * dysdh);   // d mu2D_y
       vals[2] = es.sdhdx2;                                  // d A
@@ -309,11 +302,9 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       vals[7] = es.dc2;
       vals[8] = es.dO;
       vals[9] = es.dnu;
-#pragma unroll
-      for (int k = 10; k < 16; ++k) vals[k] = 0.f;
-      const float r = warp_reduce16(vals, lane);
-      const int idx = (lane >> 1) & 15;
-      if (!(lane & 1) && idx < 10) myacc[idx * kAccPitch + j] = r;
+      int idx;
+      const float r = warp_reduce10(vals, lane, idx);
+      if (!(lane & 1) && idx >= 0) myacc[idx * kAccPitch + j] = r;
     }
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += kRasterThreads) {
@@ -634,28 +625,27 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   const dim3 grid(G.tiles_x * G.tiles_y, n_views);
   const float4* rec = (const float4*)pr->rec;
   const short4* rect = (const short4*)pr->rect;
-#define SSS_BWD_LAUNCH(F, L)                                                                              \
-  render_bwd_kernel<F, L><<<grid, kRasterThreads, kAccBytes, s>>>(rec, rect, bins->ids, bins->ranges, G, bg[0], \
-                                                          bg[1], bg[2], fwd->rgb, fwd->final_T,         \
-                                                          fwd->last, d_rgb, target, loss_out, g2d, flags)
+#define SSS_BWD_LAUNCH(F, L, N)                                                                     \
+  render_bwd_kernel<F, L, N><<<grid, kRasterThreads, kAccBytes, s>>>(                              \
+      rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last, \
+      d_rgb, target, loss_out, g2d)
+#define SSS_BWD_LAUNCH_N(F, L)              \
+  do {                                      \
+    if (nup) SSS_BWD_LAUNCH(F, L, true);    \
+    else SSS_BWD_LAUNCH(F, L, false);       \
+  } while (0)
   const bool l1 = d_rgb == nullptr;
-  static thread_local bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(render_bwd_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
-    cudaFuncSetAttribute(render_bwd_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
-    cudaFuncSetAttribute(render_bwd_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
-    cudaFuncSetAttribute(render_bwd_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccBytes);
-    attr_set = true;
-  }
+  const bool nup = flags & SSS_BWD_NU_GRAD_PAPER;
   if (!(flags & SSS_BWD_PROJECTION_ONLY)) {
     if (G.shift > 0) {
-      if (l1) SSS_BWD_LAUNCH(true, true); else SSS_BWD_LAUNCH(true, false);
+      if (l1) SSS_BWD_LAUNCH_N(true, true); else SSS_BWD_LAUNCH_N(true, false);
     } else {
-      if (l1) SSS_BWD_LAUNCH(false, true); else SSS_BWD_LAUNCH(false, false);
+      if (l1) SSS_BWD_LAUNCH_N(false, true); else SSS_BWD_LAUNCH_N(false, false);
     }
     count_launch();
     if ((st = check_launch("sss_render_bwd(raster)")) != SSS_OK) return st;
   }
+#undef SSS_BWD_LAUNCH_N
 #undef SSS_BWD_LAUNCH
   if (p->n == 0 || (flags & SSS_BWD_RASTER_ONLY)) return SSS_OK;
   const int threads = 128;
