@@ -5,14 +5,11 @@
 namespace sss {
 
 // A CTA renders one 16x16 tile of one view; each thread owns kPX horizontally
-// adjacent pixels, a warp an (8 kPX) x 4 strip.  With kPX = 2 the per-entry
-// shared-memory loads, the warp culling test and (backward) the warp
-// reduction are amortised over 64 pixels instead of 32.
+// adjacent pixels (a warp a 16 x 32/(16/kPX) strip).  With kPX = 4 the
+// per-entry shared-memory loads, the warp inclusion test and (backward) the
+// warp reduction are amortised over 128 pixels instead of 32.
 #ifndef SSS_RASTER_PX
 #define SSS_RASTER_PX 4
-#endif
-#ifndef SSS_BOX_CULL
-#define SSS_BOX_CULL 0
 #endif
 constexpr int kPX = SSS_RASTER_PX;
 static_assert(kPX == 1 || kPX == 2 || kPX == 4, "1, 2 or 4 pixels per thread");
@@ -91,30 +88,6 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // lanes evaluate the same component).
 __device__ __forceinline__ float log2_1p(float t, bool precise) {
   return precise ? log1pf(t) * 1.4426950408889634f : lg2_approx(1.0f + t);
-}
-
-// Conservative pixel-centre bounding box of {h_f32 <= hmax} for warp-level
-// culling: x in [box.x, box.y], y in [box.z, box.w].  The half-extents
-// sqrt(hmax Sigma_xx), sqrt(hmax Sigma_yy) get a 1-pixel margin; for
-// ill-conditioned conics (where fp32 cancellation in h could exceed the
-// margin) the box is unbounded, i.e. no culling.
-__device__ __forceinline__ float4 entry_box(float4 a, float4 b) {
-  const float A = a.z, B = 0.5f * a.w, C = b.x;
-  const float det = A * C - B * B;
-  const float INF = __int_as_float(0x7f800000);
-  if (!(det > 0.01f * A * C) || !(A > 0.f) || !(C > 0.f)) return make_float4(-INF, INF, -INF, INF);
-  const float ex = sqrtf(b.y * C / det) + 1.0f;
-  const float ey = sqrtf(b.y * A / det) + 1.0f;
-  if (!(ex < 1e30f) || !(ey < 1e30f)) return make_float4(-INF, INF, -INF, INF);
-  return make_float4(a.x - ex, a.x + ex, a.y - ey, a.y + ey);
-}
-
-__device__ __forceinline__ bool box_misses(float4 bx, float x0, float x1, float y0, float y1) {
-#if SSS_BOX_CULL
-  return bx.y < x0 || bx.x > x1 || bx.w < y0 || bx.z > y1;
-#else
-  return false;
-#endif
 }
 
 }  // namespace sss

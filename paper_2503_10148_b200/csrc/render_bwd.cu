@@ -2,7 +2,7 @@
 // "Backward Pass") to the six parameter groups
 // (PAPER.md:165).
 //
-// a4 raster backward.  One CTA per tile and view, 128 threads with two
+// a4 raster backward.  One CTA per tile and view, 64 threads with four
 // pixels each, replaying the tile's bin list back to front from the last
 // composited entry (the forward's `last`).  Per pair (PAPER.md:1230-1268
 // chain, R10, R13):
@@ -12,13 +12,14 @@
 //   dT/dh = -(nu+2)/(2 nu) T / (1 + h/nu)
 //   dT/dnu = T [-1/2 ln(1 + h/nu) + (nu+2) h / (2 nu^2 (1 + h/nu))]  (R13)
 //   dh/dmu2D = -2 Q d,  dh/d(A, B, C) = (dx^2, 2 dx dy, dy^2).
-// A thread sums its two pixels' 10 per-pair values, the warp reduces them
-// with a 16-lane butterfly reduce-scatter (16 shuffles for 10 values instead
-// of 50), warps whose 16x4 strip misses the entry's box or whose lanes are
-// all excluded skip it (warp-uniform), each warp stores its partial sums in
-// its own shared-memory slot (no shared atomics), and after the batch one
-// vector RED per (component, tile) adds the 4 warps' sums to the
-// screen-space gradient record g2d[v][i] (48 B) in the workspace.
+// The replay keeps only W and the scalar g.S per pixel; a thread sums its
+// four pixels' contributions (the five geometry gradients from three row
+// sums), the warp reduces the 10 values with a butterfly reduce-scatter (12
+// shuffles instead of 50), warps whose pixels are all past their replay
+// start or all excluded skip the entry (warp-uniform), each warp stores its
+// partial sums in its own shared-memory slot (no shared atomics), and after
+// the batch one 3 x float4 RED per (component, tile) adds the warps' sums to
+// the screen-space gradient record g2d[v][i] (48 B) in the workspace.
 //
 // a6: with target != NULL the L1 image gradient sign(C - target)/(3HW) is
 // formed in the same kernel (no image-gradient buffer) and the loss summed.
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
     float4* __restrict__ g2d) {
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch], sbox[kBatch];
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
   __shared__ int32_t spos[kBatch], sid[kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
   __shared__ float wred[kRasterWarps];
@@ -145,8 +146,6 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   const float py = (float)y + 0.5f;
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  const float wx0 = (float)(tx * kTile + sx) + 0.5f, wx1 = wx0 + (float)(kWarpW - 1);
-  const float wy0 = (float)(ty * kTile + sy) + 0.5f, wy1 = wy0 + (float)(kWarpH - 1);
   const int64_t HW = (int64_t)G.width * G.height;
   const float inv3P = 1.0f / (3.0f * (float)HW);
 
@@ -238,24 +237,17 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       nb = hi - lo;
     }
     if (ok) {
-      const float4 a = rv[(int64_t)id * 3 + 0];
-      const float4 b = rv[(int64_t)id * 3 + 1];
       spos[slot] = pos;
       sid[slot] = id;
-      sa[slot] = a;
-      sb[slot] = b;
+      sa[slot] = rv[(int64_t)id * 3 + 0];
+      sb[slot] = rv[(int64_t)id * 3 + 1];
       sc[slot] = rv[(int64_t)id * 3 + 2];
-      if (SSS_BOX_CULL) sbox[slot] = entry_box(a, b);
     }
     for (int k = threadIdx.x; k < kRasterWarps * 10 * kAccPitch; k += kRasterThreads) acc[k] = 0.f;
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     for (int j = nb - 1; j >= 0; --j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      if (SSS_BOX_CULL && box_misses(sbox[j], wx0, wx1, wy0, wy1)) {  // warp-uniform
-        if (lane == 0) SSS_COUNT(2, 1);
-        continue;
-      }
       const int32_t pj = spos[j];
       if (pj >= wlast) continue;  // warp-uniform: past every pixel's replay start
       const float4 a = sa[j];

@@ -2,18 +2,21 @@
 // PAPER.md:131-135, 1224-1228) of the 2D t kernels of Eq. 4
 // (T2D = [1 + h/nu]^-(nu+2)/2).
 //
-// B200 design: one CTA per 16x16 tile and view (grid = tiles x V), 128
-// threads with two pixels each.  The tile's bin list is streamed through
-// shared memory in batches of 128 entries; for bins coarser than a tile
-// (bin_shift > 0) the batch is filtered by the component's tile rect and
-// compacted in order (warp ballots) before the 48-byte records are staged,
-// together with a conservative pixel bounding box per entry.  Each warp then
-// walks the batch with broadcast shared-memory reads, skipping (warp-
-// uniformly) entries whose box misses its 16x4 strip.  A pixel stops after
-// the component that drives W below 1e-4 (R11); a warp leaves the batch
-// when all its pixels stopped, the CTA when no pixel is live.  The hot loop
-// is FP32/issue bound (~8 ops per h test, ~15 more + 2 MUFU per composited
-// pair).
+// B200 design: one CTA per 16x16 tile and view (grid = tiles x V), 64
+// threads with kPX = 4 horizontally adjacent pixels each (a warp owns a
+// 16x8 strip), so per-entry shared-memory loads and loop overhead are shared
+// by four pixels.  The tile's bin list is streamed through shared memory in
+// batches of 64 entries; for bins coarser than a tile (bin_shift > 0) the
+// batch is filtered by the component's tile rect and compacted in order
+// (warp ballots) before the 48-byte records are staged.  Each warp walks the
+// batch with broadcast shared-memory reads; when any of its pixels is hit the
+// four pixel chains run predicated (branch-free).  A pixel stops after the
+// component that drives W below 1e-4 (R11); a warp leaves the batch when all
+// its pixels stopped, the CTA when no pixel is live.  The hot loop is
+// FP32-issue bound (~8 ops per h test, ~17 more + 2 MUFU per composited
+// pair).  (Measured and rejected: per-warp bounding-box or exact ellipse-
+// strip culling — the warps of a tile then drift apart at the batch barrier —
+// and register prefetching of the next batch.)
 #include "raster.cuh"
 
 namespace sss {
@@ -48,7 +51,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     float* __restrict__ rgb, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
     int32_t* __restrict__ last) {
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch], sbox[kBatch];
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
   __shared__ int32_t spos[kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
@@ -63,9 +66,6 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
   const float py = (float)y + 0.5f;
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  // this warp's strip (pixel centres)
-  const float wx0 = (float)(tx * kTile + sx) + 0.5f, wx1 = wx0 + (float)(kWarpW - 1);
-  const float wy0 = (float)(ty * kTile + sy) + 0.5f, wy1 = wy0 + (float)(kWarpH - 1);
 
   const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
@@ -117,23 +117,16 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
       nb = min(kBatch, end - b0);
     }
     if (ok) {
-      const float4 a = rv[(int64_t)id * 3 + 0];
-      const float4 b = rv[(int64_t)id * 3 + 1];
       spos[slot] = pos;
-      sa[slot] = a;
-      sb[slot] = b;
+      sa[slot] = rv[(int64_t)id * 3 + 0];
+      sb[slot] = rv[(int64_t)id * 3 + 1];
       sc[slot] = rv[(int64_t)id * 3 + 2];
-      if (SSS_BOX_CULL) sbox[slot] = entry_box(a, b);
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     if (__all_sync(0xffffffffu, all_done())) continue;
     for (int j = 0; j < nb; ++j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      if (SSS_BOX_CULL && box_misses(sbox[j], wx0, wx1, wy0, wy1)) {  // warp-uniform
-        if (lane == 0) SSS_COUNT(2, 1);
-        continue;
-      }
       const float4 a = sa[j];
       const float4 b = sb[j];  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
