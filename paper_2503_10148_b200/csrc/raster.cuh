@@ -12,11 +12,12 @@ namespace sss {
 #define SSS_RASTER_PX 4
 #endif
 constexpr int kPX = SSS_RASTER_PX;
-static_assert(kPX == 1 || kPX == 2 || kPX == 4, "1, 2 or 4 pixels per thread");
+static_assert(kPX == 2 || kPX == 4, "2 or 4 pixels per thread (processed as pairs)");
+constexpr int kPairs = kPX / 2;
 constexpr int kRasterThreads = 256 / kPX;
 constexpr int kRasterWarps = kRasterThreads / 32;
 constexpr int kBatch = kRasterThreads < 128 ? kRasterThreads : 128;  // entries per smem batch
-constexpr int kWarpW = kPX == 1 ? 8 : 16;         // warp strip: 8x4, 16x4 or 16x8 pixels
+constexpr int kWarpW = 16;                        // warp strip: 16x4 or 16x8 pixels
 constexpr int kWarpH = 32 * kPX / kWarpW;
 constexpr int kLanesPerRow = kWarpW / kPX;
 constexpr int kWarpsPerRow = 16 / kWarpW;
@@ -64,6 +65,23 @@ __device__ __forceinline__ void pixels_of(int tid, int& lx, int& ly, int& sx, in
 __device__ __forceinline__ float h_f32_row(float px, float mx, float A, float bdy, float cdy2) {
   const float dx = __fsub_rn(px, mx);
   return __fmaf_rn(dx, __fmaf_rn(A, dx, bdy), cdy2);
+}
+
+// Packed FP32x2 arithmetic (FADD2 / FMUL2 / FFMA2, sm_100): a thread's pixels
+// are processed as horizontally adjacent pairs, so one issue slot does the
+// work of two scalar instructions.  Each lane of a packed op is the IEEE
+// round-to-nearest result of the scalar op, never contracted.
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// h_f32_row for a pixel pair (same three rounded operations per lane), also
+// returning dx.
+__device__ __forceinline__ float2 h_f32_pair(float2 px, float mx, float A, float bdy, float cdy2, float2& dx) {
+  dx = __fadd2_rn(px, bc2(-mx));
+  return __ffma2_rn(dx, __ffma2_rn(bc2(A), dx, bc2(bdy)), bc2(cdy2));
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

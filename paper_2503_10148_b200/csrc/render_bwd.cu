@@ -65,61 +65,74 @@ __device__ __forceinline__ float warp_reduce10(const float* v, int lane, int& id
 constexpr int kAccPitch = kBatch + 1;  // conflict-free column writes
 constexpr size_t kAccBytes = (size_t)kRasterWarps * 10 * kAccPitch * sizeof(float);
 
-// Backward state of one pixel.  Only the scalar gS = g . S of the suffix
-// colour S is needed: dL/da_i = W_i (g.c_i - g.S_i) and
-// g.S_{i-1} = a_i g.c_i + (1 - a_i) g.S_i.
-struct PixB {
-  float W, gS, g0, g1, g2;
-  int32_t last;
+// Backward state of a horizontally adjacent pixel pair (packed FP32x2).
+// Only the scalar gS = g . S of the suffix colour S is needed:
+// dL/da_i = W_i (g.c_i - g.S_i) and g.S_{i-1} = a_i g.c_i + (1 - a_i) g.S_i.
+struct PixB2 {
+  float2 W, gS, g0, g1, g2;
 };
 
-// Per-thread sums over its pixels for one entry.  The thread's pixels share
-// a row (one dy), so the five screen-space geometry gradients follow from
-// sum dh, sum dh dx and sum dh dx^2:
+// Per-thread sums over its pixels for one entry (lane-wise over the pairs;
+// the two lanes are added once per entry).  The thread's pixels share a row
+// (one dy), so the five screen-space geometry gradients follow from sum dh,
+// sum dh dx and sum dh dx^2:
 //   d mu2D = -(2A sum dh dx + B2 dy sum dh, B2 sum dh dx + 2C dy sum dh),
 //   d(A, B, C) = (sum dh dx^2, 2 dy sum dh dx, dy^2 sum dh).
-struct EntrySums {
-  float sdh, sdhdx, sdhdx2, dc0, dc1, dc2, dO, dnu;
+struct EntrySums2 {
+  float2 sdh, sdhdx, sdhdx2, dc0, dc1, dc2, dO, dnu;
 };
 
-// Adds one composited pair's contribution to the thread's entry sums and
-// steps the pixel's replay state (W_i = W_{i+1} / (1 - a_i), g.S).
-// Predicated on `inc`: with a = 0 the replay state is bit-unchanged
-// (W / (1 - 0) = W, gS + (gc - gS) 0 = gS) and every contribution is zero,
-// so a warp runs its pixels' chains branch-free.
+__device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v.y : v.x; }
+
+// Adds one composited pair's contribution (for both pixels of a pixel pair)
+// to the thread's entry sums and steps the replay state (W_i = W_{i+1} /
+// (1 - a_i), g.S).  Predicated per pixel on `inc`: with a = 0 the replay
+// state is bit-unchanged (W / (1 - 0) = W, gS + (gc - gS) 0 = gS) and every
+// contribution is zero, so a warp runs its pixels' chains branch-free.
 template <bool NU_PAPER>
-__device__ __forceinline__ void pair_grad(PixB& p, float dx, float h, float4 b, float4 c, float einu,
-                                          EntrySums& e, bool inc) {
-  const float t = fmaxf(h, 0.f) * b.w;
-  const float opt = 1.f + t;
-  const float lg = log2_1p(t, b.w < (1.f / 32.f));
-  const float T = ex2_approx(c.x * lg);
-  const float araw = b.z * T;
-  float alpha = fminf(fmaxf(araw, -kAlphaMax), kAlphaMax);
-  alpha = inc ? alpha : 0.f;
-  const float Wi = p.W * rcp_approx(1.f - alpha);  // 1 - a >= 0.01 (R10): no range fix-up
-  const float aw = alpha * Wi;
-  e.dc0 = fmaf(p.g0, aw, e.dc0);
-  e.dc1 = fmaf(p.g1, aw, e.dc1);
-  e.dc2 = fmaf(p.g2, aw, e.dc2);
-  const float gc = fmaf(p.g0, c.y, fmaf(p.g1, c.z, p.g2 * c.w));
-  const float diff = gc - p.gS;
-  float da = diff * Wi;
-  p.gS = fmaf(diff, alpha, p.gS);
+__device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4 b, float4 c, float einu,
+                                           EntrySums2& e, bool inc0, bool inc1) {
+  const float2 t = mul2(make_float2(fmaxf(h.x, 0.f), fmaxf(h.y, 0.f)), bc2(b.w));
+  const float2 opt = add2(t, bc2(1.f));
+  float2 lg;
+  if (b.w < (1.f / 32.f)) {  // warp-uniform (see log2_1p)
+    lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+  } else {
+    lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+  }
+  const float2 ex = mul2(lg, bc2(c.x));
+  const float2 T = make_float2(ex2_approx(ex.x), ex2_approx(ex.y));
+  const float2 araw = mul2(T, bc2(b.z));
+  float2 alpha;
+  alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
+  alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
+  const float2 oma = sub2(bc2(1.f), alpha);  // 1 - a >= 0.01 (R10): no range fix-up
+  const float2 Wi = mul2(p.W, make_float2(rcp_approx(oma.x), rcp_approx(oma.y)));
+  const float2 aw = mul2(alpha, Wi);
+  e.dc0 = fma2(p.g0, aw, e.dc0);
+  e.dc1 = fma2(p.g1, aw, e.dc1);
+  e.dc2 = fma2(p.g2, aw, e.dc2);
+  const float2 gc = fma2(p.g0, bc2(c.y), fma2(p.g1, bc2(c.z), mul2(p.g2, bc2(c.w))));
+  const float2 diff = sub2(gc, p.gS);
+  float2 da = mul2(diff, Wi);
+  p.gS = fma2(diff, alpha, p.gS);
   p.W = Wi;
-  da = (inc && fabsf(araw) <= kAlphaMax) ? da : 0.f;  // R10: no gradient through the clamp
-  e.dO = fmaf(da, T, e.dO);
-  const float dT = da * b.z;
-  const float ropt = rcp_approx(opt);
-  const float Topt = T * ropt;
-  const float dh = dT * einu * Topt;
-  const float dTdnu = NU_PAPER ? -einu * t * Topt
-                               : T * fmaf(-einu * t, ropt, -0.34657359027997264f * lg);
-  e.dnu = fmaf(dT, dTdnu, e.dnu);
-  const float dhdx = dh * dx;
-  e.sdh += dh;
-  e.sdhdx += dhdx;
-  e.sdhdx2 = fmaf(dhdx, dx, e.sdhdx2);
+  // R10: no gradient through the clamp
+  da.x = (inc0 && fabsf(araw.x) <= kAlphaMax) ? da.x : 0.f;
+  da.y = (inc1 && fabsf(araw.y) <= kAlphaMax) ? da.y : 0.f;
+  e.dO = fma2(da, T, e.dO);
+  const float2 dT = mul2(da, bc2(b.z));
+  const float2 ropt = make_float2(rcp_approx(opt.x), rcp_approx(opt.y));
+  const float2 Topt = mul2(T, ropt);
+  const float2 dh = mul2(mul2(dT, bc2(einu)), Topt);
+  const float2 met = mul2(t, bc2(-einu));
+  const float2 dTdnu = NU_PAPER ? mul2(met, Topt)
+                                : mul2(T, fma2(met, ropt, mul2(lg, bc2(-0.34657359027997264f))));
+  e.dnu = fma2(dT, dTdnu, e.dnu);
+  const float2 dhdx = mul2(dh, dx);
+  e.sdh = add2(e.sdh, dh);
+  e.sdhdx = add2(e.sdhdx, dhdx);
+  e.sdhdx2 = fma2(dhdx, dx, e.sdhdx2);
 }
 
 template <bool FILTER, bool L1, bool NUP>
@@ -149,34 +162,40 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
   const int64_t HW = (int64_t)G.width * G.height;
   const float inv3P = 1.0f / (3.0f * (float)HW);
 
-  PixB q[kPX];
-  float px[kPX];
+  PixB2 q[kPairs];
+  float2 px[kPairs];
+  int32_t qlast[kPX];
   float lsum = 0.f;
   int32_t m = start;
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
-    q[k] = PixB{1.f, 0.f, 0.f, 0.f, 0.f, start};
-    px[k] = (float)(x0 + k) + 0.5f;
+    PixB2& qq = q[k >> 1];
+    float &W = lane_of(qq.W, k), &gS = lane_of(qq.gS, k);
+    float &g0 = lane_of(qq.g0, k), &g1 = lane_of(qq.g1, k), &g2 = lane_of(qq.g2, k);
+    W = 1.f;
+    gS = g0 = g1 = g2 = 0.f;
+    qlast[k] = start;
+    lane_of(px[k >> 1], k) = (float)(x0 + k) + 0.5f;
     if (!(x0 + k < G.width && y < G.height)) continue;
     const int64_t pix = (int64_t)y * G.width + x0 + k;
-    q[k].last = last[(int64_t)v * HW + pix];
-    q[k].W = final_T[(int64_t)v * HW + pix];
-    m = max(m, q[k].last);
+    qlast[k] = last[(int64_t)v * HW + pix];
+    W = final_T[(int64_t)v * HW + pix];
+    m = max(m, qlast[k]);
     if (L1) {
       const float* cimg = rgb + (int64_t)v * 3 * HW + pix;
       const float* timg = target + (int64_t)v * 3 * HW + pix;
       const float d0 = cimg[0] - timg[0], d1 = cimg[HW] - timg[HW], d2 = cimg[2 * HW] - timg[2 * HW];
-      q[k].g0 = d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f);
-      q[k].g1 = d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f);
-      q[k].g2 = d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f);
+      g0 = d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f);
+      g1 = d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f);
+      g2 = d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f);
       lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
     } else {
       const float* gimg = d_rgb + (int64_t)v * 3 * HW + pix;
-      q[k].g0 = gimg[0];
-      q[k].g1 = gimg[HW];
-      q[k].g2 = gimg[2 * HW];
+      g0 = gimg[0];
+      g1 = gimg[HW];
+      g2 = gimg[2 * HW];
     }
-    q[k].gS = fmaf(q[k].g0, bg0, fmaf(q[k].g1, bg1, q[k].g2 * bg2));  // S_n = bg (R12)
+    gS = fmaf(g0, bg0, fmaf(g1, bg1, g2 * bg2));  // S_n = bg (R12)
   }
   // tile end = max over pixels of `last`; loss partial sums
 #pragma unroll
@@ -255,15 +274,15 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
-      float h[kPX], dx[kPX];
+      float2 h[kPairs], dx[kPairs];
       bool inc[kPX];
       bool any = false;
 #pragma unroll
-      for (int k = 0; k < kPX; ++k) {
-        dx[k] = __fsub_rn(px[k], a.x);  // the h_f32 sequence, dx kept for the gradient
-        h[k] = __fmaf_rn(dx[k], __fmaf_rn(a.z, dx[k], bdy), cdy2);
-        inc[k] = pj < q[k].last && h[k] <= b.y;
-        any = any || inc[k];
+      for (int k = 0; k < kPairs; ++k) {
+        h[k] = h_f32_pair(px[k], a.x, a.z, bdy, cdy2, dx[k]);  // dx kept for the gradient
+        inc[2 * k] = pj < qlast[2 * k] && h[k].x <= b.y;
+        inc[2 * k + 1] = pj < qlast[2 * k + 1] && h[k].y <= b.y;
+        any = any || inc[2 * k] || inc[2 * k + 1];
       }
 #ifdef SSS_COUNTERS
       {
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
         int ninc = 0, nlive = 0;
         for (int k = 0; k < kPX; ++k) {
           ninc += __popc(__ballot_sync(0xffffffffu, inc[k]));
-          nlive += __popc(__ballot_sync(0xffffffffu, pj < q[k].last));
+          nlive += __popc(__ballot_sync(0xffffffffu, pj < qlast[k]));
         }
         if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
       }
@@ -279,21 +298,23 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       if (!__any_sync(0xffffffffu, any)) continue;
       const float4 c = sc[j];  // {e, r, g, b}
       const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
-      EntrySums es{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const float2 z2 = bc2(0.f);
+      EntrySums2 e2{z2, z2, z2, z2, z2, z2, z2, z2};
 #pragma unroll
-      for (int k = 0; k < kPX; ++k) pair_grad<NUP>(q[k], dx[k], h[k], b, c, einu, es, inc[k]);
-      const float dysdh = dy * es.sdh;
+      for (int k = 0; k < kPairs; ++k) pair_grad2<NUP>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+      const float sdh = e2.sdh.x + e2.sdh.y, sdhdx = e2.sdhdx.x + e2.sdhdx.y;
+      const float dysdh = dy * sdh;
       float vals[10];
-      vals[0] = -fmaf(2.f * a.z, es.sdhdx, a.w * dysdh);   // d mu2D_x
-      vals[1] = -fmaf(a.w, es.sdhdx, 2.f * b.x * dysdh);   // d mu2D_y
-      vals[2] = es.sdhdx2;                                  // d A
-      vals[3] = 2.f * dy * es.sdhdx;                        // d B (conic_xy)
-      vals[4] = dy * dysdh;                                 // d C
-      vals[5] = es.dc0;
-      vals[6] = es.dc1;
-      vals[7] = es.dc2;
-      vals[8] = es.dO;
-      vals[9] = es.dnu;
+      vals[0] = -fmaf(2.f * a.z, sdhdx, a.w * dysdh);   // d mu2D_x
+      vals[1] = -fmaf(a.w, sdhdx, 2.f * b.x * dysdh);   // d mu2D_y
+      vals[2] = e2.sdhdx2.x + e2.sdhdx2.y;              // d A
+      vals[3] = 2.f * dy * sdhdx;                       // d B (conic_xy)
+      vals[4] = dy * dysdh;                             // d C
+      vals[5] = e2.dc0.x + e2.dc0.y;
+      vals[6] = e2.dc1.x + e2.dc1.y;
+      vals[7] = e2.dc2.x + e2.dc2.y;
+      vals[8] = e2.dO.x + e2.dO.y;
+      vals[9] = e2.dnu.x + e2.dnu.y;
       int idx;
       const float r = warp_reduce10(vals, lane, idx);
       if (!(lane & 1) && idx >= 0) myacc[idx * kAccPitch + j] = r;

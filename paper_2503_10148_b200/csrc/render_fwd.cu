@@ -22,28 +22,35 @@
 namespace sss {
 namespace {
 
-struct PixF {  // forward state of one pixel
-  float W, C0, C1, C2;
-  int32_t cnt, last;
-  bool done;
+struct PixF2 {  // forward colour state of a horizontally adjacent pixel pair
+  float2 W, C0, C1, C2;
 };
 
-// One pair of Eq. 7, predicated on `inc` (a = 0 leaves C and W bit-unchanged:
-// C + c*0 = C, W - 0*W = W), so a warp runs its pixels' chains branch-free.
-__device__ __forceinline__ void composite(PixF& p, float h, float4 b, float4 c, int32_t pos, bool inc) {
-  const float t = fmaxf(h, 0.f) * b.w;
-  const float T = ex2_approx(c.x * log2_1p(t, b.w < (1.f / 32.f)));
-  float alpha = fminf(fmaxf(b.z * T, -kAlphaMax), kAlphaMax);
-  alpha = inc ? alpha : 0.f;
-  const float aw = alpha * p.W;
-  p.C0 = fmaf(c.y, aw, p.C0);
-  p.C1 = fmaf(c.z, aw, p.C1);
-  p.C2 = fmaf(c.w, aw, p.C2);
-  p.W = fmaf(-alpha, p.W, p.W);
-  p.cnt += inc ? 1 : 0;
-  p.last = inc ? pos + 1 : p.last;
-  p.done = p.W < kWStop;
+// One pair of Eq. 7 for both pixels of a pair, predicated per pixel on `inc`
+// (a = 0 leaves C and W bit-unchanged: C + c*0 = C, W - 0*W = W), so a warp
+// runs its pixels' chains branch-free.
+__device__ __forceinline__ void composite2(PixF2& p, float2 h, float4 b, float4 c, bool inc0, bool inc1) {
+  const float2 t = mul2(make_float2(fmaxf(h.x, 0.f), fmaxf(h.y, 0.f)), bc2(b.w));
+  float2 lg;
+  if (b.w < (1.f / 32.f)) {  // warp-uniform (see log2_1p)
+    lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+  } else {
+    const float2 opt = add2(t, bc2(1.f));
+    lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+  }
+  const float2 e = mul2(lg, bc2(c.x));
+  const float2 araw = mul2(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(b.z));
+  float2 alpha;
+  alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
+  alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
+  const float2 aw = mul2(alpha, p.W);
+  p.C0 = fma2(bc2(c.y), aw, p.C0);
+  p.C1 = fma2(bc2(c.z), aw, p.C1);
+  p.C2 = fma2(bc2(c.w), aw, p.C2);
+  p.W = fma2(make_float2(-alpha.x, -alpha.y), p.W, p.W);
 }
+
+__device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v.y : v.x; }
 
 template <bool FILTER>
 __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
@@ -72,20 +79,27 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
   const short4* rcv = rect + (int64_t)v * G.n;
 
   if (threadIdx.x == 0) SSS_COUNT(7, end - start);
-  PixF p[kPX];
-  float px[kPX];
+  PixF2 p[kPairs];
+  float2 px[kPairs];
+  int32_t cnt[kPX], lastc[kPX];
+  bool done[kPX];
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
     const bool inside = x0 + k < G.width && y < G.height;
     // pixels outside the image start with W = 0: done, and the predicated
     // composite (done = W < 1e-4) keeps them done (their outputs are unused)
-    p[k] = PixF{inside ? 1.f : 0.f, 0.f, 0.f, 0.f, 0, start, !inside};
-    px[k] = (float)(x0 + k) + 0.5f;
+    PixF2& pp = p[k >> 1];
+    lane_of(pp.W, k) = inside ? 1.f : 0.f;
+    lane_of(pp.C0, k) = lane_of(pp.C1, k) = lane_of(pp.C2, k) = 0.f;
+    lane_of(px[k >> 1], k) = (float)(x0 + k) + 0.5f;
+    cnt[k] = 0;
+    lastc[k] = start;
+    done[k] = !inside;
   }
   auto all_done = [&]() {
     bool d = true;
 #pragma unroll
-    for (int k = 0; k < kPX; ++k) d = d && p[k].done;
+    for (int k = 0; k < kPX; ++k) d = d && done[k];
     return d;
   };
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
@@ -132,14 +146,16 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
-      float h[kPX];
+      float2 h[kPairs];
       bool inc[kPX];
       bool any = false;
 #pragma unroll
-      for (int k = 0; k < kPX; ++k) {
-        h[k] = h_f32_row(px[k], a.x, a.z, bdy, cdy2);
-        inc[k] = !p[k].done && h[k] <= b.y;
-        any = any || inc[k];
+      for (int k = 0; k < kPairs; ++k) {
+        float2 dx;
+        h[k] = h_f32_pair(px[k], a.x, a.z, bdy, cdy2, dx);
+        inc[2 * k] = !done[2 * k] && h[k].x <= b.y;
+        inc[2 * k + 1] = !done[2 * k + 1] && h[k].y <= b.y;
+        any = any || inc[2 * k] || inc[2 * k + 1];
       }
 #ifdef SSS_COUNTERS
       {
@@ -147,7 +163,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
         int ninc = 0, nlive = 0;
         for (int k = 0; k < kPX; ++k) {
           ninc += __popc(__ballot_sync(0xffffffffu, inc[k]));
-          nlive += __popc(__ballot_sync(0xffffffffu, !p[k].done));
+          nlive += __popc(__ballot_sync(0xffffffffu, !done[k]));
         }
         if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
       }
@@ -156,7 +172,13 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
         const float4 c = sc[j];  // {e, r, g, b}
         const int32_t pj = spos[j];
 #pragma unroll
-        for (int k = 0; k < kPX; ++k) composite(p[k], h[k], b, c, pj, inc[k]);
+        for (int k = 0; k < kPairs; ++k) composite2(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
+#pragma unroll
+        for (int k = 0; k < kPX; ++k) {
+          cnt[k] += inc[k] ? 1 : 0;
+          lastc[k] = inc[k] ? pj + 1 : lastc[k];
+          done[k] = lane_of(p[k >> 1].W, k) < kWStop;
+        }
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
     }
@@ -167,12 +189,14 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
     if (!(x0 + k < G.width && y < G.height)) continue;
     const int64_t pix = (int64_t)y * G.width + x0 + k;
     float* o = rgb + (int64_t)v * 3 * HW + pix;
-    o[0] = p[k].C0 + bg0 * p[k].W;
-    o[HW] = p[k].C1 + bg1 * p[k].W;
-    o[2 * HW] = p[k].C2 + bg2 * p[k].W;
-    final_T[(int64_t)v * HW + pix] = p[k].W;
-    n_contrib[(int64_t)v * HW + pix] = p[k].cnt;
-    last[(int64_t)v * HW + pix] = p[k].last;
+    PixF2& pp = p[k >> 1];
+    const float W = lane_of(pp.W, k);
+    o[0] = lane_of(pp.C0, k) + bg0 * W;
+    o[HW] = lane_of(pp.C1, k) + bg1 * W;
+    o[2 * HW] = lane_of(pp.C2, k) + bg2 * W;
+    final_T[(int64_t)v * HW + pix] = W;
+    n_contrib[(int64_t)v * HW + pix] = cnt[k];
+    last[(int64_t)v * HW + pix] = lastc[k];
   }
 }
 
