@@ -49,7 +49,7 @@ typedef enum {
 } sss_status;
 
 #define SSS_TILE 16          /* tile edge in pixels */
-#define SSS_MAX_BINS 6144    /* bins per view (tiles >> bin_shift) */
+#define SSS_MAX_BINS 5632    /* bins per view (tiles >> bin_shift); bounded by the scatter CTA's shared memory */
 #define SSS_REC_FLOATS 12    /* floats per projected record (48 B) */
 #define SSS_G2D_FLOATS 12    /* floats per screen-space gradient record (48 B) */
 

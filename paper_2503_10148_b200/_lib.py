@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(PKG, "libsss.so")
 
 SSS_OK, SSS_ERR_ARG, SSS_ERR_SHAPE, SSS_ERR_CAPACITY, SSS_ERR_CUDA = range(5)
 SSS_TILE = 16
-SSS_MAX_BINS = 6144
+SSS_MAX_BINS = 5632
 SSS_REC_FLOATS = 12
 SSS_G2D_FLOATS = 12
 SSS_BWD_NU_GRAD_PAPER = 1

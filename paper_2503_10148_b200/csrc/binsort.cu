@@ -8,15 +8,22 @@
 // B200 design — two stages instead of one 64-bit key sort over all M
 // instances:
 //   1. a stable LSD radix sort (4 x 8-bit digits) of the N per-view depth keys
-//      (keys of culled components are 0xFFFFFFFF and sort last);
+//      (keys of culled components are 0xFFFFFFFF and sort last); each pass
+//      reorders its 4096-key tile by digit in shared memory so the global
+//      stores leave as per-digit runs;
 //   2. a stable counting scatter of the instances by bin, generated on the fly
 //      from the depth-sorted components: per-chunk bin histograms (shared
 //      memory), a column scan over chunks, a scan over bins, then a scatter in
-//      which each warp walks its components in order, so bins receive their
-//      entries in depth order without ever materialising 64-bit keys.
+//      which each lane of a warp owns one component and walks its bin rect;
+//      the slot of (lane, bin) is the warp's running count plus the number of
+//      lower lanes covering the bin — a popcount of per-column and per-row
+//      lane ballots — so bins receive their entries in depth order without
+//      ever materialising 64-bit keys or serialising lanes.
 // Every instance is written exactly once (4 B id, +8 B key if requested); the
 // radix passes touch only N keys per view.  All views are processed by the
 // same launches (grid.y = view).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sss {
@@ -48,14 +55,11 @@ inline BinGeom bin_geom(const sss_camera& c, int shift) {
   return g;
 }
 
-inline int chunk_size(int64_t n, int V) {
-  // components per scatter chunk: enough CTAs to fill 148 SMs a few times,
-  // but few enough chunks that the [chunk][bin] histograms stay small.
-  int64_t c = (n * (int64_t)V) / (148 * 4);
-  int cs = 1024;
-  while (cs < c && cs < 8192) cs *= 2;
-  return cs;
-}
+#ifndef SSS_CHUNK
+#define SSS_CHUNK 1024
+#endif
+constexpr int kChunk = SSS_CHUNK;  // depth-sorted components per histogram / scatter CTA
+constexpr size_t kScatterSmemMax = 225 * 1024;  // dynamic shared memory of a scatter CTA
 
 struct WsLayout {
   size_t keys_a, keys_b, vals_a, vals_b, n_vis, radix_hist, chunk_hist, bin_total, bin_start, total;
@@ -67,7 +71,7 @@ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   WsLayout L;
   L.tiles_per_view = div_up(n, kRadixTile);
-  L.chunk = chunk_size(n, V);
+  L.chunk = kChunk;
   L.n_chunks = div_up(n, L.chunk);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
@@ -145,53 +149,91 @@ __global__ void __launch_bounds__(kRadixThreads) radix_upsweep_kernel(const uint
   hist[((size_t)v * 256 + threadIdx.x) * tiles + tile] = h[threadIdx.x];
 }
 
-// exclusive scan of one view's digit-major histogram (256 * tiles entries)
-__global__ void __launch_bounds__(1024) scan_u32_kernel(uint32_t* __restrict__ data, int64_t len_per_seg) {
-  __shared__ uint32_t part[1024];
-  uint32_t* d = data + (size_t)blockIdx.x * len_per_seg;
-  const int t = threadIdx.x;
-  const int64_t per = (len_per_seg + 1023) / 1024;
-  const int64_t lo = t * per, hi = lo + per < len_per_seg ? lo + per : len_per_seg;
-  uint32_t s = 0;
-  for (int64_t k = lo; k < hi; ++k) s += d[k];
-  part[t] = s;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    uint32_t x = t >= off ? part[t - off] : 0;
-    __syncthreads();
-    part[t] += x;
-    __syncthreads();
+// exclusive scan of one view's digit-major histogram (256 * tiles entries):
+// one CTA per view walks the array in coalesced 4096-entry chunks (4 per
+// thread, warp-shuffle scans) carrying the running total.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+    if ((int)lane_id() >= o) x += t;
   }
-  uint32_t run = part[t] - s;
-  for (int64_t k = lo; k < hi; ++k) {
-    const uint32_t x = d[k];
-    d[k] = run;
-    run += x;
+  return x;
+}
+
+__global__ void __launch_bounds__(1024) scan_u32_kernel(uint32_t* __restrict__ data, int64_t len_per_seg) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry_s;
+  uint32_t* d = data + (size_t)blockIdx.x * len_per_seg;
+  const int t = threadIdx.x, w = t >> 5, lane = lane_id();
+  uint32_t carry = 0;
+  for (int64_t c0 = 0; c0 < len_per_seg; c0 += 4096) {
+    uint32_t x[4];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // thread t owns 4 consecutive entries
+      const int64_t i = c0 + 4 * t + k;
+      x[k] = i < len_per_seg ? d[i] : 0u;
+      s += x[k];
+    }
+    const uint32_t inc = warp_incl_scan(s);
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t ws = wsum[lane];
+      const uint32_t wi = warp_incl_scan(ws);
+      wsum[lane] = wi - ws;
+      if (lane == 31) carry_s = wi;
+    }
+    __syncthreads();
+    uint32_t run = carry + wsum[w] + inc - s;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = c0 + 4 * t + k;
+      if (i < len_per_seg) d[i] = run;
+      run += x[k];
+    }
+    carry += carry_s;
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
+// Stable scatter of one 4096-key tile by the digit at `shift`: ranks by
+// per-warp digit counters (8 ballots per 32 keys, in key order), then the
+// tile is reordered by digit in shared memory so that global stores go out
+// as per-digit runs (~16 consecutive keys) instead of 32 random addresses
+// per warp store.
+__global__ void __launch_bounds__(kRadixThreads, 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in, int64_t n, int shift,
     int tiles, const uint32_t* __restrict__ hist, uint32_t* __restrict__ keys_out,
     int32_t* __restrict__ vals_out) {
   __shared__ uint32_t run[kScatterWarps][256];
   __shared__ uint32_t tile_off[256];
+  __shared__ uint32_t lstart[256];
+  __shared__ uint32_t wsum[kScatterWarps];
+  __shared__ uint32_t skey[kRadixTile];
+  __shared__ int32_t sval[kRadixTile];
   const int v = blockIdx.y, tile = blockIdx.x;
   const int w = threadIdx.x >> 5, lane = lane_id();
   for (int k = threadIdx.x; k < kScatterWarps * 256; k += kRadixThreads) (&run[0][0])[k] = 0;
   tile_off[threadIdx.x] = hist[((size_t)v * 256 + threadIdx.x) * tiles + tile];
   __syncthreads();
-  const int64_t base = (int64_t)tile * kRadixTile + w * (32 * kRadixItems);
+  const int64_t tbase = (int64_t)tile * kRadixTile;
+  const int64_t base = tbase + w * (32 * kRadixItems);
+  const uint32_t* kin = keys_in + (int64_t)v * n;
+  const int32_t* vin = vals_in + (int64_t)v * n;
   uint32_t key[kRadixItems];
-  int32_t val[kRadixItems];
   uint32_t loc[kRadixItems];
+#pragma unroll
+  for (int c = 0; c < kRadixItems; ++c) {
+    const int64_t i = base + c * 32 + lane;
+    key[c] = i < n ? kin[i] : 0xFFFFFFFFu;
+  }
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int c = 0; c < kRadixItems; ++c) {
     const int64_t i = base + c * 32 + lane;
     const bool ok = i < n;
-    key[c] = ok ? keys_in[(int64_t)v * n + i] : 0u;
-    val[c] = ok ? vals_in[(int64_t)v * n + i] : 0;
     const unsigned d = (key[c] >> shift) & 255u;
     const unsigned valid = __ballot_sync(0xffffffffu, ok);
     const unsigned pm = peers_of(d) & valid;
@@ -202,15 +244,23 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
     __syncwarp();
   }
   __syncthreads();
-  // exclusive prefix over warps per digit -> warp base
+  // per digit: exclusive prefix over warps, tile count; then tile-local digit starts
   {
     const int d = threadIdx.x;
-    uint32_t acc = tile_off[d];
+    uint32_t acc = 0;
     for (int ww = 0; ww < kScatterWarps; ++ww) {
       const uint32_t x = run[ww][d];
       run[ww][d] = acc;
       acc += x;
     }
+    const uint32_t inc = warp_incl_scan(acc);
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t wo = 0;
+    for (int ww = 0; ww < w; ++ww) wo += wsum[ww];
+    const uint32_t st = wo + inc - acc;
+    lstart[d] = st;
+    for (int ww = 0; ww < kScatterWarps; ++ww) run[ww][d] += st;
   }
   __syncthreads();
 #pragma unroll
@@ -218,10 +268,21 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep_kernel(
     const int64_t i = base + c * 32 + lane;
     if (i < n) {
       const unsigned d = (key[c] >> shift) & 255u;
-      const uint32_t pos = run[w][d] + loc[c];
-      keys_out[(int64_t)v * n + pos] = key[c];
-      vals_out[(int64_t)v * n + pos] = val[c];
+      const uint32_t lp = run[w][d] + loc[c];
+      skey[lp] = key[c];
+      sval[lp] = vin[i];
     }
+  }
+  __syncthreads();
+  const int cnt = (int)min((int64_t)kRadixTile, n - tbase);
+  uint32_t* kout = keys_out + (int64_t)v * n;
+  int32_t* vout = vals_out + (int64_t)v * n;
+  for (int i = threadIdx.x; i < cnt; i += kRadixThreads) {
+    const uint32_t k = skey[i];
+    const unsigned d = (k >> shift) & 255u;
+    const uint32_t pos = tile_off[d] + (uint32_t)i - lstart[d];
+    kout[pos] = k;
+    vout[pos] = sval[i];
   }
 }
 
@@ -317,23 +378,29 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   }
 }
 
-// Walks the instances (component, bin) of the warp's components
-// [wlo, whi) in order — component-major, bin row-major — 32 instances per
-// step: the instance counts of 32 consecutive components are prefix-summed
-// across the warp, each lane finds the component owning its flat index by a
-// 5-step binary search over the lanes, and lanes hitting the same bin in the
-// same step are ranked by lane order (match.any), which preserves the
-// (depth, index) order within every bin.  COUNT: per-warp bin counts;
-// otherwise write ids (and keys) at base[b] + the warp's running offset.
+// Walks the warp's depth-sorted components [wlo, whi), 32 at a time, one
+// component per lane; each lane loops over the bins of its component's bin
+// rect (row-major).
+//   COUNT: per-warp bin counts (shared atomics).
+//   place: the slot of (lane i, bin b) is cnt[b] + the number of lanes
+//   i' < i whose component also covers b.  The lanes covering b are
+//   colmask[bx] & rowmask[by] (one ballot per bin column and row), so the
+//   rank is a popcount and no lane order has to be serialised; the first
+//   lane covering b then advances cnt[b] by the number of covering lanes.
+//   The (depth, index) order within every bin follows.  The id is written
+//   straight to its global slot gofs[b] + slot (4-byte stores that L2
+//   merges; staging the chunk in shared memory for coalesced runs measured
+//   slower — it costs occupancy).
 template <bool COUNT>
-__device__ __forceinline__ void warp_instances(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
-                                               const float* __restrict__ dv, int64_t wlo, int64_t whi,
-                                               const BinGeom& g, uint16_t* my, const uint32_t* base,
-                                               int32_t* __restrict__ idv, uint64_t* __restrict__ kv) {
+__device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
+                                          const float* __restrict__ dv, int64_t wlo, int64_t whi,
+                                          const BinGeom& g, uint32_t* cnt, uint32_t* colmask,
+                                          uint32_t* rowmask, const uint32_t* gofs,
+                                          int32_t* __restrict__ idv, uint64_t* __restrict__ kv) {
   const int lane = lane_id();
+  const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  // software pipeline: the next group's (id, rect) gathers are in flight
-  // while the current group's instances are placed
+  const int by_max = g.bins_y - 1, bx_max = g.bins_x - 1;
   int id_n = 0;
   short4 r_n = make_short4(1, 1, 0, 0);
   if (wlo + lane < whi) {
@@ -341,113 +408,103 @@ __device__ __forceinline__ void warp_instances(const int32_t* __restrict__ sid, 
     r_n = rv[id_n];
   }
   for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
-    const int64_t j = j0 + lane;
     const int id = id_n;
+    const bool valid = j0 + lane < whi;
     const short4 r = r_n;
-    if (j + 32 < whi) {
-      id_n = sid[j + 32];
+    if (j0 + 32 + lane < whi) {  // prefetch the next 32 components
+      id_n = sid[j0 + 32 + lane];
       r_n = rv[id_n];
     }
-    int bx0 = 0, by0 = 0, bw = 1, nb = 0;
+    int bx0 = r.x >> g.shift, by0 = r.y >> g.shift;
+    int bx1 = r.z >> g.shift, by1 = r.w >> g.shift;
+    if (!valid) { bx0 = by0 = 1; bx1 = by1 = 0; }  // empty
+    if constexpr (COUNT) {
+      for (int by = by0; by <= by1; ++by)
+        for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&cnt[by * g.bins_x + bx], 1u);
+    } else {
+    // covering lanes per bin column / row
+    for (int x = 0; x <= bx_max; ++x) {
+      const unsigned m = __ballot_sync(full, bx0 <= x && x <= bx1);
+      if (lane == 0) colmask[x] = m;
+    }
+    for (int y = 0; y <= by_max; ++y) {
+      const unsigned m = __ballot_sync(full, by0 <= y && y <= by1);
+      if (lane == 0) rowmask[y] = m;
+    }
+    __syncwarp();
     uint32_t dbits = 0;
-    if (j < whi) {
-      bx0 = r.x >> g.shift;
-      by0 = r.y >> g.shift;
-      bw = (r.z >> g.shift) - bx0 + 1;
-      nb = bw * ((r.w >> g.shift) - by0 + 1);
-      if (!COUNT && kv) dbits = __float_as_uint(dv[id]);
+    if (kv && valid) dbits = __float_as_uint(dv[id]);
+    for (int by = by0; by <= by1; ++by) {
+      const unsigned rm = rowmask[by];
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const int b = by * g.bins_x + bx;
+        const uint32_t pos = gofs[b] + cnt[b] + __popc(colmask[bx] & rm & lt);
+        idv[pos] = id;
+        if (kv) kv[pos] = ((uint64_t)b << 32) | dbits;
+      }
     }
-    int incl = nb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+    __syncwarp();
+    for (int by = by0; by <= by1; ++by) {
+      const unsigned rm = rowmask[by];
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const unsigned m = colmask[bx] & rm;
+        if ((m & lt) == 0) cnt[by * g.bins_x + bx] += __popc(m);
+      }
     }
-    const int excl = incl - nb;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int f0 = 0; f0 < total; f0 += 32) {
-      const int f = f0 + lane;
-      const bool act = f < total;
-      int k = 0;  // owner lane: the largest k with excl_k <= f
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int e = __shfl_sync(0xffffffffu, excl, k + step);
-        if (e <= f) k += step;
-      }
-      const int t = f - __shfl_sync(0xffffffffu, excl, k);
-      const int kbw = __shfl_sync(0xffffffffu, bw, k);
-      const int kbx0 = __shfl_sync(0xffffffffu, bx0, k);
-      const int kby0 = __shfl_sync(0xffffffffu, by0, k);
-      const int row = t / kbw;
-      const int b = (kby0 + row) * g.bins_x + kbx0 + (t - row * kbw);
-      // lanes of this step with the same bin (ballots on its bits; cheaper
-      // than match.any on sm_100)
-      unsigned peers = __ballot_sync(0xffffffffu, act);
-      for (int i = 0; i < g.bits; ++i) {
-        const bool bit = (b >> i) & 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? bal : ~bal;
-      }
-      const int rank = __popc(peers & lt);
-      if (!COUNT) {
-        const int kid = __shfl_sync(0xffffffffu, id, k);
-        const uint32_t kd = __shfl_sync(0xffffffffu, dbits, k);
-        if (act) {
-          const uint32_t pos = base[b] + my[b] + rank;
-          idv[pos] = kid;
-          if (kv) kv[pos] = ((uint64_t)b << 32) | kd;
-        }
-      }
-      __syncwarp();
-      if (act && rank == 0) my[b] += (uint16_t)__popc(peers);
-      __syncwarp();
+    __syncwarp();
     }
   }
 }
 
-// stable scatter: CTA per (chunk, view); warp w owns components
-// [chunk*c + w*chunk/8, ...) and walks their instances in order.
+// stable scatter: CTA per (chunk of kChunk depth-sorted components, view);
+// warp w owns kChunk/8 consecutive components.  Phase 1 counts per (warp,
+// bin); an exclusive prefix over warps turns the counts into each warp's
+// first slot in the chunk's segment of every bin, and phase 2 writes the ids.
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
-    const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int chunk,
-    int n_chunks, BinGeom g, const uint32_t* __restrict__ chunk_hist,
-    const uint32_t* __restrict__ bin_start, const int64_t* __restrict__ totals, int64_t capacity,
-    int32_t* __restrict__ ids, uint64_t* __restrict__ keys) {
+    const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
+    const uint32_t* __restrict__ chunk_hist, const uint32_t* __restrict__ bin_start,
+    const int64_t* __restrict__ totals, int64_t capacity, int32_t* __restrict__ ids,
+    uint64_t* __restrict__ keys) {
   extern __shared__ uint32_t sm[];
   const int v = blockIdx.y, c = blockIdx.x;
   if (totals[v] > capacity) return;
-  const int64_t lo = (int64_t)c * chunk;
+  const int64_t lo = (int64_t)c * kChunk;
   const int64_t nvis = n_vis[v];
   if (lo >= nvis) return;
-  uint32_t* base = sm;                                    // [n_bins]
-  uint16_t* woff = (uint16_t*)(sm + g.n_bins);            // [8][n_bins]
-  const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * g.n_bins;
-  const uint32_t* bs = bin_start + (size_t)v * g.n_bins;
-  for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) base[b] = bs[b] + ch[b];
-  for (int k = threadIdx.x; k < kScatterWarps * g.n_bins; k += blockDim.x) woff[k] = 0;
+  const int nb = g.n_bins;
+  uint32_t* cnt = sm;                                  // [8][n_bins] per-warp counters / slots
+  uint32_t* gofs = cnt + (size_t)kScatterWarps * nb;  // [n_bins] the chunk's first slot per bin
+  uint32_t* masks = gofs + nb;                         // [8][bins_x + bins_y] lane masks
+  for (int k = threadIdx.x; k < kScatterWarps * nb; k += blockDim.x) cnt[k] = 0;
+  const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
+  const uint32_t* bs = bin_start + (size_t)v * nb;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) gofs[b] = bs[b] + ch[b];
   __syncthreads();
   const int w = threadIdx.x >> 5;
-  const int per_warp = chunk / kScatterWarps;
+  constexpr int per_warp = kChunk / kScatterWarps;
   const int64_t wlo = lo + (int64_t)w * per_warp;
   const int64_t whi = min(wlo + per_warp, nvis);
-  uint16_t* my = woff + (size_t)w * g.n_bins;
+  uint32_t* my = cnt + (size_t)w * nb;
+  uint32_t* colmask = masks + w * (g.bins_x + g.bins_y);
+  uint32_t* rowmask = colmask + g.bins_x;
   const int32_t* sid = sorted_ids + (int64_t)v * n;
   const short4* rv = rect + (int64_t)v * n;
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  warp_instances<true>(sid, rv, dv, wlo, whi, g, my, base, idv, kv);  // phase 1: counts
+  warp_walk<true>(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);  // phase 1
   __syncthreads();
-  for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // warp prefix per bin
     uint32_t acc = 0;
     for (int ww = 0; ww < kScatterWarps; ++ww) {
-      const uint32_t x = woff[(size_t)ww * g.n_bins + b];
-      woff[(size_t)ww * g.n_bins + b] = (uint16_t)acc;
+      const uint32_t x = cnt[(size_t)ww * nb + b];
+      cnt[(size_t)ww * nb + b] = acc;
       acc += x;
     }
   }
   __syncthreads();
-  warp_instances<false>(sid, rv, dv, wlo, whi, g, my, base, idv, kv);  // phase 2: scatter
+  warp_walk<false>(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);  // phase 2
 }
 
 }  // namespace
@@ -534,14 +591,14 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   if (n > 0) {
     static thread_local bool attr_set = false;
     if (!attr_set) {
-      cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmemMax);
       cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_set = true;
     }
-    const size_t ssm = (size_t)g.n_bins * 4 + (size_t)kScatterWarps * g.n_bins * 2;
+    const size_t ssm = ((size_t)(kScatterWarps + 1) * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y)) * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
-        vals_a, n_vis, rect, pr->depth, n, L.chunk, L.n_chunks, g, chist, bstart, out->totals,
-        out->capacity, out->ids, out->keys);
+        vals_a, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, bstart, out->totals, out->capacity,
+        out->ids, out->keys);
     count_launch();
   }
   return check_launch("sss_bin_sort");
