@@ -122,7 +122,9 @@ typedef struct {
 /* Rendered frames (output of sss_render_fwd; all views share one size).
  *  rgb       [V][3][H][W]  C(u) of Eq. 7 + bg * W (unclamped, R21)
  *  final_T   [V][H][W]     final transmittance W
- *  n_contrib [V][H][W]     number of composited (included) components (R23)
+ *  n_contrib [V][H][W]     number of composited (included) components (R23);
+ *                          optional diagnostic: NULL = not counted (the backward
+ *                          does not read it)
  *  last      [V][H][W]     private: bin-list offset one past the last
  *                          composited entry (start of the backward replay) */
 typedef struct {

@@ -143,7 +143,7 @@ class Bins:
 class Frame:
     rgb: torch.Tensor        # [V][3][H][W] f32
     final_T: torch.Tensor    # [V][H][W] f32
-    n_contrib: torch.Tensor  # [V][H][W] i32
+    n_contrib: Optional[torch.Tensor]  # [V][H][W] i32; None = not counted (diagnostic)
     last: torch.Tensor       # [V][H][W] i32
 
     @classmethod

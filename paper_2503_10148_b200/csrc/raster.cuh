@@ -20,6 +20,16 @@ constexpr int kBatch = kRasterThreads < 128 ? kRasterThreads : 128;  // entries 
 constexpr int kWarpW = 16;                        // warp strip: 16x4 or 16x8 pixels
 constexpr int kWarpH = 32 * kPX / kWarpW;
 constexpr int kLanesPerRow = kWarpW / kPX;
+// resident CTAs per SM the register allocation must allow (occupancy hides
+// the fixed-latency FP32/MUFU dependency chains of the hot loops)
+#ifndef SSS_FWD_MINB
+#define SSS_FWD_MINB 20  // 48 registers: 40 warps per SM (measured: -7% vs 56 registers)
+#endif
+#ifndef SSS_BWD_MINB
+#define SSS_BWD_MINB 1
+#endif
+constexpr int kFwdMinBlocks = SSS_FWD_MINB;
+constexpr int kBwdMinBlocks = SSS_BWD_MINB;
 constexpr int kWarpsPerRow = 16 / kWarpW;
 
 // Development counters (variant builds with -DSSS_COUNTERS only).

@@ -89,23 +89,34 @@ __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v
 // (1 - a_i), g.S).  Predicated per pixel on `inc`: with a = 0 the replay
 // state is bit-unchanged (W / (1 - 0) = W, gS + (gc - gS) 0 = gS) and every
 // contribution is zero, so a warp runs its pixels' chains branch-free.
-template <bool NU_PAPER>
+// T / (1 + h/nu) comes from one ex2 of (e - 1) log2(1 + h/nu) (T = that
+// times 1 + h/nu), so a pair costs lg2, ex2 and rcp(1 - a) on the MUFU pipe.
+// GENERAL handles the rare warp-uniform cases (as the forward): nu > 32
+// (accurate log1p) and |o| > 0.989, where the +-0.99 clamp (R10) can bind
+// and then cuts the gradient.
+template <bool NU_PAPER, bool GENERAL>
 __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4 b, float4 c, float einu,
                                            EntrySums2& e, bool inc0, bool inc1) {
-  const float2 t = mul2(make_float2(fmaxf(h.x, 0.f), fmaxf(h.y, 0.f)), bc2(b.w));
+  const float2 t = mul2(h, bc2(b.w));
   const float2 opt = add2(t, bc2(1.f));
   float2 lg;
-  if (b.w < (1.f / 32.f)) {  // warp-uniform (see log2_1p)
+  if (GENERAL && b.w < (1.f / 32.f)) {
     lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
   } else {
     lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
   }
-  const float2 ex = mul2(lg, bc2(c.x));
-  const float2 T = make_float2(ex2_approx(ex.x), ex2_approx(ex.y));
+  const float2 exm = mul2(lg, bc2(c.x - 1.f));
+  const float2 Topt = make_float2(ex2_approx(exm.x), ex2_approx(exm.y));  // T / (1 + h/nu)
+  const float2 T = mul2(Topt, opt);
   const float2 araw = mul2(T, bc2(b.z));
   float2 alpha;
-  alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
-  alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
+  if (GENERAL) {
+    alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
+    alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
+  } else {
+    alpha.x = inc0 ? araw.x : 0.f;
+    alpha.y = inc1 ? araw.y : 0.f;
+  }
   const float2 oma = sub2(bc2(1.f), alpha);  // 1 - a >= 0.01 (R10): no range fix-up
   const float2 Wi = mul2(p.W, make_float2(rcp_approx(oma.x), rcp_approx(oma.y)));
   const float2 aw = mul2(alpha, Wi);
@@ -117,17 +128,19 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
   float2 da = mul2(diff, Wi);
   p.gS = fma2(diff, alpha, p.gS);
   p.W = Wi;
-  // R10: no gradient through the clamp
-  da.x = (inc0 && fabsf(araw.x) <= kAlphaMax) ? da.x : 0.f;
-  da.y = (inc1 && fabsf(araw.y) <= kAlphaMax) ? da.y : 0.f;
+  if (GENERAL) {  // R10: no gradient through the clamp
+    da.x = (inc0 && fabsf(araw.x) <= kAlphaMax) ? da.x : 0.f;
+    da.y = (inc1 && fabsf(araw.y) <= kAlphaMax) ? da.y : 0.f;
+  } else {
+    da.x = inc0 ? da.x : 0.f;
+    da.y = inc1 ? da.y : 0.f;
+  }
   e.dO = fma2(da, T, e.dO);
   const float2 dT = mul2(da, bc2(b.z));
-  const float2 ropt = make_float2(rcp_approx(opt.x), rcp_approx(opt.y));
-  const float2 Topt = mul2(T, ropt);
   const float2 dh = mul2(mul2(dT, bc2(einu)), Topt);
   const float2 met = mul2(t, bc2(-einu));
   const float2 dTdnu = NU_PAPER ? mul2(met, Topt)
-                                : mul2(T, fma2(met, ropt, mul2(lg, bc2(-0.34657359027997264f))));
+                                : fma2(met, Topt, mul2(T, mul2(lg, bc2(-0.34657359027997264f))));
   e.dnu = fma2(dT, dTdnu, e.dnu);
   const float2 dhdx = mul2(dh, dx);
   e.sdh = add2(e.sdh, dh);
@@ -136,7 +149,7 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
 }
 
 template <bool FILTER, bool L1, bool NUP>
-__global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
+__global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kernel(
     const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
@@ -300,8 +313,15 @@ __global__ void __launch_bounds__(kRasterThreads) render_bwd_kernel(
       const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
       const float2 z2 = bc2(0.f);
       EntrySums2 e2{z2, z2, z2, z2, z2, z2, z2, z2};
+      if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
-      for (int k = 0; k < kPairs; ++k) pair_grad2<NUP>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+        for (int k = 0; k < kPairs; ++k)
+          pair_grad2<NUP, true>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kPairs; ++k)
+          pair_grad2<NUP, false>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+      }
       const float sdh = e2.sdh.x + e2.sdh.y, sdhdx = e2.sdhdx.x + e2.sdhdx.y;
       const float dysdh = dy * sdh;
       float vals[10];

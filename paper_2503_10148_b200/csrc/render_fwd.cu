@@ -28,21 +28,29 @@ struct PixF2 {  // forward colour state of a horizontally adjacent pixel pair
 
 // One pair of Eq. 7 for both pixels of a pair, predicated per pixel on `inc`
 // (a = 0 leaves C and W bit-unchanged: C + c*0 = C, W - 0*W = W), so a warp
-// runs its pixels' chains branch-free.
+// runs its pixels' chains branch-free.  GENERAL handles the two rare
+// warp-uniform cases: nu > 32 (accurate log1p, see log2_1p) and |o| > 0.989,
+// where the +-0.99 clamp (R10) can bind (T <= 1 for h >= 0, so |o| <= 0.989
+// leaves |o T| < 0.99 even for an h rounded slightly below 0).
+template <bool GENERAL>
 __device__ __forceinline__ void composite2(PixF2& p, float2 h, float4 b, float4 c, bool inc0, bool inc1) {
-  const float2 t = mul2(make_float2(fmaxf(h.x, 0.f), fmaxf(h.y, 0.f)), bc2(b.w));
+  const float2 t = mul2(h, bc2(b.w));
   float2 lg;
-  if (b.w < (1.f / 32.f)) {  // warp-uniform (see log2_1p)
+  if (GENERAL && b.w < (1.f / 32.f)) {
     lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
   } else {
     const float2 opt = add2(t, bc2(1.f));
     lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
   }
   const float2 e = mul2(lg, bc2(c.x));
-  const float2 araw = mul2(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(b.z));
+  float2 araw = mul2(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(b.z));
+  if (GENERAL) {
+    araw.x = fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax);
+    araw.y = fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax);
+  }
   float2 alpha;
-  alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
-  alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
+  alpha.x = inc0 ? araw.x : 0.f;
+  alpha.y = inc1 ? araw.y : 0.f;
   const float2 aw = mul2(alpha, p.W);
   p.C0 = fma2(bc2(c.y), aw, p.C0);
   p.C1 = fma2(bc2(c.z), aw, p.C1);
@@ -52,8 +60,8 @@ __device__ __forceinline__ void composite2(PixF2& p, float2 h, float4 b, float4 
 
 __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v.y : v.x; }
 
-template <bool FILTER>
-__global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
+template <bool FILTER, bool COUNT>
+__global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kernel(
     const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     float* __restrict__ rgb, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
@@ -82,24 +90,22 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
   PixF2 p[kPairs];
   float2 px[kPairs];
   int32_t cnt[kPX], lastc[kPX];
-  bool done[kPX];
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
     const bool inside = x0 + k < G.width && y < G.height;
-    // pixels outside the image start with W = 0: done, and the predicated
-    // composite (done = W < 1e-4) keeps them done (their outputs are unused)
+    // a pixel is live while W >= 1e-4 (R11); pixels outside the image start
+    // with W = 0 and so are never composited (their outputs are unused)
     PixF2& pp = p[k >> 1];
     lane_of(pp.W, k) = inside ? 1.f : 0.f;
     lane_of(pp.C0, k) = lane_of(pp.C1, k) = lane_of(pp.C2, k) = 0.f;
     lane_of(px[k >> 1], k) = (float)(x0 + k) + 0.5f;
     cnt[k] = 0;
     lastc[k] = start;
-    done[k] = !inside;
   }
   auto all_done = [&]() {
     bool d = true;
 #pragma unroll
-    for (int k = 0; k < kPX; ++k) d = d && done[k];
+    for (int k = 0; k < kPX; ++k) d = d && !(lane_of(p[k >> 1].W, k) >= kWStop);
     return d;
   };
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
@@ -153,8 +159,8 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
       for (int k = 0; k < kPairs; ++k) {
         float2 dx;
         h[k] = h_f32_pair(px[k], a.x, a.z, bdy, cdy2, dx);
-        inc[2 * k] = !done[2 * k] && h[k].x <= b.y;
-        inc[2 * k + 1] = !done[2 * k + 1] && h[k].y <= b.y;
+        inc[2 * k] = p[k].W.x >= kWStop && h[k].x <= b.y;
+        inc[2 * k + 1] = p[k].W.y >= kWStop && h[k].y <= b.y;
         any = any || inc[2 * k] || inc[2 * k + 1];
       }
 #ifdef SSS_COUNTERS
@@ -163,21 +169,25 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
         int ninc = 0, nlive = 0;
         for (int k = 0; k < kPX; ++k) {
           ninc += __popc(__ballot_sync(0xffffffffu, inc[k]));
-          nlive += __popc(__ballot_sync(0xffffffffu, !done[k]));
+          nlive += __popc(__ballot_sync(0xffffffffu, lane_of(p[k >> 1].W, k) >= kWStop));
         }
         if (lane == 0) { SSS_COUNT(3, ba != 0); SSS_COUNT(4, ninc); SSS_COUNT(5, nlive); }
       }
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
         const float4 c = sc[j];  // {e, r, g, b}
-        const int32_t pj = spos[j];
+        const int32_t pj1 = spos[j] + 1;
+        if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
-        for (int k = 0; k < kPairs; ++k) composite2(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
+          for (int k = 0; k < kPairs; ++k) composite2<true>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kPairs; ++k) composite2<false>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
+        }
 #pragma unroll
         for (int k = 0; k < kPX; ++k) {
-          cnt[k] += inc[k] ? 1 : 0;
-          lastc[k] = inc[k] ? pj + 1 : lastc[k];
-          done[k] = lane_of(p[k >> 1].W, k) < kWStop;
+          lastc[k] = inc[k] ? pj1 : lastc[k];
+          if (COUNT) cnt[k] += inc[k] ? 1 : 0;
         }
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(kRasterThreads) render_fwd_kernel(
     o[HW] = lane_of(pp.C1, k) + bg1 * W;
     o[2 * HW] = lane_of(pp.C2, k) + bg2 * W;
     final_T[(int64_t)v * HW + pix] = W;
-    n_contrib[(int64_t)v * HW + pix] = cnt[k];
+    if (COUNT) n_contrib[(int64_t)v * HW + pix] = cnt[k];
     last[(int64_t)v * HW + pix] = lastc[k];
   }
 }
@@ -229,21 +239,24 @@ extern "C" sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bi
   if ((st = validate_cams(cams, n_views, "sss_render_fwd")) != SSS_OK) return st;
   RasterGeom G;
   if (!raster_geom(pr, bins, cams, n_views, G)) { set_error("sss_render_fwd: geometry mismatch"); return SSS_ERR_SHAPE; }
-  if (!out->rgb || !out->final_T || !out->n_contrib || !out->last || !bins->ranges ||
+  if (!out->rgb || !out->final_T || !out->last || !bins->ranges ||
       (pr->n > 0 && (!pr->rec || !pr->rect)) || (bins->capacity > 0 && !bins->ids)) {
     set_error("sss_render_fwd: null buffer");
     return SSS_ERR_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 grid(G.tiles_x * G.tiles_y, n_views);
-  if (G.shift > 0)
-    render_fwd_kernel<true><<<grid, kRasterThreads, 0, s>>>((const float4*)pr->rec, (const short4*)pr->rect,
-                                                            bins->ids, bins->ranges, G, bg[0], bg[1], bg[2],
-                                                            out->rgb, out->final_T, out->n_contrib, out->last);
-  else
-    render_fwd_kernel<false><<<grid, kRasterThreads, 0, s>>>((const float4*)pr->rec, (const short4*)pr->rect,
-                                                             bins->ids, bins->ranges, G, bg[0], bg[1], bg[2],
-                                                             out->rgb, out->final_T, out->n_contrib, out->last);
+#define SSS_FWD_LAUNCH(F, N)                                                                       \
+  render_fwd_kernel<F, N><<<grid, kRasterThreads, 0, s>>>((const float4*)pr->rec, (const short4*)pr->rect, \
+                                                          bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], \
+                                                          out->rgb, out->final_T, out->n_contrib, out->last)
+  const bool cnt = out->n_contrib != nullptr;
+  if (G.shift > 0) {
+    if (cnt) SSS_FWD_LAUNCH(true, true); else SSS_FWD_LAUNCH(true, false);
+  } else {
+    if (cnt) SSS_FWD_LAUNCH(false, true); else SSS_FWD_LAUNCH(false, false);
+  }
+#undef SSS_FWD_LAUNCH
   count_launch();
   return check_launch("sss_render_fwd");
 }

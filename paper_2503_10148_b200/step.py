@@ -88,8 +88,11 @@ class TrainStep:
         return A.Projected(self.proj.rec[:nv], self.proj.depth[:nv], self.proj.rect[:nv])
 
     def _frame_view(self, nv: int) -> A.Frame:
+        # n_contrib is a diagnostic the backward does not read: counted only
+        # when the caller collects statistics
         f = self.frame
-        return A.Frame(f.rgb[:nv], f.final_T[:nv], f.n_contrib[:nv], f.last[:nv])
+        nc = f.n_contrib[:nv] if self.stats is not None else None
+        return A.Frame(f.rgb[:nv], f.final_T[:nv], nc, f.last[:nv])
 
     def _bins_view(self, nv: int) -> A.Bins:
         b = self.bins[0]

@@ -320,3 +320,23 @@ def test_edge_cases(orc, sss):
     bins = sss.sss_bin_sort(pr, sc.cameras, capacity=10)
     assert sss.sss_check_overflow(bins)
     assert int(bins.ranges.abs().max().item()) == 0
+
+
+def test_render_fwd_without_count_is_identical(sss, scenes):
+    """n_contrib is an optional diagnostic: a NULL buffer selects the
+    non-counting kernel, whose image, transmittance and replay offsets are
+    bit-identical to the counting one."""
+    import torch
+
+    from gpu_helpers import gpu_forward
+
+    for shift in (0, 2):
+        sc = scenes["blobs_d2_3v"]
+        params, pr, bins, fr = gpu_forward(sc, bin_shift=shift)
+        f2 = sss.Frame(torch.empty_like(fr.rgb), torch.empty_like(fr.final_T), None,
+                       torch.empty_like(fr.last))
+        sss.sss_render_fwd(pr, bins, sc.cameras, out=f2)
+        torch.cuda.synchronize()
+        assert torch.equal(f2.rgb, fr.rgb)
+        assert torch.equal(f2.final_T, fr.final_T)
+        assert torch.equal(f2.last, fr.last)

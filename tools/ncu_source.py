@@ -8,7 +8,13 @@ rows = list(csv.reader(out.splitlines()))
 hi = [i for i, r in enumerate(rows) if 'Instructions Executed' in r][0]
 h = rows[hi]
 ie, src, st = h.index('Instructions Executed'), h.index('Source'), h.index('Warp Stall Sampling (All Samples)')
-data = [(int(r[ie] or 0), int(r[st] or 0), r[src].strip()) for r in rows[hi + 1:] if len(r) > ie]
+data = []
+for r in rows[hi + 1:]:
+    if len(r) <= ie:
+        continue
+    if r[ie] == 'Instructions Executed':  # next launch's section
+        break
+    data.append((int(r[ie] or 0), int(r[st] or 0), r[src].strip()))
 tot = sum(d[0] for d in data) or 1
 tots = sum(d[1] for d in data) or 1
 print('total warp instructions', tot, 'stall samples', tots)

@@ -11,6 +11,7 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--views", type=int, default=None)
 ap.add_argument("--shift", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--no-count", action="store_true", help="forward without the n_contrib diagnostic")
 a = ap.parse_args()
 sc = make_scene(a.config, n_views=a.views)
 cams = sc.cameras
@@ -20,6 +21,7 @@ tgt = torch.from_numpy(make_targets(sc)).cuda()
 pr = P.sss_project(params, cams)
 bins = P.sss_bin_sort(pr, cams, bin_shift=a.shift)
 fr = P.sss_render_fwd(pr, bins, cams)
+fr_nc = P.Frame(fr.rgb, fr.final_T, None, fr.last)
 ws_g2d = torch.zeros(A.render_bwd_workspace_bytes(params.n, V), dtype=torch.uint8, device="cuda")
 ws_bin = torch.empty(A.bin_sort_workspace_bytes(params.n, cams, a.shift), dtype=torch.uint8, device="cuda")
 grad = P.Params.zeros_like(params)
@@ -28,7 +30,7 @@ cc = A.cameras_c(cams)
 phases = {
   "project": lambda: P.sss_project(params, cams, out=pr, cams_c=cc),
   "bin_sort": lambda: P.sss_bin_sort(pr, cams, bin_shift=a.shift, ws=ws_bin, out=bins, cams_c=cc),
-  "render_fwd": lambda: P.sss_render_fwd(pr, bins, cams, out=fr, cams_c=cc),
+  "render_fwd": lambda: P.sss_render_fwd(pr, bins, cams, out=fr_nc if a.no_count else fr, cams_c=cc),
   "render_bwd": lambda: P.sss_render_bwd(params, pr, bins, cams, fr, target=tgt, grad=grad, loss=loss, ws=ws_g2d, cams_c=cc),
 }
 res = {}
