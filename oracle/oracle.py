@@ -54,7 +54,8 @@ class _HP(C.Structure):
                 ("g_adam", C.c_int32), ("lr_scale", C.c_double), ("lr_rot", C.c_double),
                 ("lr_nu", C.c_double), ("lr_opacity", C.c_double), ("lr_sh", C.c_double),
                 ("beta1", C.c_double), ("beta2", C.c_double), ("adam_eps", C.c_double),
-                ("grad_scale", C.c_double), ("step", C.c_int64), ("seed", C.c_uint64)]
+                ("grad_scale", C.c_double), ("step", C.c_int64), ("seed", C.c_uint64),
+                ("eps_o", C.c_double), ("eps_sigma", C.c_double)]
 
 
 _lib = None
@@ -79,6 +80,8 @@ def lib():
             ("orc_philox4x32_10", None, [p, p, p]),
             ("orc_normals3", None, [C.c_uint64, i64, i64, p]),
             ("orc_sghmc_step", C.c_int, [i64, i32, p, p, p, p, p, p]),
+            ("orc_image_loss", d, [p, p, i32, i32, d, p]),
+            ("orc_regularizers", None, [i64, i32, p, p]),
         ]:
             f = getattr(_lib, name)
             f.restype = res
@@ -320,6 +323,30 @@ def l1_loss_and_grad(rgb, target):
     return float(np.mean(np.abs(diff))), np.sign(diff) / diff.size
 
 
+def image_loss(rgb, target, eps_dssim):
+    """Image part of Eq. 8 for one view: (1 - eps) L1 + eps (1 - SSIM) and
+    dL/dC (see orc_image_loss).  rgb, target: [3][H][W]."""
+    x = np.ascontiguousarray(np.asarray(rgb, np.float64))
+    y = np.ascontiguousarray(np.asarray(target, np.float64))
+    assert x.shape == y.shape and x.ndim == 3 and x.shape[0] == 3
+    d = np.zeros_like(x)
+    val = lib().orc_image_loss(_ptr(x), _ptr(y), x.shape[1], x.shape[2], float(eps_dssim), _ptr(d))
+    return float(val), d
+
+
+def ssim(a, b):
+    """Mean SSIM of two [3][H][W] images (1 - the D-SSIM term)."""
+    return 1.0 - image_loss(a, b, 1.0)[0]
+
+
+def regularizers(planes, sh_degree):
+    """(sum_i |o_i|, sum_i sum_j sqrt(lambda_ij)) of Eq. 8."""
+    pl = np.ascontiguousarray(np.asarray(planes, np.float64))
+    out = np.zeros(2)
+    lib().orc_regularizers(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(out))
+    return float(out[0]), float(out[1])
+
+
 def sghmc_step(planes, sh_degree, grad, m, v, r, hp):
     """One a7 step on fp64 copies; returns (planes, m, v, r) updated."""
     pl = np.ascontiguousarray(np.asarray(planes, np.float64)).copy()
@@ -329,7 +356,8 @@ def sghmc_step(planes, sh_degree, grad, m, v, r, hp):
     rr = np.ascontiguousarray(np.asarray(r, np.float64)).copy()
     h = _HP(hp.lr, hp.friction, hp.noise, hp.gate_k, hp.gate_t, int(hp.burn_in), int(hp.g_adam),
             hp.lr_scale, hp.lr_rot, hp.lr_nu, hp.lr_opacity, hp.lr_sh, hp.beta1, hp.beta2,
-            hp.adam_eps, hp.grad_scale, int(hp.step), int(hp.seed))
+            hp.adam_eps, hp.grad_scale, int(hp.step), int(hp.seed),
+            getattr(hp, "eps_o", 0.0), getattr(hp, "eps_sigma", 0.0))
     lib().orc_sghmc_step(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(g), _ptr(mm), _ptr(vv),
                          _ptr(rr), C.byref(h))
     return pl, mm, vv, rr

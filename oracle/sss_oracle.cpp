@@ -66,6 +66,7 @@ typedef struct {
   double beta1, beta2, adam_eps, grad_scale;
   int64_t step;
   uint64_t seed;
+  double eps_o, eps_sigma;  // regularizer weights of Eq. 8
 } orc_sghmc_hp;
 
 }  // extern "C"
@@ -835,9 +836,16 @@ int orc_sghmc_step(int64_t n, int32_t sh_degree, double* planes, const double* g
     // Adam moments on every non-mean plane; on the mean planes only when
     // g_adam is set (R17: "we employ the Adam gradient in SGHMC").
     double adir[64];
+    // Eq. 8 regularizers (R27): eps_o sum |o| and
+    // eps_Sigma sum_j sqrt(lambda_j); the eigenvalues of Sigma = R S S^T R^T
+    // are exp(2 s_j), so sqrt(lambda_j) = exp(s_j) and
+    //   d/ds_j = eps_Sigma exp(s_j),  d/draw_o = eps_o sign(o) (1 - o^2).
+    double reg[64] = {0.0};
+    for (int j = 0; j < 3; ++j) reg[3 + j] = hp->eps_sigma * std::exp(c.s[j]);
+    reg[11] = hp->eps_o * (o > 0.0 ? 1.0 : (o < 0.0 ? -1.0 : 0.0)) * (1.0 - o * o);
     for (int p = 0; p < P; ++p) {
       if (p < 3 && !hp->g_adam) { adir[p] = 0.0; continue; }
-      const double g = grad[(int64_t)p * n + i] * hp->grad_scale;
+      const double g = grad[(int64_t)p * n + i] * hp->grad_scale + reg[p];
       double& mm = m[(int64_t)p * n + i];
       double& vv = v[(int64_t)p * n + i];
       mm = hp->beta1 * mm + (1.0 - hp->beta1) * g;
@@ -869,6 +877,86 @@ int orc_sghmc_step(int64_t n, int32_t sh_degree, double* planes, const double* g
     }
   }
   return 0;
+}
+
+// ---- NEXT-1: the image part of Eq. 8 ------------------
+// L_img = (1 - eps_D) L1 + eps_D (1 - SSIM), per view and channel-averaged:
+//   L1   = mean over the 3HW values of |C - target|;
+//   SSIM = mean over channels and valid window positions p (R28: 11x11
+//          window fully inside the image, no padding) of
+//          SSIM_p = (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx2 + sy2 + C2)),
+//          with Gaussian-weighted local statistics (w = g g^T,
+//          g_k = exp(-(k-5)^2 / (2 1.5^2)) / sum, K1 = 0.01, K2 = 0.03, range 1):
+//          mx = sum w x, sx2 = sum w x^2 - mx^2, sxy = sum w x y - mx my.
+// dL/dC by the chain rule through mx, sx2, sxy (fp64, plain loops):
+//   dSSIM_p/dx_q = w_{q-p} (dS/dmx + dS/dsx2 (2 x_q - 2 mx) + dS/dsxy (y_q - my)).
+// rgb, target, d_rgb: [3][H][W]; returns L_img (d_rgb overwritten).
+double orc_image_loss(const double* rgb, const double* target, int32_t H, int32_t W, double eps_d,
+                      double* d_rgb) {
+  const int64_t P = (int64_t)H * W;
+  double l1 = 0.0;
+  for (int64_t k = 0; k < 3 * P; ++k) {
+    const double d = rgb[k] - target[k];
+    l1 += std::fabs(d);
+    d_rgb[k] = (1.0 - eps_d) * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / (3.0 * P);
+  }
+  l1 /= (double)(3 * P);
+  if (eps_d == 0.0) return l1;
+  if (H < 11 || W < 11) return std::numeric_limits<double>::quiet_NaN();
+  double g[11], gs = 0.0;
+  for (int k = 0; k < 11; ++k) { g[k] = std::exp(-(k - 5) * (k - 5) / (2.0 * 1.5 * 1.5)); gs += g[k]; }
+  for (int k = 0; k < 11; ++k) g[k] /= gs;
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  const int Hv = H - 10, Wv = W - 10;
+  const double npos = 3.0 * Hv * Wv;
+  double ssum = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double* x = rgb + c * P;
+    const double* y = target + c * P;
+    double* dx = d_rgb + c * P;
+    for (int py = 0; py < Hv; ++py)
+      for (int px = 0; px < Wv; ++px) {
+        double mx = 0, my = 0, xx = 0, yy = 0, xy = 0;
+        for (int i = 0; i < 11; ++i)
+          for (int j = 0; j < 11; ++j) {
+            const double w = g[i] * g[j];
+            const double a = x[(int64_t)(py + i) * W + px + j], b = y[(int64_t)(py + i) * W + px + j];
+            mx += w * a; my += w * b; xx += w * a * a; yy += w * b * b; xy += w * a * b;
+          }
+        const double sx2 = xx - mx * mx, sy2 = yy - my * my, sxy = xy - mx * my;
+        const double n1 = 2 * mx * my + C1, n2 = 2 * sxy + C2;
+        const double d1 = mx * mx + my * my + C1, d2 = sx2 + sy2 + C2;
+        const double S = (n1 * n2) / (d1 * d2);
+        ssum += S;
+        // partials of S
+        const double dS_dmx = (2 * my * n2) / (d1 * d2) - S * (2 * mx) / d1;
+        const double dS_dsx2 = -S / d2;
+        const double dS_dsxy = (2 * n1) / (d1 * d2);
+        const double k = -eps_d / npos;  // d(eps_D (1 - mean SSIM)) / dSSIM_p
+        for (int i = 0; i < 11; ++i)
+          for (int j = 0; j < 11; ++j) {
+            const double w = g[i] * g[j];
+            const int64_t q = (int64_t)(py + i) * W + px + j;
+            dx[q] += k * w * (dS_dmx + dS_dsx2 * (2 * x[q] - 2 * mx) + dS_dsxy * (y[q] - my));
+          }
+      }
+  }
+  return (1.0 - eps_d) * l1 + eps_d * (1.0 - ssum / npos);
+}
+
+// Eq. 8 regularizer values: out[0] = sum_i |o_i|, out[1] = sum_i sum_j sqrt(lambda_ij)
+// with lambda the eigenvalues of Sigma_i (= exp(2 s_ij), R27).
+void orc_regularizers(int64_t n, int32_t sh_degree, const double* planes, double* out) {
+  orc_params pp{n, sh_degree, 0, planes};
+  double so = 0.0, ss = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    Comp c;
+    load_comp(&pp, i, c);
+    so += std::fabs(opacity_of(c.raw_o));
+    for (int j = 0; j < 3; ++j) ss += std::exp(c.s[j]);
+  }
+  out[0] = so;
+  out[1] = ss;
 }
 
 }  // extern "C"

@@ -102,6 +102,8 @@ class SGHMCParams:
     grad_scale: float = 1.0
     step: int = 1
     seed: int = 1234
+    eps_o: float = 0.0  # Eq. 8 opacity regularizer weight (0: the BASELINE L1 objective)
+    eps_sigma: float = 0.0  # Eq. 8 sqrt-eigenvalue regularizer weight
 
 
 @dataclass
