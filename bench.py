@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    # NEXT-1: the full Eq. 8 objective (default: the BASELINE config's L1)
+    ap.add_argument("--eps-dssim", type=float, default=0.0)
+    ap.add_argument("--eps-o", type=float, default=0.0)
+    ap.add_argument("--eps-sigma", type=float, default=0.0)
     return ap.parse_args()
 
 
@@ -131,8 +135,9 @@ def ncu_traffic(kernel, views_per_launch):
     return int(b * views_per_launch / d.get("views_per_launch", views_per_launch))
 
 
-def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16):
-    """Roofline entry of the dominant kernel (largest share of the timed step)."""
+def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, kernel=None):
+    """Roofline entry of the dominant kernel (largest share of the timed step),
+    or of `kernel` if given."""
     lane_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6  # FP32 lane-ops/s (DESIGN.md §5)
     hbm_peak = pk["hbm_gbs"] * 1e9
     table = {}
@@ -148,7 +153,9 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16):
     table["render_bwd_projection"] = ("hbm", views * n * 48 + counts["launches_per_step"] * n * 4 * P * 3,
                                       hbm_peak, "GB/s")
     table["sghmc"] = ("hbm", n * 4 * (P * 7 + 6), hbm_peak, "GB/s")
-    dom = max((k for k in phase_ms if k in table), key=lambda k: phase_ms[k])
+    # image loss (L1 + D-SSIM): 132 B per pixel
+    table["image_loss"] = ("hbm", counts.get("pixels", 0) * 132, hbm_peak, "GB/s")
+    dom = kernel or max((k for k in phase_ms if k in table), key=lambda k: phase_ms[k])
     bound, work, peak, unit = table[dom]
     t = phase_ms[dom] / 1e3 / steps  # seconds per step in that kernel (all its launches)
     achieved = work / t
@@ -266,9 +273,9 @@ def main():
     tg_np = make_targets(sc, mine)
     targets = torch.from_numpy(tg_np).cuda()
     planes = torch.from_numpy(sc.params).cuda()
-    hp = sghmc_params_for(sc)
+    hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
     ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
-                   views_per_batch=a.views_per_batch)
+                   views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim)
     for _ in range(a.warmup):
         ts.step(targets)
         if ts.overflowed():
@@ -308,10 +315,16 @@ def main():
     pairs, inst = float(ts.stats["pairs"].item()), float(ts.stats["instances"].item())
     ts.stats = None
     counts = {"pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
-              "launches_per_step": len(ts.batches) * a.steps}
+              "launches_per_step": len(ts.batches) * a.steps,
+              "pixels": len(mine) * a.steps * sc.cameras[0].width * sc.cameras[0].height}
     pk = peaks()
     dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
                              views_per_launch=len(ts.batches[0]))
+    extra_roof = {}
+    if "image_loss" in phases:
+        extra_roof["image_loss"] = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
+                                                views_per_launch=len(ts.batches[0]),
+                                                kernel="image_loss")[1]
     # ---- end to end through the public API: H2D targets + loss read back
     e2e_steps = a.e2e_steps or a.steps
     host_t = torch.from_numpy(tg_np).pin_memory()
@@ -346,11 +359,15 @@ def main():
             "config": {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": V,
                        "width": W, "height": H, "sh_degree": sc.sh_degree,
                        "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch,
+                       "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
+                                if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
+                       "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
                        "parallelism": f"view-dp{world}",
                        "l2": "no flush: inputs > L2 (params 720 MB, targets 837 MB, bins GBs)"},
             "mpix_per_s_fwd_bwd": round(mpix, 2),
             "phase_ms_per_step": {k: round(v / a.steps, 3) for k, v in phases.items()},
             "roofline": roof,
+            **({"roofline_next": extra_roof} if extra_roof else {}),
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),

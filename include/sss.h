@@ -146,6 +146,11 @@ typedef struct {
   float beta1, beta2, adam_eps, grad_scale;
   int64_t step;    /* 1-based step (Adam bias correction, noise counter) */
   uint64_t seed;   /* Philox4x32-10 key */
+  /* Eq. 8 regularizers (R27), folded into the step:
+   * eps_o sum_i |o_i| adds eps_o sign(o)(1 - o^2) to d raw_opacity and
+   * eps_sigma sum_ij sqrt(lambda_ij) adds eps_sigma exp(s_j) to d log_scale_j
+   * (after grad_scale).  0, 0 = the BASELINE L1 objective. */
+  float eps_o, eps_sigma;
 } sss_sghmc_hparams;
 
 /* flags for sss_render_bwd */
@@ -204,6 +209,24 @@ SSS_API sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, 
                           const sss_frame* fwd, const float* d_rgb, const float* target,
                           float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
                           int32_t flags, void* stream);
+
+/* Bytes of device scratch sss_image_loss needs for n_views views of
+ * height x width (the three SSIM partial-derivative maps over the valid
+ * window positions).  0 on invalid input. */
+SSS_API size_t sss_image_loss_workspace(int32_t n_views, int32_t height, int32_t width);
+
+/* NEXT-1 — image part of Eq. 8 for a batch of views:
+ *   L_v = (1 - eps_dssim) mean|C - T| + eps_dssim (1 - SSIM(C, T)),
+ * SSIM the mean over channels and valid 11x11 window positions of the local
+ * SSIM with a Gaussian window (sigma 1.5, K1 0.01, K2 0.03, range 1; R28).
+ * rgb, target: [V][3][H][W] device; d_rgb (out, overwritten): dL_v/dC in the
+ * same layout, ready for sss_render_bwd's d_rgb; loss (device float[1],
+ * nullable) is incremented by sum_v L_v.  eps_dssim in [0, 1]; with
+ * eps_dssim > 0 both sides must be >= 11 pixels (else SSS_ERR_SHAPE).
+ * ws: at least sss_image_loss_workspace() bytes. */
+SSS_API sss_status sss_image_loss(const float* rgb, const float* target, int32_t n_views, int32_t height,
+                                  int32_t width, float eps_dssim, float* d_rgb, float* loss, void* ws,
+                                  size_t ws_bytes, void* stream);
 
 /* a7 — one sampler step in place (Eq. 10, 1492-1523; Adam on
  * every non-mean group).  p, adam_m, adam_v: device

@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     n_planes,
     sss_bin_sort,
     sss_check_overflow,
+    sss_image_loss,
     sss_project,
     sss_render_bwd,
     sss_render_fwd,

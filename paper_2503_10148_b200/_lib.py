@@ -23,6 +23,7 @@ SSS_BWD_PROJECTION_ONLY = 4
 
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",
+           "sss_image_loss_workspace", "sss_image_loss",
            "sss_status_string", "sss_last_error", "sss_launch_count"]
 
 
@@ -60,7 +61,8 @@ class sss_sghmc_hparams(C.Structure):
                 ("g_adam", C.c_int32), ("lr_scale", C.c_float), ("lr_rot", C.c_float),
                 ("lr_nu", C.c_float), ("lr_opacity", C.c_float), ("lr_sh", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
-                ("grad_scale", C.c_float), ("step", C.c_int64), ("seed", C.c_uint64)]
+                ("grad_scale", C.c_float), ("step", C.c_int64), ("seed", C.c_uint64),
+                ("eps_o", C.c_float), ("eps_sigma", C.c_float)]
 
 
 _lib = None
@@ -96,6 +98,9 @@ def load(path: str = LIB_PATH):
                                 P(sss_params), vp, C.c_size_t, C.c_int32, vp]),
         "sss_sghmc_step": (st, [P(sss_params), P(sss_params), P(sss_params), P(sss_params), vp,
                                 P(sss_sghmc_hparams), vp]),
+        "sss_image_loss_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+        "sss_image_loss": (st, [vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, vp, vp, vp,
+                                C.c_size_t, vp]),
         "sss_status_string": (C.c_char_p, [C.c_int]),
         "sss_last_error": (C.c_char_p, []),
         "sss_launch_count": (C.c_int64, [C.c_int32]),

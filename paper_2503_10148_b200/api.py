@@ -162,7 +162,8 @@ def hparams_c(hp) -> L.sss_sghmc_hparams:
     return L.sss_sghmc_hparams(hp.lr, hp.friction, hp.noise, hp.gate_k, hp.gate_t,
                                int(hp.burn_in), int(hp.g_adam), hp.lr_scale, hp.lr_rot, hp.lr_nu,
                                hp.lr_opacity, hp.lr_sh, hp.beta1, hp.beta2, hp.adam_eps,
-                               hp.grad_scale, int(hp.step), int(hp.seed))
+                               hp.grad_scale, int(hp.step), int(hp.seed),
+                               float(getattr(hp, "eps_o", 0.0)), float(getattr(hp, "eps_sigma", 0.0)))
 
 
 # ------------------------------------------------------------- entry points
@@ -271,6 +272,30 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
                                _ptr(d_rgb), _ptr(target), _ptr(loss), C.byref(gc), _ptr(ws),
                                ws.numel(), flags, _stream_ptr(stream)), "sss_render_bwd")
     return grad
+
+
+def image_loss_workspace_bytes(V: int, H: int, W: int) -> int:
+    return int(L.load().sss_image_loss_workspace(V, H, W))
+
+
+def sss_image_loss(rgb: torch.Tensor, target: torch.Tensor, eps_dssim: float,
+                   d_rgb: Optional[torch.Tensor] = None, loss: Optional[torch.Tensor] = None,
+                   ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Image part of Eq. 8 for [V][3][H][W] renders: writes dL/dC into d_rgb
+    (returned) and adds sum_v L_v to `loss` (device float[1]) if given."""
+    lib = L.load()
+    assert rgb.shape == target.shape and rgb.dim() == 4 and rgb.shape[1] == 3
+    for t in (rgb, target):
+        assert t.is_contiguous() and t.dtype == torch.float32
+    V, _, H, W = rgb.shape
+    d_rgb = d_rgb if d_rgb is not None else torch.empty_like(rgb)
+    need = image_loss_workspace_bytes(V, H, W)
+    if ws is None:
+        ws = torch.empty(max(need, 4), dtype=torch.uint8, device=rgb.device)
+    L.check(lib.sss_image_loss(_ptr(rgb), _ptr(target), V, H, W, float(eps_dssim), _ptr(d_rgb),
+                               _ptr(loss), _ptr(ws), ws.numel(), _stream_ptr(stream)),
+            "sss_image_loss")
+    return d_rgb
 
 
 def sss_sghmc_step(params: Params, grad: Params, adam_m: Params, adam_v: Params,

@@ -8,6 +8,8 @@
 //   mu'   = mu - eps^2 g + gate (F + N),  F = eps (1 - eps C) r,  N = eta xi
 //   gate  = sigmoid(-k (|o| - t))
 //   burn-in: F = 0, N = eta Sigma xi (Sigma of the pre-update component)
+//   Eq. 8 regularizers (R27): g(log_scale_j) += eps_Sigma exp(s_j),
+//         g(raw_o) += eps_o sign(o)(1 - o^2)  (sqrt(lambda_j(Sigma)) = exp(s_j))
 //   Adam: m' = b1 m + (1-b1) g, v' = b2 v + (1-b2) g^2,
 //         theta -= lr (m'/(1-b1^t)) / (sqrt(v'/(1-b2^t)) + eps_hat)
 // xi: three standard normals from Philox4x32-10 (cuRAND's device function),
@@ -28,6 +30,7 @@ struct HP {
   int burn_in, g_adam;
   float lr_group[5];  // log_scale, rot, nu, opacity, sh
   float beta1, beta2, adam_eps, grad_scale;
+  float eps_o, eps_sigma;  // Eq. 8 regularizer weights
   float inv_b1t, inv_b2t;  // 1 / (1 - beta^t)
   uint32_t ctr2, ctr3;     // step (lo, hi)
   uint32_t key0, key1;     // seed (lo, hi)
@@ -42,8 +45,8 @@ __device__ __forceinline__ float adam_dir(float g, float* m, float* v, int64_t i
 }
 
 __device__ __forceinline__ void adam_plane(float* theta, const float* grad, float* m, float* v, int64_t i,
-                                           float lr, const HP& hp) {
-  const float g = grad[i] * hp.grad_scale;
+                                           float lr, const HP& hp, float reg = 0.f) {
+  const float g = fmaf(grad[i], hp.grad_scale, reg);
   theta[i] -= lr * adam_dir(g, m, v, i, hp);
 }
 
@@ -102,10 +105,15 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
   }
   // ---- Adam on the other groups
-  for (int a = 0; a < 3; ++a) adam_plane(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, a * n + i, hp.lr_group[0], hp);
+  for (int a = 0; a < 3; ++a) {
+    const int64_t idx = a * n + i;
+    const float reg = hp.eps_sigma != 0.f ? hp.eps_sigma * expf(P.log_scale[idx]) : 0.f;
+    adam_plane(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, idx, hp.lr_group[0], hp, reg);
+  }
   for (int a = 0; a < 4; ++a) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
   adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
-  adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp);
+  const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (1.f - o * o);
+  adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
   for (int k = 0; k < 3 * K; ++k) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
 }
 
@@ -136,6 +144,7 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
   hp.lr_group[0] = h->lr_scale; hp.lr_group[1] = h->lr_rot; hp.lr_group[2] = h->lr_nu;
   hp.lr_group[3] = h->lr_opacity; hp.lr_group[4] = h->lr_sh;
   hp.beta1 = h->beta1; hp.beta2 = h->beta2; hp.adam_eps = h->adam_eps; hp.grad_scale = h->grad_scale;
+  hp.eps_o = h->eps_o; hp.eps_sigma = h->eps_sigma;
   hp.inv_b1t = (float)(1.0 / (1.0 - pow((double)h->beta1, (double)h->step)));
   hp.inv_b2t = (float)(1.0 / (1.0 - pow((double)h->beta2, (double)h->step)));
   hp.ctr2 = (uint32_t)h->step; hp.ctr3 = (uint32_t)((uint64_t)h->step >> 32);

@@ -25,7 +25,8 @@ class TrainStep:
                  total_views: Optional[int] = None, bin_shift: int = 0,
                  views_per_batch: int = 16, bg=(0.0, 0.0, 0.0), headroom: float = 1.25,
                  group=None, momentum: Optional[torch.Tensor] = None,
-                 adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None):
+                 adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
+                 eps_dssim: float = 0.0):
         dev = planes.device
         self.params = A.Params(planes, sh_degree)
         self.grad = A.Params.zeros_like(self.params)
@@ -55,6 +56,15 @@ class TrainStep:
         self.ws_g2d = torch.zeros(max(A.render_bwd_workspace_bytes(n, vb), 4), dtype=torch.uint8,
                                   device=dev)
         self.loss = torch.zeros(1, device=dev)
+        # Eq. 8 image loss: eps_dssim = 0 keeps the fused-L1 backward (BASELINE
+        # configs); > 0 forms (1 - eps) L1 + eps D-SSIM and its image gradient
+        # with sss_image_loss, then runs the backward on that gradient.  The
+        # regularizer weights travel in hp (eps_o, eps_sigma).
+        self.eps_dssim = float(eps_dssim)
+        if self.eps_dssim > 0.0:
+            self.d_rgb = torch.empty((vb, 3, H, W), dtype=torch.float32, device=dev)
+            self.ws_loss = torch.empty(max(A.image_loss_workspace_bytes(vb, H, W), 4),
+                                       dtype=torch.uint8, device=dev)
         self.bins: List[A.Bins] = []
         self.prof = None  # list of (phase, cuda event) when timing phases
         self.stats = None  # dict of device counters (pairs, instances) when counting
@@ -121,17 +131,19 @@ class TrainStep:
             if self.stats is not None:
                 self.stats["pairs"] += fv.n_contrib.sum(dtype=torch.int64)
                 self.stats["instances"] += bv.totals.sum()
+            d_rgb = None
+            if self.eps_dssim > 0.0:
+                d_rgb = A.sss_image_loss(fv.rgb, tg, self.eps_dssim, d_rgb=self.d_rgb[:nv],
+                                         loss=self.loss, ws=self.ws_loss)
+                self._mark("image_loss")
+            kw = dict(bg=self.bg, target=None if d_rgb is not None else tg, d_rgb=d_rgb,
+                      grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
             if self.prof is None:
-                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
-                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, **kw)
             else:  # same two kernels, split so each can be timed
-                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
-                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc,
-                                 half="raster")
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, half="raster", **kw)
                 self._mark("render_bwd_raster")
-                A.sss_render_bwd(self.params, pv, bv, cams, fv, bg=self.bg, target=tg,
-                                 grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc,
-                                 half="projection")
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, half="projection", **kw)
                 self._mark("render_bwd_projection")
 
     def step(self, targets: torch.Tensor) -> torch.Tensor:
