@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--views-per-batch", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row timings")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     # NEXT-1: the full Eq. 8 objective (default: the BASELINE config's L1)
     ap.add_argument("--eps-dssim", type=float, default=0.0)
@@ -165,6 +166,52 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, ker
                  "traffic_unit": "dram bytes per launch (ncu --set full, profiles/traffic.json)",
                  "peak_source": pk["source"] + (" (148 SMs x 128 FP32 lanes x sm_max_mhz)" if bound == "alu" else " hbm_gbs"),
                  "share_of_step": round(phase_ms[dom] / sum(phase_ms.values()), 3)}
+
+
+def time_next_rows(ts, targets, pk):
+    """NEXT-1 image loss (L1 + D-SSIM, eps 0.2) on the last view batch's
+    frames, and one NEXT-2 recycling pass (5% cap) on a copy of the step's
+    parameters, each timed with CUDA events on the launching stream."""
+    import torch
+
+    import paper_2503_10148_b200 as P
+    from paper_2503_10148_b200 import api as A
+
+    def timed(fn, reps=5):
+        fn()
+        ts_ = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts_.append(e0.elapsed_time(e1))
+        return sorted(ts_)[len(ts_) // 2]
+
+    out = {}
+    nv = len(ts.batches[-1])
+    fr = ts.frame.rgb[:nv]
+    tg = targets[ts.batches[-1][0]:ts.batches[-1][-1] + 1]
+    V, _, H, W = fr.shape
+    d = torch.empty_like(fr)
+    ws = torch.empty(max(A.image_loss_workspace_bytes(V, H, W), 4), dtype=torch.uint8, device=fr.device)
+    ms = timed(lambda: P.sss_image_loss(fr, tg, 0.2, d_rgb=d, ws=ws))
+    gbs = V * H * W * 132 / (ms / 1e3) / 1e9
+    out["image_loss"] = {"ms": round(ms, 3), "views": V, "bound": "hbm", "achieved_gbs": round(gbs, 1),
+                         "peak_gbs": pk["hbm_gbs"], "frac": round(gbs / pk["hbm_gbs"], 4),
+                         "bytes_per_pixel": 132}
+    planes = ts.params.planes.clone()
+    params = P.Params(planes, ts.params.sh_degree)
+    m, v = P.Params(torch.zeros_like(planes), params.sh_degree), P.Params(torch.zeros_like(planes), params.sh_degree)
+    r = torch.zeros((3, params.n), device=planes.device)
+    ws_r = torch.empty(A.relocate_workspace_bytes(params.n), dtype=torch.uint8, device=planes.device)
+    moved = torch.zeros(1, dtype=torch.int64, device=planes.device)
+    ms_r = timed(lambda: P.sss_relocate(params, m, v, r, seed=1, step=1, n_moved=moved, ws=ws_r))
+    out["relocate"] = {"ms": round(ms_r, 3), "n": params.n, "moved": int(moved.item()),
+                       "note": "one recycling pass (dead |o| < 0.005, 5% cap, n_max 32)"}
+    del planes, params, m, v, r, ws_r
+    return out
 
 
 def cpu_baseline_sample(scene, targets_np, budget_s, views_total):
@@ -344,6 +391,10 @@ def main():
     e2e = {"value": round(e2e_steps / (e2e_ms / 1e3), 4), "unit": "it/s",
            "h2d_bytes_per_step": int(host_t.numel() * 4), "d2h_bytes_per_step": 4}
     del dev_t, host_t
+    # ---- NEXT rows, timed outside the step (CUDA events, 5 repeats, median)
+    next_rows = {}
+    if not a.no_next:
+        next_rows = time_next_rows(ts, targets, pk)
     if rank == 0:
         cb = None
         if world == 1 and not a.no_cpu_baseline:
@@ -371,6 +422,7 @@ def main():
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "next_rows": next_rows,
             "clocks": clocks,
             "bin_overflow": bool(overflow),
         }

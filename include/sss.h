@@ -228,6 +228,34 @@ SSS_API sss_status sss_image_loss(const float* rgb, const float* target, int32_t
                                   int32_t width, float eps_dssim, float* d_rgb, float* loss, void* ws,
                                   size_t ws_bytes, void* stream);
 
+/* Settings of one recycling pass (host struct; R29-R31). */
+typedef struct {
+  float threshold; /* dead iff |o| < threshold (0.005, the gate threshold) */
+  float cap_frac;  /* at most floor(cap_frac * n) dead relocated per pass (0.05) */
+  int32_t n_max;   /* at most n_max members per group incl. the target, in [2, 64] (R29) */
+  int32_t reserved;
+  uint64_t seed;   /* Philox4x32-10 key of the multinomial draws */
+  int64_t step;    /* draw counter (the pass's iteration number) */
+} sss_relocate_params;
+
+/* Bytes of device scratch sss_relocate needs for n components. */
+SSS_API size_t sss_relocate_workspace(int64_t n);
+
+/* NEXT-2 — one component-recycling pass in place (PAPER.md:168-183 Eqs.
+ * 11-12, 1317-1460; 1081 multinomial over opacity).  Dead components
+ * (|o| < threshold) are moved onto live targets drawn with probability
+ * proportional to |o|; each group of N members (target + dead) takes the
+ * target's mean, rotation, nu and SH, o_new with (1 - o_new)^N = 1 - o_old
+ * and Sigma_new = o_old^2 (beta(1/2,(nu+2)/2)/K)^2 Sigma_old (Eq. 12,
+ * nu_new = nu_old); momentum and Adam moments of the members are reset.
+ * p, adam_m, adam_v must each be one flat [P][n] device buffer (planes
+ * consecutive, as sss_params documents); momentum [3][n].  target_of
+ * (device int32[n], nullable): the target of every relocated component, -1
+ * elsewhere.  n_moved (device int64[1]): number relocated.  n < 2^31. */
+SSS_API sss_status sss_relocate(sss_params* p, sss_params* adam_m, sss_params* adam_v, float* momentum,
+                                const sss_relocate_params* rp, int32_t* target_of, int64_t* n_moved,
+                                void* ws, size_t ws_bytes, void* stream);
+
 /* a7 — one sampler step in place (Eq. 10, 1492-1523; Adam on
  * every non-mean group).  p, adam_m, adam_v: device
  * planes (same n / sh_degree); grad read-only; momentum [3][n] device; hp host.

@@ -82,6 +82,9 @@ def lib():
             ("orc_sghmc_step", C.c_int, [i64, i32, p, p, p, p, p, p]),
             ("orc_image_loss", d, [p, p, i32, i32, d, p]),
             ("orc_regularizers", None, [i64, i32, p, p]),
+            ("orc_beta", d, [d, d]), ("orc_reloc_opacity", d, [d, i32]),
+            ("orc_reloc_K", d, [i32, d, d]), ("orc_reloc_scale", d, [d, d, d, i32]),
+            ("orc_relocate", i64, [i64, i32, p, p, p, p, d, d, i32, C.c_uint64, i64, p]),
         ]:
             f = getattr(_lib, name)
             f.restype = res
@@ -345,6 +348,36 @@ def regularizers(planes, sh_degree):
     out = np.zeros(2)
     lib().orc_regularizers(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(out))
     return float(out[0]), float(out[1])
+
+
+def beta(x, y):
+    return lib().orc_beta(float(x), float(y))
+
+
+def reloc_opacity(o_old, N):
+    return lib().orc_reloc_opacity(float(o_old), int(N))
+
+
+def reloc_K(N, o_new, nu_new):
+    return lib().orc_reloc_K(int(N), float(o_new), float(nu_new))
+
+
+def reloc_scale(o_old, nu_old, nu_new, N):
+    return lib().orc_reloc_scale(float(o_old), float(nu_old), float(nu_new), int(N))
+
+
+def relocate(planes, sh_degree, m, v, r, threshold=0.005, cap_frac=0.05, n_max=32, seed=0, step=1):
+    """One recycling pass (orc_relocate) on fp64 copies; returns
+    (planes, m, v, r, target_of, moved)."""
+    pl = np.ascontiguousarray(np.asarray(planes, np.float64)).copy()
+    mm = np.ascontiguousarray(np.asarray(m, np.float64)).copy()
+    vv = np.ascontiguousarray(np.asarray(v, np.float64)).copy()
+    rr = np.ascontiguousarray(np.asarray(r, np.float64)).copy()
+    tg = np.zeros(pl.shape[1], np.int32)
+    moved = lib().orc_relocate(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(mm), _ptr(vv), _ptr(rr),
+                               float(threshold), float(cap_frac), int(n_max), int(seed), int(step),
+                               _ptr(tg))
+    return pl, mm, vv, rr, tg, int(moved)
 
 
 def sghmc_step(planes, sh_degree, grad, m, v, r, hp):

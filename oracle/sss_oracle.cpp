@@ -959,4 +959,127 @@ void orc_regularizers(int64_t n, int32_t sh_degree, const double* planes, double
   out[1] = ss;
 }
 
+// ---- NEXT-2: component recycling (Eqs. 11-12, SM
+// "Component Recycling" PAPER.md:1317-1460, implementation PAPER.md:1081) --
+
+// beta(x, y) through ln Gamma, as the paper evaluates it.
+double orc_beta(double x, double y) { return std::exp(std::lgamma(x) + std::lgamma(y) - std::lgamma(x + y)); }
+
+// (1 - o_new)^N = 1 - o_old (Eq. 12), signed o as printed (R29: the sign of
+// o_new follows o_old).
+double orc_reloc_opacity(double o_old, int32_t N) { return 1.0 - std::pow(1.0 - o_old, 1.0 / N); }
+
+// K of Eq. 12, the paper's double sum in its order:
+//   K = sum_{i=1}^{N} sum_{k=0}^{i-1} C(i-1, k) (-1)^k o_new^{k+1} Z_k,
+//   Z_k = beta(1/2, ((k+1)(nu_new + 3) - 1) / 2).
+double orc_reloc_K(int32_t N, double o_new, double nu_new) {
+  double K = 0.0;
+  for (int i = 1; i <= N; ++i) {
+    double binom = 1.0;  // C(i-1, 0)
+    for (int k = 0; k <= i - 1; ++k) {
+      const double Z = orc_beta(0.5, ((k + 1) * (nu_new + 3.0) - 1.0) / 2.0);
+      K += binom * ((k % 2) ? -1.0 : 1.0) * std::pow(o_new, k + 1) * Z;
+      binom = binom * (double)(i - 1 - k) / (double)(k + 1);
+    }
+  }
+  return K;
+}
+
+// Sigma_new / Sigma_old of Eq. 12:
+//   (o_old)^2 (nu_old / nu_new) (beta(1/2, (nu_old + 2)/2) / K)^2.
+double orc_reloc_scale(double o_old, double nu_old, double nu_new, int32_t N) {
+  const double o_new = orc_reloc_opacity(o_old, N);
+  const double K = orc_reloc_K(N, o_new, nu_new);
+  const double b = orc_beta(0.5, (nu_old + 2.0) / 2.0);
+  return o_old * o_old * (nu_old / nu_new) * (b / K) * (b / K);
+}
+
+// One recycling pass (readings R29-R31):
+//  1. dead = components with |o| < threshold, o = fp32(tanh(raw_o)) (the
+//     decision is taken in fp32, as on the GPU), in index order;
+//  2. at most floor(cap_frac * n) of them (the first ones) are relocated;
+//  3. targets: multinomial over the live components with probability
+//     proportional to |o| ("Multinomial distribution of opacity values"),
+//     as integer weights w_i = floor(|o_i| 2^32); draw j takes
+//     u = floor(r_j * total / 2^64), r_j = 64 Philox bits (counter
+//     (j, 0x52454C4F, step lo, step hi), key seed), target = first i with
+//     w_0 + ... + w_i > u;
+//  4. a target keeps at most n_max - 1 dead (in j order); the others stay
+//     dead for the next pass;
+//  5. per target t with N - 1 accepted dead (N members after relocation):
+//     o_new, Sigma_new of Eq. 12 with nu_new = nu_old (R30); every member
+//     takes t's mean, rotation, nu and SH, raw_o = atanh(o_new) and
+//     log_scale_t + ln(scale)/2; momentum and Adam moments of all members
+//     are reset to 0 (R31).
+// target_of[n] (out): t for every relocated dead component, -1 otherwise.
+// Returns the number of relocated components.
+int64_t orc_relocate(int64_t n, int32_t sh_degree, double* planes, double* m, double* v, double* r,
+                     double threshold, double cap_frac, int32_t n_max, uint64_t seed, int64_t step,
+                     int32_t* target_of) {
+  const int P = n_planes(sh_degree);
+  std::vector<int64_t> dead;
+  std::vector<uint64_t> cum(n);
+  uint64_t total = 0;
+  const float thr = (float)threshold;
+  for (int64_t i = 0; i < n; ++i) {
+    target_of[i] = -1;
+    const float o32 = (float)std::tanh(planes[11 * n + i]);
+    const float a = std::fabs(o32);
+    if (a < thr) {
+      dead.push_back(i);
+    } else {
+      total += (uint64_t)std::floor((double)a * 4294967296.0);
+    }
+    cum[i] = total;
+  }
+  const int64_t cap = (int64_t)std::floor(cap_frac * (double)n);
+  const int64_t n_sel = std::min<int64_t>((int64_t)dead.size(), cap);
+  if (n_sel == 0 || total == 0) return 0;
+  // 3. draws
+  std::vector<int64_t> tgt(n_sel);
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (int64_t j = 0; j < n_sel; ++j) {
+    const uint32_t ctr[4] = {(uint32_t)j, 0x52454C4Fu, (uint32_t)step, (uint32_t)((uint64_t)step >> 32)};
+    uint32_t x[4];
+    orc_philox4x32_10(ctr, key, x);
+    const uint64_t r64 = (uint64_t)x[0] | ((uint64_t)x[1] << 32);
+    const uint64_t u = (uint64_t)(((unsigned __int128)r64 * total) >> 64);
+    int64_t lo = 0, hi = n - 1;  // first i with cum[i] > u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (cum[mid] > u) hi = mid; else lo = mid + 1;
+    }
+    tgt[j] = lo;
+  }
+  // 4. groups in j order, at most n_max - 1 dead per target
+  std::vector<std::vector<int64_t>> members(n);
+  for (int64_t j = 0; j < n_sel; ++j)
+    if ((int32_t)members[tgt[j]].size() < n_max - 1) members[tgt[j]].push_back(dead[j]);
+  // 5. Eq. 12 per group
+  int64_t moved = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    if (members[t].empty()) continue;
+    const int N = 1 + (int)members[t].size();
+    const double o_old = opacity_of(planes[11 * n + t]);
+    const double nu = nu_of(planes[10 * n + t]);
+    const double o_new = orc_reloc_opacity(o_old, N);
+    const double scale = orc_reloc_scale(o_old, nu, nu, N);
+    planes[11 * n + t] = std::atanh(o_new);
+    for (int j = 0; j < 3; ++j) planes[(3 + j) * n + t] += 0.5 * std::log(scale);
+    std::vector<int64_t> all = members[t];
+    all.push_back(t);
+    for (int64_t d : all) {
+      for (int p = 0; p < P; ++p) {
+        planes[(int64_t)p * n + d] = planes[(int64_t)p * n + t];
+        m[(int64_t)p * n + d] = 0.0;
+        v[(int64_t)p * n + d] = 0.0;
+      }
+      for (int a = 0; a < 3; ++a) r[(int64_t)a * n + d] = 0.0;
+      if (d != t) target_of[d] = (int32_t)t;
+    }
+    moved += (int64_t)members[t].size();
+  }
+  return moved;
+}
+
 }  // extern "C"

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     Params,
     Projected,
     cameras_c,
+    grow,
     launch_count,
     n_bins_of,
     n_planes,
@@ -18,6 +19,7 @@ from .api import (  # noqa: F401
     sss_check_overflow,
     sss_image_loss,
     sss_project,
+    sss_relocate,
     sss_render_bwd,
     sss_render_fwd,
     sss_sghmc_step,

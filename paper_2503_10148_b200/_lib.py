@@ -23,7 +23,7 @@ SSS_BWD_PROJECTION_ONLY = 4
 
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",
-           "sss_image_loss_workspace", "sss_image_loss",
+           "sss_image_loss_workspace", "sss_image_loss", "sss_relocate_workspace", "sss_relocate",
            "sss_status_string", "sss_last_error", "sss_launch_count"]
 
 
@@ -65,6 +65,11 @@ class sss_sghmc_hparams(C.Structure):
                 ("eps_o", C.c_float), ("eps_sigma", C.c_float)]
 
 
+class sss_relocate_params(C.Structure):
+    _fields_ = [("threshold", C.c_float), ("cap_frac", C.c_float), ("n_max", C.c_int32),
+                ("reserved", C.c_int32), ("seed", C.c_uint64), ("step", C.c_int64)]
+
+
 _lib = None
 
 
@@ -101,6 +106,9 @@ def load(path: str = LIB_PATH):
         "sss_image_loss_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
         "sss_image_loss": (st, [vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_float, vp, vp, vp,
                                 C.c_size_t, vp]),
+        "sss_relocate_workspace": (C.c_size_t, [C.c_int64]),
+        "sss_relocate": (st, [P(sss_params), P(sss_params), P(sss_params), vp, P(sss_relocate_params),
+                              vp, vp, vp, C.c_size_t, vp]),
         "sss_status_string": (C.c_char_p, [C.c_int]),
         "sss_last_error": (C.c_char_p, []),
         "sss_launch_count": (C.c_int64, [C.c_int32]),

@@ -298,6 +298,44 @@ def sss_image_loss(rgb: torch.Tensor, target: torch.Tensor, eps_dssim: float,
     return d_rgb
 
 
+def relocate_workspace_bytes(n: int) -> int:
+    return int(L.load().sss_relocate_workspace(n))
+
+
+def sss_relocate(params: Params, adam_m: Params, adam_v: Params, momentum: torch.Tensor,
+                 threshold: float = 0.005, cap_frac: float = 0.05, n_max: int = 32, seed: int = 0,
+                 step: int = 1, target_of: Optional[torch.Tensor] = None,
+                 n_moved: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    """One recycling pass in place (NEXT-2); returns the device int64[1]
+    count of relocated components (no host sync)."""
+    lib = L.load()
+    dev = params.planes.device
+    n_moved = n_moved if n_moved is not None else torch.zeros(1, dtype=torch.int64, device=dev)
+    need = relocate_workspace_bytes(params.n)
+    if ws is None:
+        ws = torch.empty(max(need, 4), dtype=torch.uint8, device=dev)
+    rp = L.sss_relocate_params(float(threshold), float(cap_frac), int(n_max), 0, int(seed), int(step))
+    pc, mc, vc = params.c(), adam_m.c(), adam_v.c()
+    L.check(lib.sss_relocate(C.byref(pc), C.byref(mc), C.byref(vc), _ptr(momentum), C.byref(rp),
+                             _ptr(target_of), _ptr(n_moved), _ptr(ws), ws.numel(),
+                             _stream_ptr(stream)), "sss_relocate")
+    return n_moved
+
+
+def grow(planes: torch.Tensor, sh_degree: int, frac: float = 0.05) -> torch.Tensor:
+    """Adds floor(frac * n) components with zero opacity ("we
+    add 5% new components with zero opacity and then recycle them"): a new
+    flat [P][n'] buffer whose new columns are identity rotations with
+    raw_opacity 0, i.e. dead for the next sss_relocate pass.  Host-side
+    memory management only (no method arithmetic)."""
+    P, n = planes.shape
+    add = int(frac * n)
+    extra = torch.zeros((P, add), dtype=planes.dtype, device=planes.device)
+    extra[6] = 1.0  # quaternion w
+    return torch.cat([planes, extra], dim=1).contiguous()
+
+
 def sss_sghmc_step(params: Params, grad: Params, adam_m: Params, adam_v: Params,
                    momentum: torch.Tensor, hp, stream=None) -> None:
     lib = L.load()
