@@ -38,7 +38,7 @@ class _Cam(C.Structure):
 
 
 class _Params(C.Structure):
-    _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("pad_", C.c_int32),
+    _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("variant", C.c_int32),
                 ("planes", C.POINTER(C.c_double))]
 
 
@@ -55,7 +55,8 @@ class _HP(C.Structure):
                 ("lr_nu", C.c_double), ("lr_opacity", C.c_double), ("lr_sh", C.c_double),
                 ("beta1", C.c_double), ("beta2", C.c_double), ("adam_eps", C.c_double),
                 ("grad_scale", C.c_double), ("step", C.c_int64), ("seed", C.c_uint64),
-                ("eps_o", C.c_double), ("eps_sigma", C.c_double)]
+                ("eps_o", C.c_double), ("eps_sigma", C.c_double), ("mu_mode", C.c_int32),
+                ("variant", C.c_int32)]
 
 
 _lib = None
@@ -81,10 +82,11 @@ def lib():
             ("orc_normals3", None, [C.c_uint64, i64, i64, p]),
             ("orc_sghmc_step", C.c_int, [i64, i32, p, p, p, p, p, p]),
             ("orc_image_loss", d, [p, p, i32, i32, d, p]),
-            ("orc_regularizers", None, [i64, i32, p, p]),
+            ("orc_regularizers", None, [i64, i32, p, p, i32]),
+            ("orc_opacity_of_v", d, [d, i32]),
             ("orc_beta", d, [d, d]), ("orc_reloc_opacity", d, [d, i32]),
             ("orc_reloc_K", d, [i32, d, d]), ("orc_reloc_scale", d, [d, d, d, i32]),
-            ("orc_relocate", i64, [i64, i32, p, p, p, p, d, d, i32, C.c_uint64, i64, p]),
+            ("orc_relocate", i64, [i64, i32, p, p, p, p, d, d, i32, C.c_uint64, i64, p, i32]),
         ]:
             f = getattr(_lib, name)
             f.restype = res
@@ -116,9 +118,9 @@ def _cam(cam) -> _Cam:
 class _P:
     """Keeps the fp64 plane copy alive while ctypes holds a pointer to it."""
 
-    def __init__(self, planes, sh_degree):
+    def __init__(self, planes, sh_degree, variant=0):
         self.arr = np.ascontiguousarray(np.asarray(planes, np.float64))
-        self.s = _Params(self.arr.shape[1], int(sh_degree), 0,
+        self.s = _Params(self.arr.shape[1], int(sh_degree), int(variant),
                          self.arr.ctypes.data_as(C.POINTER(C.c_double)))
 
     @property
@@ -129,6 +131,10 @@ class _P:
 # --------------------------------------------------------------- primitives
 def nu_of(raw):
     return lib().orc_nu_of(float(raw))
+
+
+def opacity_of_v(raw, variant):
+    return lib().orc_opacity_of_v(float(raw), int(variant))
 
 
 def opacity_of(raw):
@@ -202,8 +208,8 @@ class Projection:
     color: np.ndarray
 
 
-def project(planes, sh_degree, cam) -> Projection:
-    P = _P(planes, sh_degree)
+def project(planes, sh_degree, cam, variant=0) -> Projection:
+    P = _P(planes, sh_degree, variant)
     n = P.arr.shape[1]
     f32 = lambda: np.zeros(n, np.float32)  # noqa: E731
     pr = Projection(mx=f32(), my=f32(), A=f32(), B2=f32(), C=f32(), hmax=f32(), depth=f32(),
@@ -223,9 +229,9 @@ def tiles_of(cam):
     return (cam.width + 15) // 16, (cam.height + 15) // 16
 
 
-def bin_sort(planes, sh_degree, cam, want_keys=True):
+def bin_sort(planes, sh_degree, cam, want_keys=True, variant=0):
     """Returns (tile_counts[tiles], ids[M], keys[M] or None)."""
-    P = _P(planes, sh_degree)
+    P = _P(planes, sh_degree, variant)
     c = _cam(cam)
     tw, th = tiles_of(cam)
     counts = np.zeros(tw * th, np.int32)
@@ -236,8 +242,8 @@ def bin_sort(planes, sh_degree, cam, want_keys=True):
     return counts, ids, keys
 
 
-def tile_lists(planes, sh_degree, cam, tiles):
-    P = _P(planes, sh_degree)
+def tile_lists(planes, sh_degree, cam, tiles, variant=0):
+    P = _P(planes, sh_degree, variant)
     c = _cam(cam)
     sel = np.ascontiguousarray(np.asarray(tiles, np.int32))
     counts = np.zeros(len(sel), np.int32)
@@ -264,9 +270,9 @@ class Frame:
 
 
 def render(planes, sh_degree, cam, bg=(0.0, 0.0, 0.0), mode="tiled", lists_in=None,
-           record_lists=0, pixels=None) -> Frame:
+           record_lists=0, pixels=None, variant=0) -> Frame:
     """Forward composite (Eq. 7).  `pixels`: optional flat pixel indices."""
-    P = _P(planes, sh_degree)
+    P = _P(planes, sh_degree, variant)
     c = _cam(cam)
     H, W = cam.height, cam.width
     bgv = np.ascontiguousarray(np.asarray(bg, np.float64))
@@ -297,10 +303,10 @@ def render(planes, sh_degree, cam, bg=(0.0, 0.0, 0.0), mode="tiled", lists_in=No
 
 
 def backward(planes, sh_degree, cam, d_rgb, bg=(0.0, 0.0, 0.0), mode="tiled", lists_in=None,
-             nu_grad_paper=False, want_g2d=False, pixels=None):
+             nu_grad_paper=False, want_g2d=False, pixels=None, variant=0):
     """Reverse mode of render(): (grad planes [P][n] fp64, g2d [n][10] or None).
     `pixels`: optional flat pixel indices; then d_rgb is [3][len(pixels)]."""
-    P = _P(planes, sh_degree)
+    P = _P(planes, sh_degree, variant)
     c = _cam(cam)
     n = P.arr.shape[1]
     bgv = np.ascontiguousarray(np.asarray(bg, np.float64))
@@ -342,11 +348,11 @@ def ssim(a, b):
     return 1.0 - image_loss(a, b, 1.0)[0]
 
 
-def regularizers(planes, sh_degree):
+def regularizers(planes, sh_degree, variant=0):
     """(sum_i |o_i|, sum_i sum_j sqrt(lambda_ij)) of Eq. 8."""
     pl = np.ascontiguousarray(np.asarray(planes, np.float64))
     out = np.zeros(2)
-    lib().orc_regularizers(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(out))
+    lib().orc_regularizers(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(out), int(variant))
     return float(out[0]), float(out[1])
 
 
@@ -366,7 +372,8 @@ def reloc_scale(o_old, nu_old, nu_new, N):
     return lib().orc_reloc_scale(float(o_old), float(nu_old), float(nu_new), int(N))
 
 
-def relocate(planes, sh_degree, m, v, r, threshold=0.005, cap_frac=0.05, n_max=32, seed=0, step=1):
+def relocate(planes, sh_degree, m, v, r, threshold=0.005, cap_frac=0.05, n_max=32, seed=0, step=1,
+             variant=0):
     """One recycling pass (orc_relocate) on fp64 copies; returns
     (planes, m, v, r, target_of, moved)."""
     pl = np.ascontiguousarray(np.asarray(planes, np.float64)).copy()
@@ -376,7 +383,7 @@ def relocate(planes, sh_degree, m, v, r, threshold=0.005, cap_frac=0.05, n_max=3
     tg = np.zeros(pl.shape[1], np.int32)
     moved = lib().orc_relocate(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(mm), _ptr(vv), _ptr(rr),
                                float(threshold), float(cap_frac), int(n_max), int(seed), int(step),
-                               _ptr(tg))
+                               _ptr(tg), int(variant))
     return pl, mm, vv, rr, tg, int(moved)
 
 
@@ -390,7 +397,8 @@ def sghmc_step(planes, sh_degree, grad, m, v, r, hp):
     h = _HP(hp.lr, hp.friction, hp.noise, hp.gate_k, hp.gate_t, int(hp.burn_in), int(hp.g_adam),
             hp.lr_scale, hp.lr_rot, hp.lr_nu, hp.lr_opacity, hp.lr_sh, hp.beta1, hp.beta2,
             hp.adam_eps, hp.grad_scale, int(hp.step), int(hp.seed),
-            getattr(hp, "eps_o", 0.0), getattr(hp, "eps_sigma", 0.0))
+            getattr(hp, "eps_o", 0.0), getattr(hp, "eps_sigma", 0.0), int(getattr(hp, "mu_mode", 0)),
+            int(getattr(hp, "variant", 0)))
     lib().orc_sghmc_step(pl.shape[1], int(sh_degree), _ptr(pl), _ptr(g), _ptr(mm), _ptr(vv),
                          _ptr(rr), C.byref(h))
     return pl, mm, vv, rr

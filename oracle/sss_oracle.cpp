@@ -41,7 +41,7 @@ typedef struct {
 typedef struct {
   int64_t n;
   int32_t sh_degree;
-  int32_t pad_;
+  int32_t variant;  // NEXT-3 ablation variants (bit flags, see kVar*); 0 = SSS
   const double* planes;  // [P][n], P = 12 + 3K; mean 0..2, log_scale 3..5,
                          // rot 6..9 (w,x,y,z), raw_nu 10, raw_opacity 11,
                          // sh 12 + 3k + c
@@ -67,6 +67,8 @@ typedef struct {
   int64_t step;
   uint64_t seed;
   double eps_o, eps_sigma;  // regularizer weights of Eq. 8
+  int32_t mu_mode;   // NEXT-3: 0 SGHMC (Eq. 10), 1 SGLD (F disabled), 2 Adam on mu (setting 1)
+  int32_t variant;   // parameter-set variant (opacity map of the gate / regularizer)
 } orc_sghmc_hp;
 
 }  // extern "C"
@@ -79,6 +81,14 @@ constexpr double kAlphaClamp = 0.99;  // R10
 constexpr double kWStop = 1e-4;       // R11
 
 inline int sh_K(int deg) { return (deg + 1) * (deg + 1); }
+
+// NEXT-3: the paper's ablation variants (R32), as flags
+// of the parameter set: positive opacity o = sigmoid(raw) (settings 1-2,
+// "positive t-dis"), the Gaussian kernel of 3DGS ("SGHMC with Gaussian
+// distributions"), and the +0.3 low-pass on the projected covariance
+// (setting 1).
+constexpr int kVarPositive = 1, kVarGaussian = 2, kVarLowpass = 4;
+constexpr double kLowpass = 0.3;
 inline int n_planes(int deg) { return 12 + 3 * sh_K(deg); }
 
 // ---------------------------------------------------------------- SH basis
@@ -172,8 +182,15 @@ double dnu_draw(double raw) {
   if (nu_of(raw) >= kNuMax) return 0.0;
   return 1.0 / (1.0 + std::exp(-raw));
 }
-// R2: o = tanh(raw)  ("we constrain the opacity by a tanh function")
-double opacity_of(double raw) { return std::tanh(raw); }
+// R2: o = tanh(raw)  ("we constrain the opacity by a tanh function");
+// positive variant (R32): o = sigmoid(raw), the 3DGS opacity.
+double opacity_of(double raw, int variant = 0) {
+  if (variant & kVarPositive) return 1.0 / (1.0 + std::exp(-raw));
+  return std::tanh(raw);
+}
+double dopacity_draw(double o, int variant) {
+  return (variant & kVarPositive) ? o * (1.0 - o) : 1.0 - o * o;
+}
 
 // Rotation from a (w,x,y,z) unit quaternion ("Sigma = R S S^T R^T").
 void quat_to_R(const double q[4], double R[9]) {
@@ -210,6 +227,7 @@ void load_comp(const orc_params* P, int64_t i, Comp& c) {
 // view.  Evaluation order of every quantity that feeds a discrete decision
 // follows DESIGN.md §2 "canonical order" (left-to-right sums, no fusion).
 struct Proj {
+  int variant;
   // Eq. 3 / R1-R3
   double nu, o, qn, qh[4], Rq[9], S[3], M[9], Sig[9];
   // Eq. 4
@@ -224,9 +242,10 @@ struct Proj {
   int cull;
 };
 
-void project(const Comp& c, int deg, const orc_cam& cam, Proj& r) {
+void project(const Comp& c, int deg, const orc_cam& cam, Proj& r, int variant = 0) {
+  r.variant = variant;
   r.nu = nu_of(c.raw_nu);
-  r.o = opacity_of(c.raw_o);
+  r.o = opacity_of(c.raw_o, variant);
   // q normalisation
   r.qn = std::sqrt(((c.q[0] * c.q[0] + c.q[1] * c.q[1]) + c.q[2] * c.q[2]) + c.q[3] * c.q[3]);
   for (int k = 0; k < 4; ++k) r.qh[k] = c.q[k] / r.qn;
@@ -291,6 +310,10 @@ void project(const Comp& c, int deg, const orc_cam& cam, Proj& r) {
   r.cov[0] = (K2[0] * r.J[0] + K2[1] * r.J[1]) + K2[2] * r.J[2];
   r.cov[1] = (K2[0] * r.J[3] + K2[1] * r.J[4]) + K2[2] * r.J[5];
   r.cov[2] = (K2[3] * r.J[3] + K2[4] * r.J[4]) + K2[5] * r.J[5];
+  if (variant & kVarLowpass) {  // setting 1's "small value (0.3)"
+    r.cov[0] = r.cov[0] + kLowpass;
+    r.cov[2] = r.cov[2] + kLowpass;
+  }
   r.det = r.cov[0] * r.cov[2] - r.cov[1] * r.cov[1];
   r.conic[0] = r.cov[2] / r.det;
   r.conic[1] = -r.cov[1] / r.det;
@@ -299,6 +322,7 @@ void project(const Comp& c, int deg, const orc_cam& cam, Proj& r) {
   r.mean2d[1] = (cam.fy * py) / pz + cam.cy;
   // L9 cutoff: pair included iff |o| T >= 1/255  <=>  h <= hmax  (R9)
   r.hmax = r.nu * std::expm1((2.0 / (r.nu + 2.0)) * std::log(255.0 * std::fabs(r.o)));
+  if (variant & kVarGaussian) r.hmax = 2.0 * std::log(255.0 * std::fabs(r.o));  // |o| e^{-h/2} = 1/255
   r.mx_f = (float)r.mean2d[0];
   r.my_f = (float)r.mean2d[1];
   r.A_f = (float)r.conic[0];
@@ -351,6 +375,18 @@ inline double dT_dnu(double h, double nu, bool paper) {
   return T * (-0.5 * std::log(g) + (nu + 2.0) * h / (2.0 * nu * nu * g));
 }
 
+// The component's kernel at h: the 2D t of Eq. 4, or the Gaussian e^{-h/2}
+// of 3DGS (Eq. 1) for the Gaussian variant (dT/dnu = 0).
+inline double kernel_T(const Proj& r, double h) {
+  return (r.variant & kVarGaussian) ? std::exp(-0.5 * h) : t2d(h, r.nu);
+}
+inline double kernel_dT_dh(const Proj& r, double h) {
+  return (r.variant & kVarGaussian) ? -0.5 * std::exp(-0.5 * h) : dT_dh(h, r.nu);
+}
+inline double kernel_dT_dnu(const Proj& r, double h, bool paper) {
+  return (r.variant & kVarGaussian) ? 0.0 : dT_dnu(h, r.nu, paper);
+}
+
 struct View {
   int W, H, tw, th;
   std::vector<Proj> pr;
@@ -367,7 +403,7 @@ void build_view(const orc_params* P, const orc_cam& cam, View& v, bool bin) {
   for (int64_t i = 0; i < n; ++i) {
     Comp c;
     load_comp(P, i, c);
-    project(c, P->sh_degree, cam, v.pr[i]);
+    project(c, P->sh_degree, cam, v.pr[i], P->variant);
   }
   v.order.clear();
   for (int64_t i = 0; i < n; ++i)
@@ -414,7 +450,7 @@ void pixel_list(const View& v, int x, int y, int mode, const int32_t* frozen, in
     e.dx = pxd - r.mean2d[0];
     e.dy = pyd - r.mean2d[1];
     e.h = r.conic[0] * e.dx * e.dx + 2.0 * r.conic[1] * e.dx * e.dy + r.conic[2] * e.dy * e.dy;
-    e.T = t2d(e.h, r.nu);
+    e.T = kernel_T(r, e.h);
     const double a = r.o * e.T;
     e.clamped = (a > kAlphaClamp) || (a < -kAlphaClamp);
     e.alpha = std::min(std::max(a, -kAlphaClamp), kAlphaClamp);
@@ -446,6 +482,7 @@ int orc_num_planes(int sh_degree) { return n_planes(sh_degree); }
 // ---- primitives exposed for the pins ------------------------------------
 double orc_nu_of(double raw) { return nu_of(raw); }
 double orc_opacity_of(double raw) { return opacity_of(raw); }
+double orc_opacity_of_v(double raw, int32_t variant) { return opacity_of(raw, variant); }
 double orc_t2d(double h, double nu) { return t2d(h, nu); }
 double orc_t3d(double h, double nu) { return std::pow(1.0 + h / nu, -(nu + 3.0) / 2.0); }  // Eq. 3
 double orc_dT_dh(double h, double nu) { return dT_dh(h, nu); }
@@ -477,7 +514,7 @@ int orc_project(const orc_params* P, const orc_cam* cam, orc_proj_out* out) {
     Comp c;
     load_comp(P, i, c);
     Proj r;
-    project(c, P->sh_degree, *cam, r);
+    project(c, P->sh_degree, *cam, r, P->variant);
     out->mx[i] = r.mx_f; out->my[i] = r.my_f; out->A[i] = r.A_f; out->B2[i] = r.B2_f;
     out->C[i] = r.C_f; out->hmax[i] = r.hmax_f; out->depth[i] = r.depth_f;
     for (int k = 0; k < 4; ++k) out->rect[i * 4 + k] = r.rect[k];
@@ -627,8 +664,8 @@ int orc_backward(const orc_params* P, const orc_cam* cam, const double* bg, cons
         if (e.clamped) da = 0.0;  // R10: zero gradient through an active clamp
         const double d_o = da * e.T;      // a = o T
         const double d_T = da * r.o;
-        const double d_h = d_T * dT_dh(e.h, r.nu);
-        const double d_nu = d_T * dT_dnu(e.h, r.nu, nu_grad_paper != 0);
+        const double d_h = d_T * kernel_dT_dh(r, e.h);
+        const double d_nu = d_T * kernel_dT_dnu(r, e.h, nu_grad_paper != 0);
         // h = A dx^2 + 2 B dx dy + C dy^2, d = u - mean2d
         const double A = r.conic[0], B = r.conic[1], Cc = r.conic[2];
         const double dmx = d_h * -2.0 * (A * e.dx + B * e.dy);
@@ -657,7 +694,7 @@ int orc_backward(const orc_params* P, const orc_cam* cam, const double* bg, cons
     Comp c;
     load_comp(P, i, c);
     Proj r;
-    project(c, P->sh_degree, *cam, r);
+    project(c, P->sh_degree, *cam, r, P->variant);
     const double px = r.p[0], py = r.p[1], pz = r.p[2];
     // conic gradient as a symmetric matrix, then Sigma2D: G_S = -Q G_Q Q
     const double Q[4] = {r.conic[0], r.conic[1], r.conic[1], r.conic[2]};
@@ -748,7 +785,7 @@ int orc_backward(const orc_params* P, const orc_cam* cam, const double* bg, cons
     const double dd = gdir[0] * r.dir[0] + gdir[1] * r.dir[1] + gdir[2] * r.dir[2];
     for (int a = 0; a < 3; ++a) dmu[a] += (gdir[a] - r.dir[a] * dd) / r.dist;
     // reparameterisations (R1, R2)
-    const double draw_o = G[8] * (1.0 - r.o * r.o);
+    const double draw_o = G[8] * dopacity_draw(r.o, P->variant);
     const double draw_nu = G[9] * dnu_draw(c.raw_nu);
     double* gp = grad_planes;
     for (int a = 0; a < 3; ++a) gp[(0 + a) * n + i] += dmu[a];
@@ -816,7 +853,7 @@ int orc_sghmc_step(int64_t n, int32_t sh_degree, double* planes, const double* g
     Comp c;
     orc_params pp{n, sh_degree, 0, planes};
     load_comp(&pp, i, c);
-    const double o = opacity_of(c.raw_o);
+    const double o = opacity_of(c.raw_o, hp->variant);
     const double gate = 1.0 / (1.0 + std::exp(hp->gate_k * (std::fabs(o) - hp->gate_t)));
     double Sig[9];
     if (hp->burn_in) {
@@ -842,9 +879,9 @@ int orc_sghmc_step(int64_t n, int32_t sh_degree, double* planes, const double* g
     //   d/ds_j = eps_Sigma exp(s_j),  d/draw_o = eps_o sign(o) (1 - o^2).
     double reg[64] = {0.0};
     for (int j = 0; j < 3; ++j) reg[3 + j] = hp->eps_sigma * std::exp(c.s[j]);
-    reg[11] = hp->eps_o * (o > 0.0 ? 1.0 : (o < 0.0 ? -1.0 : 0.0)) * (1.0 - o * o);
+    reg[11] = hp->eps_o * (o > 0.0 ? 1.0 : (o < 0.0 ? -1.0 : 0.0)) * dopacity_draw(o, hp->variant);
     for (int p = 0; p < P; ++p) {
-      if (p < 3 && !hp->g_adam) { adir[p] = 0.0; continue; }
+      if (p < 3 && !hp->g_adam && hp->mu_mode != 2) { adir[p] = 0.0; continue; }
       const double g = grad[(int64_t)p * n + i] * hp->grad_scale + reg[p];
       double& mm = m[(int64_t)p * n + i];
       double& vv = v[(int64_t)p * n + i];
@@ -860,9 +897,13 @@ int orc_sghmc_step(int64_t n, int32_t sh_degree, double* planes, const double* g
       for (int a = 0; a < 3; ++a) noise[a] = eta * xi[a];
     }
     for (int a = 0; a < 3; ++a) {
+      if (hp->mu_mode == 2) {  // setting 1: Adam on the means, no sampler state
+        planes[(int64_t)a * n + i] = c.mu[a] - eps * adir[a];
+        continue;
+      }
       const double g = hp->g_adam ? adir[a] : grad[(int64_t)a * n + i] * hp->grad_scale;
       const double ra = r[(int64_t)a * n + i];
-      const double F = hp->burn_in ? 0.0 : eps * (1.0 - eps * C) * ra;
+      const double F = (hp->burn_in || hp->mu_mode == 1) ? 0.0 : eps * (1.0 - eps * C) * ra;
       planes[(int64_t)a * n + i] = c.mu[a] - eps * eps * g + gate * (F + noise[a]);
       r[(int64_t)a * n + i] = (1.0 - eps * C) * ra - eps * g + (eta / eps) * xi[a];
     }
@@ -946,13 +987,13 @@ double orc_image_loss(const double* rgb, const double* target, int32_t H, int32_
 
 // Eq. 8 regularizer values: out[0] = sum_i |o_i|, out[1] = sum_i sum_j sqrt(lambda_ij)
 // with lambda the eigenvalues of Sigma_i (= exp(2 s_ij), R27).
-void orc_regularizers(int64_t n, int32_t sh_degree, const double* planes, double* out) {
-  orc_params pp{n, sh_degree, 0, planes};
+void orc_regularizers(int64_t n, int32_t sh_degree, const double* planes, double* out, int32_t variant) {
+  orc_params pp{n, sh_degree, variant, planes};
   double so = 0.0, ss = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     Comp c;
     load_comp(&pp, i, c);
-    so += std::fabs(opacity_of(c.raw_o));
+    so += std::fabs(opacity_of(c.raw_o, variant));
     for (int j = 0; j < 3; ++j) ss += std::exp(c.s[j]);
   }
   out[0] = so;
@@ -1015,7 +1056,7 @@ double orc_reloc_scale(double o_old, double nu_old, double nu_new, int32_t N) {
 // Returns the number of relocated components.
 int64_t orc_relocate(int64_t n, int32_t sh_degree, double* planes, double* m, double* v, double* r,
                      double threshold, double cap_frac, int32_t n_max, uint64_t seed, int64_t step,
-                     int32_t* target_of) {
+                     int32_t* target_of, int32_t variant) {
   const int P = n_planes(sh_degree);
   std::vector<int64_t> dead;
   std::vector<uint64_t> cum(n);
@@ -1023,7 +1064,7 @@ int64_t orc_relocate(int64_t n, int32_t sh_degree, double* planes, double* m, do
   const float thr = (float)threshold;
   for (int64_t i = 0; i < n; ++i) {
     target_of[i] = -1;
-    const float o32 = (float)std::tanh(planes[11 * n + i]);
+    const float o32 = (float)opacity_of(planes[11 * n + i], variant);
     const float a = std::fabs(o32);
     if (a < thr) {
       dead.push_back(i);
@@ -1060,11 +1101,11 @@ int64_t orc_relocate(int64_t n, int32_t sh_degree, double* planes, double* m, do
   for (int64_t t = 0; t < n; ++t) {
     if (members[t].empty()) continue;
     const int N = 1 + (int)members[t].size();
-    const double o_old = opacity_of(planes[11 * n + t]);
+    const double o_old = opacity_of(planes[11 * n + t], variant);
     const double nu = nu_of(planes[10 * n + t]);
     const double o_new = orc_reloc_opacity(o_old, N);
     const double scale = orc_reloc_scale(o_old, nu, nu, N);
-    planes[11 * n + t] = std::atanh(o_new);
+    planes[11 * n + t] = (variant & kVarPositive) ? std::log(o_new / (1.0 - o_new)) : std::atanh(o_new);
     for (int j = 0; j < 3; ++j) planes[(3 + j) * n + t] += 0.5 * std::log(scale);
     std::vector<int64_t> all = members[t];
     all.push_back(t);

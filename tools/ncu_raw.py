@@ -15,8 +15,9 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 out = subprocess.run(['ncu', '-i', sys.argv[1], '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
+units = rows[1]
 for r in rows[2:]:
     print('----', r[h.index('Kernel Name')][:90])
     for w in WANT:
         if w in h:
-            print(f'  {w:60s} {r[h.index(w)]}')
+            print(f'  {w:60s} {r[h.index(w)]} {units[h.index(w)]}')
