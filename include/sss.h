@@ -69,11 +69,17 @@ typedef struct {
  * colour c, opacity o, degree parameter nu"), device SoA planes, see above.
  * nu = min(1 + softplus(raw_nu), 1e4) (R1); o = tanh(raw_opacity)
  * (R2); S = diag(exp(log_scale)) (R3); R = R(q / |q|).
- * The same struct describes gradients and Adam moments (same layout). */
+ * The same struct describes gradients and Adam moments (same layout).
+ * variant: 0 for SSS, or the paper's ablation variants (PAPER.md:1109-1111,
+ * R32) as SSS_VARIANT_* flags; every entry point taking the parameter set
+ * honours them (the projected records carry the kernel). */
+#define SSS_VARIANT_POSITIVE 1 /* o = sigmoid(raw_opacity): "positive t-dis" (settings 1-2) */
+#define SSS_VARIANT_GAUSSIAN 2 /* 3DGS Gaussian kernel exp(-h/2) (nu unused; inv_nu = 0 in the record) */
+#define SSS_VARIANT_LOWPASS 4  /* +0.3 on the diagonal of Sigma2D (setting 1) */
 typedef struct {
   int64_t n;
   int32_t sh_degree;
-  int32_t reserved;
+  int32_t variant;
   float* mean;
   float* log_scale;
   float* rot;
@@ -151,6 +157,10 @@ typedef struct {
    * eps_sigma sum_ij sqrt(lambda_ij) adds eps_sigma exp(s_j) to d log_scale_j
    * (after grad_scale).  0, 0 = the BASELINE L1 objective. */
   float eps_o, eps_sigma;
+  /* NEXT-3 mean update: 0 gated SGHMC (Eq. 10), 1 SGLD (F disabled,
+   * PAPER.md:161), 2 Adam on the means with lr (setting 1's optimiser). */
+  int32_t mu_mode;
+  int32_t reserved;
 } sss_sghmc_hparams;
 
 /* flags for sss_render_bwd */

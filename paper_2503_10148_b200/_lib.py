@@ -17,6 +17,7 @@ SSS_TILE = 16
 SSS_MAX_BINS = 5632
 SSS_REC_FLOATS = 12
 SSS_G2D_FLOATS = 12
+SSS_VARIANT_POSITIVE, SSS_VARIANT_GAUSSIAN, SSS_VARIANT_LOWPASS = 1, 2, 4
 SSS_BWD_NU_GRAD_PAPER = 1
 SSS_BWD_RASTER_ONLY = 2
 SSS_BWD_PROJECTION_ONLY = 4
@@ -34,7 +35,7 @@ class sss_camera(C.Structure):
 
 
 class sss_params(C.Structure):
-    _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("variant", C.c_int32),
                 ("mean", C.c_void_p), ("log_scale", C.c_void_p), ("rot", C.c_void_p),
                 ("raw_nu", C.c_void_p), ("raw_opacity", C.c_void_p), ("sh", C.c_void_p)]
 
@@ -62,7 +63,8 @@ class sss_sghmc_hparams(C.Structure):
                 ("lr_nu", C.c_float), ("lr_opacity", C.c_float), ("lr_sh", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
                 ("grad_scale", C.c_float), ("step", C.c_int64), ("seed", C.c_uint64),
-                ("eps_o", C.c_float), ("eps_sigma", C.c_float)]
+                ("eps_o", C.c_float), ("eps_sigma", C.c_float), ("mu_mode", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class sss_relocate_params(C.Structure):

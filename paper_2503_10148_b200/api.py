@@ -34,11 +34,12 @@ class Params:
     Gradients and Adam moments use the same class (identical layout), so the
     whole gradient is one contiguous buffer for the NCCL all-reduce."""
 
-    def __init__(self, planes: torch.Tensor, sh_degree: int):
+    def __init__(self, planes: torch.Tensor, sh_degree: int, variant: int = 0):
         assert planes.dtype == torch.float32 and planes.is_contiguous() and planes.dim() == 2
         assert planes.shape[0] == n_planes(sh_degree), (planes.shape, sh_degree)
         self.planes = planes
         self.sh_degree = int(sh_degree)
+        self.variant = int(variant)  # SSS_VARIANT_* flags (NEXT-3 ablations); 0 = SSS
 
     @property
     def n(self) -> int:
@@ -46,13 +47,14 @@ class Params:
 
     @classmethod
     def zeros_like(cls, other: "Params") -> "Params":
-        return cls(torch.zeros_like(other.planes), other.sh_degree)
+        return cls(torch.zeros_like(other.planes), other.sh_degree, other.variant)
 
     def c(self) -> L.sss_params:
         b = self.planes.data_ptr()
         n = self.n
         off = lambda p: C.c_void_p(b + 4 * p * n)  # noqa: E731
-        return L.sss_params(n, self.sh_degree, 0, off(0), off(3), off(6), off(10), off(11), off(12))
+        return L.sss_params(n, self.sh_degree, self.variant, off(0), off(3), off(6), off(10), off(11),
+                            off(12))
 
 
 def camera_c(cam) -> L.sss_camera:
@@ -163,7 +165,8 @@ def hparams_c(hp) -> L.sss_sghmc_hparams:
                                int(hp.burn_in), int(hp.g_adam), hp.lr_scale, hp.lr_rot, hp.lr_nu,
                                hp.lr_opacity, hp.lr_sh, hp.beta1, hp.beta2, hp.adam_eps,
                                hp.grad_scale, int(hp.step), int(hp.seed),
-                               float(getattr(hp, "eps_o", 0.0)), float(getattr(hp, "eps_sigma", 0.0)))
+                               float(getattr(hp, "eps_o", 0.0)), float(getattr(hp, "eps_sigma", 0.0)),
+                               int(getattr(hp, "mu_mode", 0)), 0)
 
 
 # ------------------------------------------------------------- entry points

@@ -36,6 +36,7 @@ sss_status validate_params(const sss_params* p, const char* what) {
     set_error("%s: sh_degree %d outside [0,3]", what, p->sh_degree);
     return SSS_ERR_ARG;
   }
+  if (p->variant < 0 || p->variant > 7) { set_error("%s: variant %d outside [0,7]", what, p->variant); return SSS_ERR_ARG; }
   if (p->n > 0 && (!p->mean || !p->log_scale || !p->rot || !p->raw_nu || !p->raw_opacity || !p->sh)) {
     set_error("%s: null plane pointer", what);
     return SSS_ERR_ARG;

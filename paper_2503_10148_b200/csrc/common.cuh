@@ -13,6 +13,8 @@ constexpr int kMaxViewsPerLaunch = 128;
 constexpr float kAlphaMax = 0.99f;   // R10
 constexpr float kWStop = 1e-4f;      // R11
 constexpr double kNuMax = 1e4;
+constexpr float kLowpass = 0.3f;     // setting 1's low-pass
+constexpr float kGaussExp2 = -0.72134752044448170f;  // -log2(e)/2: exp(-h/2) = 2^(kGaussExp2 h)
 
 struct DevCamera {  // a camera as the kernels see it
   float R[9];

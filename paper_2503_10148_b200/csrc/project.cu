@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(128) project_kernel(sss_params P, const __grid
   {
     const double sp = raw_nu > 30.0 ? raw_nu : log1p(exp(raw_nu));
     vi.nu = fmin(1.0 + sp, kNuMax);
-    vi.o = tanh(raw_o);
+    vi.o = (P.variant & SSS_VARIANT_POSITIVE) ? 1.0 / (1.0 + exp(-raw_o)) : tanh(raw_o);
     const double qn = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
     const double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
     double R[9];
@@ -116,12 +116,16 @@ __global__ void __launch_bounds__(128) project_kernel(sss_params P, const __grid
       for (int b = 0; b < 3; ++b)
         vi.Sig[a * 3 + b] = (M[a * 3 + 0] * M[b * 3 + 0] + M[a * 3 + 1] * M[b * 3 + 1]) + M[a * 3 + 2] * M[b * 3 + 2];
     vi.hmax = vi.nu * expm1((2.0 / (vi.nu + 2.0)) * log(255.0 * fabs(vi.o)));
+    if (P.variant & SSS_VARIANT_GAUSSIAN) vi.hmax = 2.0 * log(255.0 * fabs(vi.o));  // |o| e^{-h/2} = 1/255
   }
   const bool opaque_enough = 255.0 * fabs(vi.o) > 1.0;  // R25
   const float hmax_f = (float)vi.hmax;
   const float o_f = (float)vi.o;
-  const float inv_nu_f = (float)(1.0 / vi.nu);
-  const float e_f = (float)(-(vi.nu + 2.0) / 2.0);
+  // Gaussian variant: inv_nu = 0 marks the kernel exp(-h/2) in the record
+  const bool gauss = P.variant & SSS_VARIANT_GAUSSIAN;
+  const float inv_nu_f = gauss ? 0.f : (float)(1.0 / vi.nu);
+  const float e_f = gauss ? -0.5f : (float)(-(vi.nu + 2.0) / 2.0);
+  const bool lowpass = P.variant & SSS_VARIANT_LOWPASS;
 
   for (int vv = 0; vv < nv; ++vv) {
     const DevCamera& cam = cp.cam[vv];
@@ -153,9 +157,13 @@ __global__ void __launch_bounds__(128) project_kernel(sss_params P, const __grid
       for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 3; ++b)
           K2[a * 3 + b] = (J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b]) + J[a * 3 + 2] * Sc[2 * 3 + b];
-      const double cxx = (K2[0] * J[0] + K2[1] * J[1]) + K2[2] * J[2];
+      double cxx = (K2[0] * J[0] + K2[1] * J[1]) + K2[2] * J[2];
       const double cxy = (K2[0] * J[3] + K2[1] * J[4]) + K2[2] * J[5];
-      const double cyy = (K2[3] * J[3] + K2[4] * J[4]) + K2[5] * J[5];
+      double cyy = (K2[3] * J[3] + K2[4] * J[4]) + K2[5] * J[5];
+      if (lowpass) {
+        cxx = cxx + 0.3;
+        cyy = cyy + 0.3;
+      }
       const double det = cxx * cyy - cxy * cxy;
       const double A = cyy / det, B = -cxy / det, C = cxx / det;
       const double mx = (fx * px) / pz + (double)cam.cx;

@@ -70,11 +70,15 @@ RelocWs reloc_ws(int64_t n) {
 }
 
 // weights and dead flags
-__global__ void reloc_weights_kernel(const float* __restrict__ raw_o, int64_t n, float thr,
+__device__ __forceinline__ double opacity_d(double raw, bool positive) {
+  return positive ? 1.0 / (1.0 + exp(-raw)) : tanh(raw);
+}
+
+__global__ void reloc_weights_kernel(const float* __restrict__ raw_o, int64_t n, float thr, bool positive,
                                      uint64_t* __restrict__ w, uint64_t* __restrict__ dead) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float a = fabsf((float)tanh((double)raw_o[i]));
+  const float a = fabsf((float)opacity_d((double)raw_o[i], positive));
   const bool d = a < thr;
   dead[i] = d ? 1ull : 0ull;
   w[i] = d ? 0ull : (uint64_t)floor((double)a * 4294967296.0);
@@ -210,7 +214,8 @@ __global__ void reloc_apply_kernel(const uint32_t* __restrict__ tkey, const int3
   const int64_t n = P.n;
   const int Pn = 12 + 3 * (P.sh_degree + 1) * (P.sh_degree + 1);
   // Eq. 12 in fp64 from the target's fp32 state
-  const double o_old = tanh((double)P.raw_opacity[t]);
+  const bool positive = P.variant & SSS_VARIANT_POSITIVE;
+  const double o_old = opacity_d((double)P.raw_opacity[t], positive);
   const double raw_nu = (double)P.raw_nu[t];
   const double sp = raw_nu > 30.0 ? raw_nu : log1p(exp(raw_nu));
   const double nu = fmin(1.0 + sp, 1e4);
@@ -226,7 +231,7 @@ __global__ void reloc_apply_kernel(const uint32_t* __restrict__ tkey, const int3
   }
   const double b = beta_lg(0.5, (nu + 2.0) / 2.0);
   const double scale = o_old * o_old * (b / K) * (b / K);
-  const float raw_o_new = (float)atanh(o_new);
+  const float raw_o_new = (float)(positive ? log(o_new / (1.0 - o_new)) : atanh(o_new));
   const double dls = 0.5 * log(scale);
   // the target's new state, then copied to every member
   P.raw_opacity[t] = raw_o_new;
@@ -309,7 +314,8 @@ extern "C" sss_status sss_relocate(sss_params* p, sss_params* adam_m, sss_params
   int64_t* n_sel = (int64_t*)(w + L.scal);
   uint64_t* total = (uint64_t*)(w + L.scal + 8);
   const int eb = div_up(n, 256);
-  reloc_weights_kernel<<<eb, 256, 0, s>>>(p->raw_opacity, n, rp->threshold, cw, cd);
+  reloc_weights_kernel<<<eb, 256, 0, s>>>(p->raw_opacity, n, rp->threshold, (p->variant & SSS_VARIANT_POSITIVE) != 0,
+                                          cw, cd);
   for (int q = 0; q < 2; ++q) {
     uint64_t* data = q ? cd : cw;
     uint64_t* bs = q ? bd : bw;

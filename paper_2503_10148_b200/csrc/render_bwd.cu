@@ -92,20 +92,26 @@ __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v
 // T / (1 + h/nu) comes from one ex2 of (e - 1) log2(1 + h/nu) (T = that
 // times 1 + h/nu), so a pair costs lg2, ex2 and rcp(1 - a) on the MUFU pipe.
 // GENERAL handles the rare warp-uniform cases (as the forward): nu > 32
-// (accurate log1p) and |o| > 0.989, where the +-0.99 clamp (R10) can bind
-// and then cuts the gradient.
+// (accurate log1p), the Gaussian kernel of the ablation variant (inv_nu = 0:
+// T = exp(-h/2), dT/dh = -T/2, dT/dnu = 0) and |o| > 0.989, where the +-0.99
+// clamp (R10) can bind and then cuts the gradient.
 template <bool NU_PAPER, bool GENERAL>
 __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4 b, float4 c, float einu,
                                            EntrySums2& e, bool inc0, bool inc1) {
   const float2 t = mul2(h, bc2(b.w));
   const float2 opt = add2(t, bc2(1.f));
-  float2 lg;
-  if (GENERAL && b.w < (1.f / 32.f)) {
-    lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+  float2 lg, exm;
+  if (GENERAL && b.w == 0.f) {  // Gaussian variant: T = exp(-h/2), t = 0, lg = 0
+    lg = bc2(0.f);
+    exm = mul2(h, bc2(kGaussExp2));
   } else {
-    lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+    if (GENERAL && b.w < (1.f / 32.f)) {
+      lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+    } else {
+      lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+    }
+    exm = mul2(lg, bc2(c.x - 1.f));
   }
-  const float2 exm = mul2(lg, bc2(c.x - 1.f));
   const float2 Topt = make_float2(ex2_approx(exm.x), ex2_approx(exm.y));  // T / (1 + h/nu)
   const float2 T = mul2(Topt, opt);
   const float2 araw = mul2(T, bc2(b.z));
@@ -310,7 +316,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
 #endif
       if (!__any_sync(0xffffffffu, any)) continue;
       const float4 c = sc[j];  // {e, r, g, b}
-      const float einu = c.x * b.w;  // e / nu = -(nu+2)/(2 nu)
+      // e / nu = -(nu+2)/(2 nu): dT/dh = einu T/(1 + h/nu); -1/2 for the Gaussian variant
+      const float einu = b.w == 0.f ? -0.5f : c.x * b.w;
       const float2 z2 = bc2(0.f);
       EntrySums2 e2{z2, z2, z2, z2, z2, z2, z2, z2};
       if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
@@ -512,9 +519,13 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(sss_params P, const __
     float K2[6];
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 3; ++b) K2[a * 3 + b] = J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b] + J[a * 3 + 2] * Sc[2 * 3 + b];
-    const float cxx = K2[0] * J[0] + K2[2] * J[2];
+    float cxx = K2[0] * J[0] + K2[2] * J[2];
     const float cxy = K2[1] * J[4] + K2[2] * J[5];
-    const float cyy = K2[4] * J[4] + K2[5] * J[5];
+    float cyy = K2[4] * J[4] + K2[5] * J[5];
+    if (P.variant & SSS_VARIANT_LOWPASS) {  // conic of Sigma2D + 0.3 I; d(Sigma2D + 0.3 I) = d Sigma2D
+      cxx += kLowpass;
+      cyy += kLowpass;
+    }
     const float idet = 1.f / (cxx * cyy - cxy * cxy);
     const float QA = cyy * idet, QB = -cxy * idet, QC = cxx * idet;
     // G_S = -Q G_Q Q with G_Q = [[dA, dB/2], [dB/2, dC]]
@@ -603,14 +614,15 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(sss_params P, const __
   const float dotq = gq[0] * qw + gq[1] * qx + gq[2] * qy + gq[3] * qz;
   const float qh[4] = {qw, qx, qy, qz};
   // reparameterisations
-  const float o = tanhf(raw_o);
+  const bool positive = P.variant & SSS_VARIANT_POSITIVE;
+  const float o = positive ? 1.f / (1.f + expf(-raw_o)) : tanhf(raw_o);
   const float sp = raw_nu > 30.f ? raw_nu : log1pf(expf(raw_nu));
   const float dnu = (1.f + sp >= (float)kNuMax) ? 0.f : 1.f / (1.f + expf(-raw_nu));
   for (int a = 0; a < 3; ++a) Gd.mean[a * n + i] += gmu[a];
   for (int a = 0; a < 3; ++a) Gd.log_scale[a * n + i] += gls[a];
   for (int a = 0; a < 4; ++a) Gd.rot[a * n + i] += (gq[a] - qh[a] * dotq) / qn;
   Gd.raw_nu[i] += g_nu * dnu;
-  Gd.raw_opacity[i] += g_o * (1.f - o * o);
+  Gd.raw_opacity[i] += g_o * (positive ? o * (1.f - o) : 1.f - o * o);
 #pragma unroll
   for (int k = 0; k < 3 * K; ++k) Gd.sh[k * n + i] += gsh[k];
 }

@@ -29,20 +29,26 @@ struct PixF2 {  // forward colour state of a horizontally adjacent pixel pair
 // One pair of Eq. 7 for both pixels of a pair, predicated per pixel on `inc`
 // (a = 0 leaves C and W bit-unchanged: C + c*0 = C, W - 0*W = W), so a warp
 // runs its pixels' chains branch-free.  GENERAL handles the two rare
-// warp-uniform cases: nu > 32 (accurate log1p, see log2_1p) and |o| > 0.989,
+// warp-uniform cases: nu > 32 (accurate log1p, see log2_1p), the Gaussian
+// kernel of the ablation variant (inv_nu = 0 in the record) and |o| > 0.989,
 // where the +-0.99 clamp (R10) can bind (T <= 1 for h >= 0, so |o| <= 0.989
 // leaves |o T| < 0.99 even for an h rounded slightly below 0).
 template <bool GENERAL>
 __device__ __forceinline__ void composite2(PixF2& p, float2 h, float4 b, float4 c, bool inc0, bool inc1) {
   const float2 t = mul2(h, bc2(b.w));
   float2 lg;
-  if (GENERAL && b.w < (1.f / 32.f)) {
-    lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+  float2 e;
+  if (GENERAL && b.w == 0.f) {  // Gaussian variant: T = exp(-h/2) = 2^(kGaussExp2 h)
+    e = mul2(h, bc2(kGaussExp2));
   } else {
-    const float2 opt = add2(t, bc2(1.f));
-    lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+    if (GENERAL && b.w < (1.f / 32.f)) {
+      lg = make_float2(log2_1p(t.x, true), log2_1p(t.y, true));
+    } else {
+      const float2 opt = add2(t, bc2(1.f));
+      lg = make_float2(lg2_approx(opt.x), lg2_approx(opt.y));
+    }
+    e = mul2(lg, bc2(c.x));
   }
-  const float2 e = mul2(lg, bc2(c.x));
   float2 araw = mul2(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(b.z));
   if (GENERAL) {
     araw.x = fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax);

@@ -8,6 +8,8 @@
 //   mu'   = mu - eps^2 g + gate (F + N),  F = eps (1 - eps C) r,  N = eta xi
 //   gate  = sigmoid(-k (|o| - t))
 //   burn-in: F = 0, N = eta Sigma xi (Sigma of the pre-update component)
+//   NEXT-3 mu_mode: 1 = SGLD (F = 0), 2 = Adam on the means;
+//   the opacity map follows the parameter variant (sigmoid for POSITIVE).
 //   Eq. 8 regularizers (R27): g(log_scale_j) += eps_Sigma exp(s_j),
 //         g(raw_o) += eps_o sign(o)(1 - o^2)  (sqrt(lambda_j(Sigma)) = exp(s_j))
 //   Adam: m' = b1 m + (1-b1) g, v' = b2 v + (1-b2) g^2,
@@ -31,6 +33,7 @@ struct HP {
   float lr_group[5];  // log_scale, rot, nu, opacity, sh
   float beta1, beta2, adam_eps, grad_scale;
   float eps_o, eps_sigma;  // Eq. 8 regularizer weights
+  int mu_mode;             // 0 SGHMC, 1 SGLD (F = 0), 2 Adam on the means
   float inv_b1t, inv_b2t;  // 1 / (1 - beta^t)
   uint32_t ctr2, ctr3;     // step (lo, hi)
   uint32_t key0, key1;     // seed (lo, hi)
@@ -57,7 +60,8 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   if (i >= n) return;
   const int K = (P.sh_degree + 1) * (P.sh_degree + 1);
   // gate and (burn-in) covariance from the pre-update state
-  const float o = tanhf(P.raw_opacity[i]);
+  const bool positive = P.variant & SSS_VARIANT_POSITIVE;
+  const float o = positive ? 1.f / (1.f + expf(-P.raw_opacity[i])) : tanhf(P.raw_opacity[i]);
   const float gate = 1.f / (1.f + expf(hp.gate_k * (fabsf(o) - hp.gate_t)));
   float Sig[9];
   if (hp.burn_in) {
@@ -98,9 +102,13 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   for (int a = 0; a < 3; ++a) {
     const int64_t idx = a * n + i;
     const float graw = Gr.mean[idx] * hp.grad_scale;
+    if (hp.mu_mode == 2) {  // setting 1: Adam on the means, no sampler state
+      P.mean[idx] -= eps * adam_dir(graw, Mo.mean, Vo.mean, idx, hp);
+      continue;
+    }
     const float g = hp.g_adam ? adam_dir(graw, Mo.mean, Vo.mean, idx, hp) : graw;
     const float ra = r[idx];
-    const float F = hp.burn_in ? 0.f : eps * (1.f - eps * Cf) * ra;
+    const float F = (hp.burn_in || hp.mu_mode == 1) ? 0.f : eps * (1.f - eps * Cf) * ra;
     P.mean[idx] = P.mean[idx] - eps * eps * g + gate * (F + noise[a]);
     r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
   }
@@ -112,7 +120,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   }
   for (int a = 0; a < 4; ++a) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
   adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
-  const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (1.f - o * o);
+  const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (positive ? o * (1.f - o) : 1.f - o * o);
   adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
   for (int k = 0; k < 3 * K; ++k) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
 }
@@ -145,6 +153,8 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
   hp.lr_group[3] = h->lr_opacity; hp.lr_group[4] = h->lr_sh;
   hp.beta1 = h->beta1; hp.beta2 = h->beta2; hp.adam_eps = h->adam_eps; hp.grad_scale = h->grad_scale;
   hp.eps_o = h->eps_o; hp.eps_sigma = h->eps_sigma;
+  hp.mu_mode = h->mu_mode;
+  if (hp.mu_mode < 0 || hp.mu_mode > 2) { set_error("sss_sghmc_step: mu_mode outside [0,2]"); return SSS_ERR_ARG; }
   hp.inv_b1t = (float)(1.0 / (1.0 - pow((double)h->beta1, (double)h->step)));
   hp.inv_b2t = (float)(1.0 / (1.0 - pow((double)h->beta2, (double)h->step)));
   hp.ctr2 = (uint32_t)h->step; hp.ctr3 = (uint32_t)((uint64_t)h->step >> 32);

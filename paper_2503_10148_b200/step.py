@@ -26,12 +26,12 @@ class TrainStep:
                  views_per_batch: int = 16, bg=(0.0, 0.0, 0.0), headroom: float = 1.25,
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
-                 eps_dssim: float = 0.0):
+                 eps_dssim: float = 0.0, variant: int = 0):
         dev = planes.device
-        self.params = A.Params(planes, sh_degree)
+        self.params = A.Params(planes, sh_degree, variant)
         self.grad = A.Params.zeros_like(self.params)
-        self.m = A.Params(adam_m if adam_m is not None else torch.zeros_like(planes), sh_degree)
-        self.v = A.Params(adam_v if adam_v is not None else torch.zeros_like(planes), sh_degree)
+        self.m = A.Params(adam_m if adam_m is not None else torch.zeros_like(planes), sh_degree, variant)
+        self.v = A.Params(adam_v if adam_v is not None else torch.zeros_like(planes), sh_degree, variant)
         n = self.params.n
         self.r = momentum if momentum is not None else torch.zeros((3, n), device=dev)
         self.hp = hp

@@ -104,6 +104,8 @@ class SGHMCParams:
     seed: int = 1234
     eps_o: float = 0.0  # Eq. 8 opacity regularizer weight (0: the BASELINE L1 objective)
     eps_sigma: float = 0.0  # Eq. 8 sqrt-eigenvalue regularizer weight
+    mu_mode: int = 0  # NEXT-3: 0 SGHMC, 1 SGLD (F disabled), 2 Adam on the means
+    variant: int = 0  # parameter-set variant (oracle: opacity map of gate / regularizer)
 
 
 @dataclass
