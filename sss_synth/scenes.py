@@ -314,3 +314,75 @@ def sghmc_params_for(scene: Scene, **kw) -> SGHMCParams:
     for k, v in kw.items():
         setattr(p, k, v)
     return p
+
+
+# ------------------------------------------------------------------ NEXT-4
+# Torus scooping toy (Fig. 2): a torus with ambient
+# lighting seen in frontal views; the targets are its silhouettes (constant
+# colour on black).  Input generation only (ray marching of the implicit
+# torus); the fit itself runs through the product's TrainStep.
+TORUS_R, TORUS_r, TORUS_COLOR = 0.6, 0.25, (0.9, 0.8, 0.3)
+
+
+def torus_cameras(n_views: int = 4, size: int = 64, dist: float = 3.0, tilt: float = 0.12) -> List[Camera]:
+    """Frontal cameras on the torus axis (+z), slightly tilted around it."""
+    cams = []
+    for k in range(n_views):
+        a = 2 * math.pi * k / max(1, n_views)
+        pos = np.array([tilt * math.cos(a), tilt * math.sin(a), 1.0])
+        pos = dist * pos / np.linalg.norm(pos)
+        R, t = look_at(pos, up=(0.0, 1.0, 0.0))
+        f = (size / 2.0) / math.tan(math.radians(60.0) / 2.0)
+        cams.append(Camera(R=R.astype(np.float32), t=t.astype(np.float32), fx=float(np.float32(f)),
+                           fy=float(np.float32(f)), cx=size / 2.0, cy=size / 2.0, width=size,
+                           height=size, z_near=0.2))
+    return cams
+
+
+def torus_targets(cams: List[Camera], R: float = TORUS_R, r: float = TORUS_r,
+                  color=TORUS_COLOR, samples: int = 512) -> np.ndarray:
+    """Silhouette images [V][3][H][W] float32: a pixel (centre ray) is the
+    torus colour iff its ray enters (sqrt(x^2 + y^2) - R)^2 + z^2 <= r^2."""
+    out = []
+    for cam in cams:
+        H, W = cam.height, cam.width
+        ys, xs = np.mgrid[0:H, 0:W]
+        d_cam = np.stack([(xs + 0.5 - cam.cx) / cam.fx, (ys + 0.5 - cam.cy) / cam.fy, np.ones_like(xs, float)], -1)
+        Rm = np.asarray(cam.R, np.float64).reshape(3, 3)
+        t = np.asarray(cam.t, np.float64)
+        o = -Rm.T @ t
+        d = d_cam @ Rm  # world directions (R^T d_cam)
+        d /= np.linalg.norm(d, axis=-1, keepdims=True)
+        dist = np.linalg.norm(o)
+        ts = np.linspace(dist - (R + r) * 1.5, dist + (R + r) * 1.5, samples)
+        hit = np.zeros((H, W), bool)
+        for tt in ts:
+            p = o + tt * d
+            q = (np.sqrt(p[..., 0] ** 2 + p[..., 1] ** 2) - R) ** 2 + p[..., 2] ** 2
+            hit |= q <= r * r
+        img = np.zeros((3, H, W), np.float32)
+        for c in range(3):
+            img[c][hit] = color[c]
+        out.append(img)
+    return np.stack(out)
+
+
+def torus_init(n_pos: int, n_neg: int, seed: int, sh_degree: int = 0) -> np.ndarray:
+    """Component planes initialised near the torus centre (Fig. 2: "We
+    initialize the component means near the center"): means N(0, 0.05^2),
+    flattened isotropic-in-plane scales, nu 3, colour 0.5, |o| 0.5 with the
+    requested signs (negative ones slightly smaller)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = n_pos + n_neg
+    P = param_plane_count(sh_degree)
+    pl = np.zeros((P, n), np.float32)
+    pl[0:3] = rng.normal(0.0, 0.05, (3, n))
+    pl[3] = pl[4] = math.log(0.3)
+    pl[5] = math.log(0.1)
+    pl[3:6] += rng.normal(0.0, 0.05, (3, n))
+    pl[6] = 1.0
+    pl[10] = _raw_from_nu(np.full(n, 3.0))
+    o = np.concatenate([np.full(n_pos, 0.5), np.full(n_neg, -0.4)])
+    pl[11] = np.arctanh(o)
+    pl[12:15] = 0.0  # colour 0.5 (SH DC 0)
+    return pl
