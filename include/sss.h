@@ -132,12 +132,21 @@ typedef struct {
  *                          optional diagnostic: NULL = not counted (the backward
  *                          does not read it)
  *  last      [V][H][W]     private: bin-list offset one past the last
- *                          composited entry (start of the backward replay) */
+ *                          composited entry (start of the backward replay)
+ *  tile_list [V][tiles][tile_cap], tile_count [V][tiles]: private, nullable
+ *            (both or neither): the bin-list offsets of the entries some
+ *            pixel of the tile composited, in order; the backward replays
+ *            only those (a tile with tile_count > tile_cap falls back to the
+ *            full range) */
 typedef struct {
   float* rgb;
   float* final_T;
   int32_t* n_contrib;
   int32_t* last;
+  int32_t* tile_list;
+  int32_t* tile_count;
+  int32_t tile_cap;
+  int32_t reserved;
 } sss_frame;
 
 /* Hyper-parameters of one sampler step (host struct; PAPER.md:151-163,

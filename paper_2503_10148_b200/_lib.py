@@ -53,7 +53,8 @@ class sss_bins(C.Structure):
 
 class sss_frame(C.Structure):
     _fields_ = [("rgb", C.c_void_p), ("final_T", C.c_void_p), ("n_contrib", C.c_void_p),
-                ("last", C.c_void_p)]
+                ("last", C.c_void_p), ("tile_list", C.c_void_p), ("tile_count", C.c_void_p),
+                ("tile_cap", C.c_int32), ("reserved", C.c_int32)]
 
 
 class sss_sghmc_hparams(C.Structure):

@@ -141,23 +141,34 @@ class Bins:
                           _ptr(self.overflow))
 
 
+TILE_CAP = 2048  # composited entries per tile the forward records for the backward
+
+
 @dataclass
 class Frame:
     rgb: torch.Tensor        # [V][3][H][W] f32
     final_T: torch.Tensor    # [V][H][W] f32
     n_contrib: Optional[torch.Tensor]  # [V][H][W] i32; None = not counted (diagnostic)
     last: torch.Tensor       # [V][H][W] i32
+    tile_list: Optional[torch.Tensor] = None   # private [V][tiles][cap] i32 (None: full replay)
+    tile_count: Optional[torch.Tensor] = None  # private [V][tiles] i32
 
     @classmethod
-    def empty(cls, V: int, H: int, W: int, device="cuda") -> "Frame":
+    def empty(cls, V: int, H: int, W: int, device="cuda", tile_cap: int = TILE_CAP) -> "Frame":
+        tiles = ((W + L.SSS_TILE - 1) // L.SSS_TILE) * ((H + L.SSS_TILE - 1) // L.SSS_TILE)
+        tl = tc = None
+        if tile_cap > 0:
+            tl = torch.empty((V, tiles, tile_cap), dtype=torch.int32, device=device)
+            tc = torch.empty((V, tiles), dtype=torch.int32, device=device)
         return cls(torch.empty((V, 3, H, W), dtype=torch.float32, device=device),
                    torch.empty((V, H, W), dtype=torch.float32, device=device),
                    torch.empty((V, H, W), dtype=torch.int32, device=device),
-                   torch.empty((V, H, W), dtype=torch.int32, device=device))
+                   torch.empty((V, H, W), dtype=torch.int32, device=device), tl, tc)
 
     def c(self) -> L.sss_frame:
+        cap = int(self.tile_list.shape[-1]) if self.tile_list is not None else 0
         return L.sss_frame(_ptr(self.rgb), _ptr(self.final_T), _ptr(self.n_contrib),
-                           _ptr(self.last))
+                           _ptr(self.last), _ptr(self.tile_list), _ptr(self.tile_count), cap, 0)
 
 
 def hparams_c(hp) -> L.sss_sghmc_hparams:

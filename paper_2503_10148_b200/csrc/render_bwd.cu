@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
-    float4* __restrict__ g2d) {
+    float4* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
+    int32_t tile_cap) {
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
   __shared__ int32_t spos[kBatch], sid[kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
@@ -245,15 +246,24 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   float4* gv = g2d + (int64_t)v * G.n * 3;
   float* myacc = acc + w * 10 * kAccPitch;
 
-  for (int32_t hi = end; hi > start; hi -= kBatch) {
-    const int32_t lo = max(start, hi - kBatch);
+  // the forward's list of the entries this tile composited (CTA-uniform
+  // choice): replay only those; else the whole [start, end) range
+  const int64_t tslot = (int64_t)v * G.tiles_x * G.tiles_y + tile;
+  const int32_t tcount = tile_list ? tile_count[tslot] : 0;
+  const bool use_list = tile_list != nullptr && tcount <= tile_cap;
+  const int32_t* tl = use_list ? tile_list + tslot * tile_cap : nullptr;
+  const int32_t lbeg = use_list ? 0 : start;
+  const int32_t lend = use_list ? tcount : end;
+  for (int32_t hi = lend; hi > lbeg; hi -= kBatch) {
+    const int32_t lo = max(lbeg, hi - kBatch);
     __syncthreads();  // previous batch fully consumed and flushed
     if (threadIdx.x == 0) SSS_COUNT(0, 1);
-    const int32_t pos = lo + (int32_t)threadIdx.x;
-    bool ok = (int)threadIdx.x < kBatch && pos < hi;
+    const int32_t li = lo + (int32_t)threadIdx.x;
+    bool ok = (int)threadIdx.x < kBatch && li < hi;
+    const int32_t pos = ok ? (use_list ? tl[li] : li) : 0;
     const int32_t id = ok ? idv[pos] : 0;
     int slot, nb;
-    if (FILTER) {
+    if (FILTER && !use_list) {
       if (ok) {
         const short4 r = rcv[id];
         ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
@@ -673,7 +683,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
 #define SSS_BWD_LAUNCH(F, L, N)                                                                     \
   render_bwd_kernel<F, L, N><<<grid, kRasterThreads, kAccBytes, s>>>(                              \
       rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last, \
-      d_rgb, target, loss_out, g2d)
+      d_rgb, target, loss_out, g2d, fwd->tile_list, fwd->tile_count, fwd->tile_cap)
 #define SSS_BWD_LAUNCH_N(F, L)              \
   do {                                      \
     if (nup) SSS_BWD_LAUNCH(F, L, true);    \

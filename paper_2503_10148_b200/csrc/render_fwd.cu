@@ -66,14 +66,20 @@ __device__ __forceinline__ void composite2(PixF2& p, float2 h, float4 b, float4 
 
 __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v.y : v.x; }
 
-template <bool FILTER, bool COUNT>
+template <bool FILTER, bool COUNT, bool REC>
 __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kernel(
     const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     float* __restrict__ rgb, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
-    int32_t* __restrict__ last) {
+    int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
+    int32_t tile_cap) {
+  static_assert(kBatch == kRasterThreads, "one staged entry per thread");
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
-  __shared__ int32_t spos[kBatch];
+  // REC: per batch, the entries each warp composited; double-buffered with
+  // spos so the append of batch k runs after the top barrier of batch k+1
+  // without a barrier of its own
+  __shared__ unsigned wmask2[2][kRasterWarps][kBatch / 32];
+  __shared__ int32_t spos2[2][kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
@@ -114,9 +120,39 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     for (int k = 0; k < kPX; ++k) d = d && !(lane_of(p[k >> 1].W, k) >= kWStop);
     return d;
   };
-  for (int32_t b0 = start; b0 < end; b0 += kBatch) {
-    if (__syncthreads_count(!all_done()) == 0) break;
+  int32_t n_rec = 0;  // REC: entries of this tile composited by some warp so far
+  int32_t* tl = REC ? tile_list + ((int64_t)v * G.tiles_x * G.tiles_y + tile) * tile_cap : nullptr;
+  // append the entries of buffer `pb` composited by any warp, in list order
+  auto append = [&](int pb) {
+    unsigned u[kBatch / 32];
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; ++q) {
+      u[q] = 0u;
+#pragma unroll
+      for (int ww = 0; ww < kRasterWarps; ++ww) u[q] |= wmask2[pb][ww][q];
+    }
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; ++q) {
+      off += q < w ? __popc(u[q]) : 0;
+      tot += __popc(u[q]);
+    }
+    const int slot = n_rec + off + __popc(u[w] & lt);
+    if (((u[w] >> lane) & 1u) && slot < tile_cap) tl[slot] = spos2[pb][threadIdx.x];
+    n_rec += tot;
+  };
+  int pb = 0;  // buffer of the current batch
+  bool pending = false;
+  for (int32_t b0 = start; b0 < end; b0 += kBatch, pb ^= 1) {
+    const int live = __syncthreads_count(!all_done());
+    if (REC && pending) append(pb ^ 1);
+    if (live == 0) { pending = false; break; }
     if (threadIdx.x == 0) SSS_COUNT(0, 1);
+    pending = true;
+    unsigned cm[kBatch / 32];  // REC: this warp's composited entries (warp-uniform bits)
+#pragma unroll
+    for (int q = 0; q < kBatch / 32; ++q) cm[q] = 0u;
+    int32_t (&spos)[kBatch] = spos2[pb];
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? idv[pos] : 0;
@@ -150,8 +186,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
-    if (__all_sync(0xffffffffu, all_done())) continue;
-    for (int j = 0; j < nb; ++j) {
+    const int nb_w = __all_sync(0xffffffffu, all_done()) ? 0 : nb;  // warp already finished
+    for (int j = 0; j < nb_w; ++j) {
       if (lane == 0) SSS_COUNT(1, 1);
       const float4 a = sa[j];
       const float4 b = sb[j];  // {C, hmax, o, inv_nu}
@@ -181,6 +217,10 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       }
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
+        if (REC) {
+#pragma unroll
+          for (int q = 0; q < kBatch / 32; ++q) cm[q] |= (j >> 5) == q ? 1u << (j & 31) : 0u;
+        }
         const float4 c = sc[j];  // {e, r, g, b}
         const int32_t pj1 = spos[j] + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
@@ -198,7 +238,17 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
     }
+    if (REC && lane < kBatch / 32) {
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q)
+        if (q == lane) wmask2[pb][w][q] = cm[q];
+    }
   }
+  if (REC && pending) {
+    __syncthreads();
+    append(pb ^ 1);
+  }
+  if (REC && threadIdx.x == 0) tile_count[(int64_t)v * G.tiles_x * G.tiles_y + tile] = n_rec;
   const int64_t HW = (int64_t)G.width * G.height;
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
@@ -252,16 +302,23 @@ extern "C" sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bi
   }
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 grid(G.tiles_x * G.tiles_y, n_views);
-#define SSS_FWD_LAUNCH(F, N)                                                                       \
-  render_fwd_kernel<F, N><<<grid, kRasterThreads, 0, s>>>((const float4*)pr->rec, (const short4*)pr->rect, \
-                                                          bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], \
-                                                          out->rgb, out->final_T, out->n_contrib, out->last)
+#define SSS_FWD_LAUNCH(F, N, R)                                                                         \
+  render_fwd_kernel<F, N, R><<<grid, kRasterThreads, 0, s>>>(                                             \
+      (const float4*)pr->rec, (const short4*)pr->rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2],   \
+      out->rgb, out->final_T, out->n_contrib, out->last, out->tile_list, out->tile_count, out->tile_cap)
+#define SSS_FWD_LAUNCH_R(F, N)                 \
+  do {                                         \
+    if (recl) SSS_FWD_LAUNCH(F, N, true);      \
+    else SSS_FWD_LAUNCH(F, N, false);          \
+  } while (0)
   const bool cnt = out->n_contrib != nullptr;
+  const bool recl = out->tile_list != nullptr && out->tile_count != nullptr && out->tile_cap > 0;
   if (G.shift > 0) {
-    if (cnt) SSS_FWD_LAUNCH(true, true); else SSS_FWD_LAUNCH(true, false);
+    if (cnt) SSS_FWD_LAUNCH_R(true, true); else SSS_FWD_LAUNCH_R(true, false);
   } else {
-    if (cnt) SSS_FWD_LAUNCH(false, true); else SSS_FWD_LAUNCH(false, false);
+    if (cnt) SSS_FWD_LAUNCH_R(false, true); else SSS_FWD_LAUNCH_R(false, false);
   }
+#undef SSS_FWD_LAUNCH_R
 #undef SSS_FWD_LAUNCH
   count_launch();
   return check_launch("sss_render_fwd");

@@ -102,7 +102,9 @@ class TrainStep:
         # when the caller collects statistics
         f = self.frame
         nc = f.n_contrib[:nv] if self.stats is not None else None
-        return A.Frame(f.rgb[:nv], f.final_T[:nv], nc, f.last[:nv])
+        return A.Frame(f.rgb[:nv], f.final_T[:nv], nc, f.last[:nv],
+                       f.tile_list[:nv] if f.tile_list is not None else None,
+                       f.tile_count[:nv] if f.tile_count is not None else None)
 
     def _bins_view(self, nv: int) -> A.Bins:
         b = self.bins[0]

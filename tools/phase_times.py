@@ -12,6 +12,7 @@ ap.add_argument("--views", type=int, default=None)
 ap.add_argument("--shift", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-count", action="store_true", help="forward without the n_contrib diagnostic")
+ap.add_argument("--tile-cap", type=int, default=None)
 a = ap.parse_args()
 sc = make_scene(a.config, n_views=a.views)
 cams = sc.cameras
@@ -20,8 +21,8 @@ params = P.Params(torch.from_numpy(sc.params).cuda(), sc.sh_degree)
 tgt = torch.from_numpy(make_targets(sc)).cuda()
 pr = P.sss_project(params, cams)
 bins = P.sss_bin_sort(pr, cams, bin_shift=a.shift)
-fr = P.sss_render_fwd(pr, bins, cams)
-fr_nc = P.Frame(fr.rgb, fr.final_T, None, fr.last)
+fr = P.sss_render_fwd(pr, bins, cams, out=P.Frame.empty(V, cams[0].height, cams[0].width, **({} if a.tile_cap is None else {"tile_cap": a.tile_cap})))
+fr_nc = P.Frame(fr.rgb, fr.final_T, None, fr.last, fr.tile_list, fr.tile_count)
 ws_g2d = torch.zeros(A.render_bwd_workspace_bytes(params.n, V), dtype=torch.uint8, device="cuda")
 ws_bin = torch.empty(A.bin_sort_workspace_bytes(params.n, cams, a.shift), dtype=torch.uint8, device="cuda")
 grad = P.Params.zeros_like(params)
@@ -43,7 +44,11 @@ for name, f in phases.items():
     res[name] = min(ts)
 tot = bins.totals.cpu().numpy()
 nc = fr.n_contrib.float()
+tcs = fr.tile_count.float() if fr.tile_count is not None else torch.zeros(1, device="cuda")
+cap = fr.tile_list.shape[-1] if fr.tile_list is not None else 0
 out = dict(config=a.config, views=V, shift=a.shift, ms=res, total_ms=sum(res.values()),
+           tile_count=dict(mean=float(tcs.mean()), max=float(tcs.max()), cap=int(cap),
+                           over=float((tcs > cap).float().mean())),
            instances_per_view=float(tot.mean()), capacity=bins.capacity,
            pairs_per_view=float(nc.sum().item()/V), mean_contrib=float(nc.mean().item()),
            mpix_per_s=V*cams[0].width*cams[0].height/sum(res.values())/1e3)
