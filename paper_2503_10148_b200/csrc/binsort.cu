@@ -59,7 +59,7 @@ constexpr int kChunk = SSS_CHUNK;  // depth-sorted components per histogram / sc
 constexpr size_t kScatterSmemMax = 225 * 1024;  // dynamic shared memory of a scatter CTA
 
 struct WsLayout {
-  size_t keys_a, keys_b, vals_a, vals_b, n_vis, radix_hist, chunk_hist, bin_total, bin_start, total;
+  size_t keys_a, keys_b, vals_a, vals_b, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start, total;
   int tiles_per_view, n_chunks, chunk;
 };
 
@@ -80,6 +80,7 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.n_vis = take((size_t)V * 4);
   L.radix_hist = take((size_t)V * 256 * (size_t)L.tiles_per_view * 4);
   L.chunk_hist = take((size_t)V * L.n_chunks * (size_t)g.n_bins * 4);
+  L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
   L.bin_total = take((size_t)V * g.n_bins * 4);
   L.bin_start = take((size_t)V * g.n_bins * 4);
   L.total = off;
@@ -116,27 +117,47 @@ __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0
   bx0 = r.x >> shift; by0 = r.y >> shift; bx1 = r.z >> shift; by1 = r.w >> shift;
 }
 
+// Per (chunk, view): bin counts of the chunk's instances, per warp of the
+// scatter's partition (warp w owns kChunk/8 consecutive depth-sorted
+// components).  Writes the chunk totals (u32, for the scans) and the per-warp
+// counts (u8: a warp's 128 components hit a bin at most 128 times), so the
+// scatter needs no counting pass of its own.
 __global__ void __launch_bounds__(256) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
                                                          const int32_t* __restrict__ n_vis,
                                                          const short4* __restrict__ rect, int64_t n,
                                                          int chunk, int n_chunks, BinGeom g,
-                                                         uint32_t* __restrict__ chunk_hist) {
-  extern __shared__ uint32_t hs[];
+                                                         uint32_t* __restrict__ chunk_hist,
+                                                         uint8_t* __restrict__ warp_hist) {
+  extern __shared__ uint32_t hs[];  // [8][n_bins]
   const int v = blockIdx.y, c = blockIdx.x;
-  for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) hs[b] = 0;
+  const int nb = g.n_bins;
+  for (int k = threadIdx.x; k < kScatterWarps * nb; k += blockDim.x) hs[k] = 0;
   __syncthreads();
-  const int64_t lo = (int64_t)c * chunk;
-  const int64_t hi = min((int64_t)(c + 1) * chunk, (int64_t)n_vis[v]);
-  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+  const int w = threadIdx.x >> 5;
+  const int per_warp = chunk / kScatterWarps;
+  const int64_t wlo = (int64_t)c * chunk + (int64_t)w * per_warp;
+  const int64_t whi = min(wlo + per_warp, (int64_t)n_vis[v]);
+  uint32_t* my = hs + (size_t)w * nb;
+  for (int64_t j = wlo + lane_id(); j < whi; j += 32) {
     const int id = sorted_ids[(int64_t)v * n + j];
     int bx0, by0, bx1, by1;
     bin_rect(rect[(int64_t)v * n + id], g.shift, bx0, by0, bx1, by1);
     for (int by = by0; by <= by1; ++by)
-      for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&hs[by * g.bins_x + bx], 1u);
+      for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&my[by * g.bins_x + bx], 1u);
   }
   __syncthreads();
-  uint32_t* out = chunk_hist + ((size_t)v * n_chunks + c) * g.n_bins;
-  for (int b = threadIdx.x; b < g.n_bins; b += blockDim.x) out[b] = hs[b];
+  uint32_t* out = chunk_hist + ((size_t)v * n_chunks + c) * nb;
+  uint8_t* wout = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int ww = 0; ww < kScatterWarps; ++ww) {
+      const uint32_t x = hs[(size_t)ww * nb + b];
+      wout[(size_t)ww * nb + b] = (uint8_t)x;
+      t += x;
+    }
+    out[b] = t;
+  }
 }
 
 // per (view, bin): exclusive scan over chunks in place; bin totals
@@ -206,8 +227,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
 // Walks the warp's depth-sorted components [wlo, whi), 32 at a time, one
 // component per lane; each lane loops over the bins of its component's bin
 // rect (row-major).
-//   COUNT: per-warp bin counts (shared atomics).
-//   place: the slot of (lane i, bin b) is cnt[b] + the number of lanes
+//   The slot of (lane i, bin b) is cnt[b] + the number of lanes
 //   i' < i whose component also covers b.  The lanes covering b are
 //   colmask[bx] & rowmask[by] (one ballot per bin column and row), so the
 //   rank is a popcount and no lane order has to be serialised; the first
@@ -216,7 +236,6 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
 //   straight to its global slot gofs[b] + slot (4-byte stores that L2
 //   merges; staging the chunk in shared memory for coalesced runs measured
 //   slower — it costs occupancy).
-template <bool COUNT>
 __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
                                           const float* __restrict__ dv, int64_t wlo, int64_t whi,
                                           const BinGeom& g, uint32_t* cnt, uint32_t* colmask,
@@ -243,10 +262,7 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
     int bx0 = r.x >> g.shift, by0 = r.y >> g.shift;
     int bx1 = r.z >> g.shift, by1 = r.w >> g.shift;
     if (!valid) { bx0 = by0 = 1; bx1 = by1 = 0; }  // empty
-    if constexpr (COUNT) {
-      for (int by = by0; by <= by1; ++by)
-        for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&cnt[by * g.bins_x + bx], 1u);
-    } else {
+    {
     // covering lanes per bin column / row
     for (int x = 0; x <= bx_max; ++x) {
       const unsigned m = __ballot_sync(full, bx0 <= x && x <= bx1);
@@ -282,15 +298,15 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
 }
 
 // stable scatter: CTA per (chunk of kChunk depth-sorted components, view);
-// warp w owns kChunk/8 consecutive components.  Phase 1 counts per (warp,
-// bin); an exclusive prefix over warps turns the counts into each warp's
-// first slot in the chunk's segment of every bin, and phase 2 writes the ids.
+// warp w owns kChunk/8 consecutive components.  The per-(warp, bin) counts of
+// chunk_hist_kernel, prefix-summed over warps, give each warp's first slot in
+// the chunk's segment of every bin; the warps then write their ids.
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
-    const uint32_t* __restrict__ chunk_hist, const uint32_t* __restrict__ bin_start,
-    const int64_t* __restrict__ totals, int64_t capacity, int32_t* __restrict__ ids,
-    uint64_t* __restrict__ keys) {
+    const uint32_t* __restrict__ chunk_hist, const uint8_t* __restrict__ warp_hist,
+    const uint32_t* __restrict__ bin_start, const int64_t* __restrict__ totals, int64_t capacity,
+    int32_t* __restrict__ ids, uint64_t* __restrict__ keys) {
   extern __shared__ uint32_t sm[];
   const int v = blockIdx.y, c = blockIdx.x;
   if (totals[v] > capacity) return;
@@ -301,10 +317,18 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   uint32_t* cnt = sm;                                  // [8][n_bins] per-warp counters / slots
   uint32_t* gofs = cnt + (size_t)kScatterWarps * nb;  // [n_bins] the chunk's first slot per bin
   uint32_t* masks = gofs + nb;                         // [8][bins_x + bins_y] lane masks
-  for (int k = threadIdx.x; k < kScatterWarps * nb; k += blockDim.x) cnt[k] = 0;
   const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
+  const uint8_t* wh = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
   const uint32_t* bs = bin_start + (size_t)v * nb;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) gofs[b] = bs[b] + ch[b];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    gofs[b] = bs[b] + ch[b];
+    uint32_t acc = 0;  // exclusive prefix of the per-warp counts (chunk_hist_kernel)
+#pragma unroll
+    for (int ww = 0; ww < kScatterWarps; ++ww) {
+      cnt[(size_t)ww * nb + b] = acc;
+      acc += wh[(size_t)ww * nb + b];
+    }
+  }
   __syncthreads();
   const int w = threadIdx.x >> 5;
   constexpr int per_warp = kChunk / kScatterWarps;
@@ -318,18 +342,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  warp_walk<true>(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);  // phase 1
-  __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // warp prefix per bin
-    uint32_t acc = 0;
-    for (int ww = 0; ww < kScatterWarps; ++ww) {
-      const uint32_t x = cnt[(size_t)ww * nb + b];
-      cnt[(size_t)ww * nb + b] = acc;
-      acc += x;
-    }
-  }
-  __syncthreads();
-  warp_walk<false>(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);  // phase 2
+  warp_walk(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);
 }
 
 }  // namespace
@@ -379,10 +392,17 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   int32_t* n_vis = (int32_t*)(w + L.n_vis);
   uint32_t* rhist = (uint32_t*)(w + L.radix_hist);
   uint32_t* chist = (uint32_t*)(w + L.chunk_hist);
+  uint8_t* whist = (uint8_t*)(w + L.warp_hist);
   uint32_t* btot = (uint32_t*)(w + L.bin_total);
   uint32_t* bstart = (uint32_t*)(w + L.bin_start);
   const short4* rect = (const short4*)pr->rect;
 
+  static thread_local bool attr_set = false;
+  if (!attr_set) {  // large dynamic shared memory for the per-warp bin counters
+    cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmemMax);
+    cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
   cudaMemsetAsync(out->overflow, 0, sizeof(int32_t), s);
   cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   if (n > 0) {
@@ -394,8 +414,8 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     int32_t* vin = vals_a;
     // after 4 passes the sorted ids are in vals_a
     const dim3 gc(L.n_chunks, n_views);
-    const size_t hsm = (size_t)g.n_bins * 4;
-    chunk_hist_kernel<<<gc, 256, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist);
+    const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
+    chunk_hist_kernel<<<gc, 256, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
     column_scan_kernel<<<dim3(div_up(g.n_bins, 128), n_views), 128, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
     count_launch(2);
   } else {
@@ -405,15 +425,9 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
                                             out->overflow);
   count_launch();
   if (n > 0) {
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmemMax);
-      cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
     const size_t ssm = ((size_t)(kScatterWarps + 1) * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y)) * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
-        vals_a, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, bstart, out->totals, out->capacity,
+        vals_a, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, out->totals, out->capacity,
         out->ids, out->keys);
     count_launch();
   }
