@@ -17,12 +17,14 @@ WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram r
 for rep in sys.argv[1:]:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h, u, v = r[0], r[1], r[2]
-    name = v[h.index("Kernel Name")][:90]
-    print(f"### {rep}\n{name}\n")
-    print("| metric | value |\n|---|---|")
+    h, u = r[0], r[1]
+    rows = r[2:]
+    names = [row[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("unnamed>::", "")[:40] for row in rows]
+    print(f"### {rep}\n")
+    print("| metric | " + " | ".join(names) + " |")
+    print("|---|" + "---|" * len(rows))
     for k, lab in WANT:
         if k in h:
             i = h.index(k)
-            print(f"| {lab} (`{k}`) | {v[i]} {u[i]} |")
+            print(f"| {lab} ({u[i]}) | " + " | ".join(row[i] for row in rows) + " |")
     print()
