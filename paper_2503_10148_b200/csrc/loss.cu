@@ -13,12 +13,14 @@
 //   dL/dx_q = k ((w * A)_q + x_q (w * B)_q + y_q (w * C)_q),  k = -eps / (3 Hv Wv).
 //
 // B200 design: two separable-filter passes over 32x32 tiles staged in shared
-// memory (HBM-bound: the image pair is read twice, the three maps written
-// once and read once, the gradient written once — ~130 B per pixel).
+// memory, register-blocked (a thread sums 4 neighbouring outputs from one
+// 14-value window of loads).  HBM traffic: the image pair is read twice, the
+// three maps written once and read once, the gradient written once — 132 B
+// per pixel.
 //   ssim_maps_kernel:  image tiles + 10-pixel halo -> 5 moments (horizontal
 //                      then vertical 11-tap sums) -> S (block-summed into the
 //                      loss), k A, k B, k C at the tile's valid positions;
-//   ssim_grad_kernel:  k A, k B, k C tiles + halo -> 3 correlations -> the
+//   image_grad_kernel: k A, k B, k C tiles + halo -> 3 correlations -> the
 //                      gradient, plus the L1 term (1 - eps) sign(x - y)/(3HW).
 #include <cmath>
 
@@ -70,19 +72,28 @@ __global__ void __launch_bounds__(256) ssim_maps_kernel(const float* __restrict_
     ys[r][c] = in ? y[(int64_t)gy * G.W + gx] : 0.f;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kLS * kLT; k += 256) {  // horizontal 11-tap sums
-    const int r = k / kLT, c = k % kLT;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+  // horizontal 11-tap sums, 4 consecutive columns per work item (register
+  // blocked: 14 loads of x and y serve 4 outputs)
+  for (int k = threadIdx.x; k < kLS * (kLT / 4); k += 256) {
+    const int r = k / (kLT / 4), c0 = (k % (kLT / 4)) * 4;
+    float xa[kWin + 3], ya[kWin + 3];
 #pragma unroll
-    for (int t = 0; t < kWin; ++t) {
-      const float a = xs[r][c + t], b = ys[r][c + t], w = G.g[t];
-      s0 = fmaf(w, a, s0);
-      s1 = fmaf(w, b, s1);
-      s2 = fmaf(w * a, a, s2);
-      s3 = fmaf(w * b, b, s3);
-      s4 = fmaf(w * a, b, s4);
+    for (int t = 0; t < kWin + 3; ++t) { xa[t] = xs[r][c0 + t]; ya[t] = ys[r][c0 + t]; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+      for (int t = 0; t < kWin; ++t) {
+        const float a = xa[q + t], b = ya[q + t], w = G.g[t];
+        s0 = fmaf(w, a, s0);
+        s1 = fmaf(w, b, s1);
+        s2 = fmaf(w * a, a, s2);
+        s3 = fmaf(w * b, b, s3);
+        s4 = fmaf(w * a, b, s4);
+      }
+      hm[0][r][c0 + q] = s0; hm[1][r][c0 + q] = s1; hm[2][r][c0 + q] = s2;
+      hm[3][r][c0 + q] = s3; hm[4][r][c0 + q] = s4;
     }
-    hm[0][r][c] = s0; hm[1][r][c] = s1; hm[2][r][c] = s2; hm[3][r][c] = s3; hm[4][r][c] = s4;
   }
   __syncthreads();
   const int64_t HvWv = (int64_t)G.Hv * G.Wv;
@@ -90,33 +101,42 @@ __global__ void __launch_bounds__(256) ssim_maps_kernel(const float* __restrict_
   float* mB = mA + HvWv;
   float* mC = mB + HvWv;
   float ssum = 0.f;
-  for (int k = threadIdx.x; k < kLT * kLT; k += 256) {  // vertical sums -> S, A, B, C
-    const int r = k / kLT, c = k % kLT;
-    const int py = py0 + r, px = px0 + c;
-    if (py >= G.Hv || px >= G.Wv) continue;
-    float mx = 0.f, my = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
+  // vertical sums -> S, A, B, C; 4 consecutive rows per work item
+  for (int k = threadIdx.x; k < (kLT / 4) * kLT; k += 256) {
+    const int c = k % kLT, r0 = (k / kLT) * 4;
+    float mom[5][4];
 #pragma unroll
-    for (int t = 0; t < kWin; ++t) {
-      const float w = G.g[t];
-      mx = fmaf(w, hm[0][r + t][c], mx);
-      my = fmaf(w, hm[1][r + t][c], my);
-      xx = fmaf(w, hm[2][r + t][c], xx);
-      yy = fmaf(w, hm[3][r + t][c], yy);
-      xy = fmaf(w, hm[4][r + t][c], xy);
+    for (int m = 0; m < 5; ++m) {
+      float col[kWin + 3];
+#pragma unroll
+      for (int t = 0; t < kWin + 3; ++t) col[t] = hm[m][r0 + t][c];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float acc = 0.f;
+#pragma unroll
+        for (int t = 0; t < kWin; ++t) acc = fmaf(G.g[t], col[q + t], acc);
+        mom[m][q] = acc;
+      }
     }
-    const float sx2 = xx - mx * mx, sy2 = yy - my * my, sxy = xy - mx * my;
-    const float n1 = 2.f * mx * my + kC1, n2 = 2.f * sxy + kC2;
-    const float d1 = mx * mx + my * my + kC1, d2 = sx2 + sy2 + kC2;
-    const float inv = 1.f / (d1 * d2);
-    const float S = n1 * n2 * inv;
-    ssum += S;
-    const float dS_dmx = 2.f * my * n2 * inv - S * 2.f * mx / d1;
-    const float dS_dsx2 = -S / d2;
-    const float dS_dsxy = 2.f * n1 * inv;
-    const int64_t o = (int64_t)py * G.Wv + px;
-    mA[o] = G.k_ssim * (dS_dmx - 2.f * mx * dS_dsx2 - my * dS_dsxy);
-    mB[o] = G.k_ssim * (2.f * dS_dsx2);
-    mC[o] = G.k_ssim * dS_dsxy;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int py = py0 + r0 + q, px = px0 + c;
+      if (py >= G.Hv || px >= G.Wv) continue;
+      const float mx = mom[0][q], my = mom[1][q], xx = mom[2][q], yy = mom[3][q], xy = mom[4][q];
+      const float sx2 = xx - mx * mx, sy2 = yy - my * my, sxy = xy - mx * my;
+      const float n1 = 2.f * mx * my + kC1, n2 = 2.f * sxy + kC2;
+      const float d1 = mx * mx + my * my + kC1, d2 = sx2 + sy2 + kC2;
+      const float inv = 1.f / (d1 * d2);
+      const float S = n1 * n2 * inv;
+      ssum += S;
+      const float dS_dmx = 2.f * my * n2 * inv - S * 2.f * mx / d1;
+      const float dS_dsx2 = -S / d2;
+      const float dS_dsxy = 2.f * n1 * inv;
+      const int64_t o = (int64_t)py * G.Wv + px;
+      mA[o] = G.k_ssim * (dS_dmx - 2.f * mx * dS_dsx2 - my * dS_dsxy);
+      mB[o] = G.k_ssim * (2.f * dS_dsx2);
+      mC[o] = G.k_ssim * dS_dsxy;
+    }
   }
   const float bs = block_sum256(ssum, red);
   if (threadIdx.x == 0 && loss) {
@@ -154,42 +174,57 @@ __global__ void __launch_bounds__(256) image_grad_kernel(const float* __restrict
       for (int m = 0; m < 3; ++m) ms[m][r][c] = in ? mA[m * HvWv + o] : 0.f;
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < kLS * kLT; k += 256) {  // horizontal: sum_dx g[dx] M[r][c + 10 - dx]
-      const int r = k / kLT, c = k % kLT;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    // horizontal: sum_dx g[dx] M[r][c + 10 - dx], 4 columns per work item
+    for (int k = threadIdx.x; k < kLS * (kLT / 4); k += 256) {
+      const int r = k / (kLT / 4), c0 = (k % (kLT / 4)) * 4;
 #pragma unroll
-      for (int t = 0; t < kWin; ++t) {
-        const float w = G.g[t];
-        s0 = fmaf(w, ms[0][r][c + kWin - 1 - t], s0);
-        s1 = fmaf(w, ms[1][r][c + kWin - 1 - t], s1);
-        s2 = fmaf(w, ms[2][r][c + kWin - 1 - t], s2);
+      for (int m = 0; m < 3; ++m) {
+        float row[kWin + 3];
+#pragma unroll
+        for (int t = 0; t < kWin + 3; ++t) row[t] = ms[m][r][c0 + t];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float acc = 0.f;
+#pragma unroll
+          for (int t = 0; t < kWin; ++t) acc = fmaf(G.g[t], row[q + kWin - 1 - t], acc);
+          hm[m][r][c0 + q] = acc;
+        }
       }
-      hm[0][r][c] = s0; hm[1][r][c] = s1; hm[2][r][c] = s2;
     }
     __syncthreads();
   }
   float lsum = 0.f;
-  for (int k = threadIdx.x; k < kLT * kLT; k += 256) {
-    const int r = k / kLT, c = k % kLT;
-    const int qy = qy0 + r, qx = qx0 + c;
-    if (qy >= G.H || qx >= G.W) continue;
-    const int64_t o = (int64_t)qy * G.W + qx;
-    const float a = x[o], b = y[o];
-    const float df = a - b;
-    lsum += fabsf(df);
-    float gq = G.k_l1 * (df > 0.f ? 1.f : (df < 0.f ? -1.f : 0.f));
+  // 4 consecutive rows per work item: vertical correlations + gradient
+  for (int k = threadIdx.x; k < (kLT / 4) * kLT; k += 256) {
+    const int c = k % kLT, r0 = (k / kLT) * 4;
+    float f[3][4];
     if (with_ssim) {
-      float fA = 0.f, fB = 0.f, fC = 0.f;
 #pragma unroll
-      for (int t = 0; t < kWin; ++t) {  // vertical: sum_dy g[dy] H[r + 10 - dy][c]
-        const float w = G.g[t];
-        fA = fmaf(w, hm[0][r + kWin - 1 - t][c], fA);
-        fB = fmaf(w, hm[1][r + kWin - 1 - t][c], fB);
-        fC = fmaf(w, hm[2][r + kWin - 1 - t][c], fC);
+      for (int m = 0; m < 3; ++m) {
+        float col[kWin + 3];
+#pragma unroll
+        for (int t = 0; t < kWin + 3; ++t) col[t] = hm[m][r0 + t][c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // sum_dy g[dy] H[r + 10 - dy][c]
+          float acc = 0.f;
+#pragma unroll
+          for (int t = 0; t < kWin; ++t) acc = fmaf(G.g[t], col[q + kWin - 1 - t], acc);
+          f[m][q] = acc;
+        }
       }
-      gq += fA + a * fB + b * fC;
     }
-    d[o] = gq;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int qy = qy0 + r0 + q, qx = qx0 + c;
+      if (qy >= G.H || qx >= G.W) continue;
+      const int64_t o = (int64_t)qy * G.W + qx;
+      const float a = x[o], b = y[o];
+      const float df = a - b;
+      lsum += fabsf(df);
+      float gq = G.k_l1 * (df > 0.f ? 1.f : (df < 0.f ? -1.f : 0.f));
+      if (with_ssim) gq += f[0][q] + a * f[1][q] + b * f[2][q];
+      d[o] = gq;
+    }
   }
   const float bs = block_sum256(lsum, red);
   if (threadIdx.x == 0 && loss) atomicAdd(loss, G.k_l1 * bs);
