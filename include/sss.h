@@ -169,6 +169,13 @@ typedef struct {
   /* NEXT-3 mean update: 0 gated SGHMC (Eq. 10), 1 SGLD (F disabled,
    * PAPER.md:161), 2 Adam on the means with lr (setting 1's optimiser). */
   int32_t mu_mode;
+  /* Plane range [plane_begin, plane_end) this call updates (0, 0 = all):
+   * the ZeRO-1 sharded step of the multi-GPU path updates only the planes
+   * its rank owns after a reduce-scatter of the gradient, then the ranks
+   * all-gather the parameters (SURVEY.md §8(e) option 2).  Every plane's
+   * update reads the pre-update parameters, so a split into ranges equals
+   * the full update bit for bit. */
+  int32_t plane_begin, plane_end;
   int32_t reserved;
 } sss_sghmc_hparams;
 

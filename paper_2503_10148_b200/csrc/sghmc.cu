@@ -8,6 +8,7 @@
 //   mu'   = mu - eps^2 g + gate (F + N),  F = eps (1 - eps C) r,  N = eta xi
 //   gate  = sigmoid(-k (|o| - t))
 //   burn-in: F = 0, N = eta Sigma xi (Sigma of the pre-update component)
+//   plane range [p0, p1): only those planes are written (ZeRO-1 shard).
 //   NEXT-3 mu_mode: 1 = SGLD (F = 0), 2 = Adam on the means;
 //   the opacity map follows the parameter variant (sigmoid for POSITIVE).
 //   Eq. 8 regularizers (R27): g(log_scale_j) += eps_Sigma exp(s_j),
@@ -34,6 +35,7 @@ struct HP {
   float beta1, beta2, adam_eps, grad_scale;
   float eps_o, eps_sigma;  // Eq. 8 regularizer weights
   int mu_mode;             // 0 SGHMC, 1 SGLD (F = 0), 2 Adam on the means
+  int p0, p1;              // planes updated by this call
   float inv_b1t, inv_b2t;  // 1 / (1 - beta^t)
   uint32_t ctr2, ctr3;     // step (lo, hi)
   uint32_t key0, key1;     // seed (lo, hi)
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   sincospi(2.0 * u3, &s3, &c3);
   const float xi[3] = {(float)(r0 * c1), (float)(r0 * s1), (float)(r1 * c3)};
   // ---- mean: gated SGHMC
+  auto mine = [&](int p) { return p >= hp.p0 && p < hp.p1; };
   const float eps = hp.lr, Cf = hp.friction, eta = hp.noise;
   float noise[3];
   if (hp.burn_in) {
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     for (int a = 0; a < 3; ++a) noise[a] = eta * xi[a];
   }
   for (int a = 0; a < 3; ++a) {
+    if (!mine(a)) continue;
     const int64_t idx = a * n + i;
     const float graw = Gr.mean[idx] * hp.grad_scale;
     if (hp.mu_mode == 2) {  // setting 1: Adam on the means, no sampler state
@@ -114,15 +118,20 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   }
   // ---- Adam on the other groups
   for (int a = 0; a < 3; ++a) {
+    if (!mine(3 + a)) continue;
     const int64_t idx = a * n + i;
     const float reg = hp.eps_sigma != 0.f ? hp.eps_sigma * expf(P.log_scale[idx]) : 0.f;
     adam_plane(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, idx, hp.lr_group[0], hp, reg);
   }
-  for (int a = 0; a < 4; ++a) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
-  adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
-  const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (positive ? o * (1.f - o) : 1.f - o * o);
-  adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
-  for (int k = 0; k < 3 * K; ++k) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
+  for (int a = 0; a < 4; ++a)
+    if (mine(6 + a)) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
+  if (mine(10)) adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
+  if (mine(11)) {
+    const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (positive ? o * (1.f - o) : 1.f - o * o);
+    adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
+  }
+  for (int k = 0; k < 3 * K; ++k)
+    if (mine(12 + k)) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
 }
 
 }  // namespace
@@ -154,6 +163,11 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
   hp.beta1 = h->beta1; hp.beta2 = h->beta2; hp.adam_eps = h->adam_eps; hp.grad_scale = h->grad_scale;
   hp.eps_o = h->eps_o; hp.eps_sigma = h->eps_sigma;
   hp.mu_mode = h->mu_mode;
+  const int Pn = 12 + 3 * (p->sh_degree + 1) * (p->sh_degree + 1);
+  hp.p0 = h->plane_begin;
+  hp.p1 = (h->plane_begin == 0 && h->plane_end == 0) ? Pn : h->plane_end;
+  if (hp.p0 < 0 || hp.p1 > Pn || hp.p0 > hp.p1) { set_error("sss_sghmc_step: bad plane range"); return SSS_ERR_ARG; }
+  if (hp.p0 == hp.p1) return SSS_OK;
   if (hp.mu_mode < 0 || hp.mu_mode > 2) { set_error("sss_sghmc_step: mu_mode outside [0,2]"); return SSS_ERR_ARG; }
   hp.inv_b1t = (float)(1.0 / (1.0 - pow((double)h->beta1, (double)h->step)));
   hp.inv_b2t = (float)(1.0 / (1.0 - pow((double)h->beta2, (double)h->step)));

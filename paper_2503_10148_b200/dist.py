@@ -1,11 +1,18 @@
 """View-parallel data parallelism.
 
-One process per GPU (torchrun); rank r renders views {v : v mod R = r}, all
-ranks hold a full parameter replica, the flat fp32 gradient buffer is summed
-with one NCCL all-reduce over NVLink/NVSwitch, and every rank then applies
-the identical SGHMC/Adam step (same Philox counters), so replicas stay
-bit-identical without a parameter broadcast.  torch.distributed is plumbing
-only (process group + NCCL); nothing here computes the method.
+One process per GPU (torchrun); rank r renders views {v : v mod R = r} and
+all ranks hold a full parameter replica.  Two exchange schemes for the flat
+fp32 [P][n] gradient buffer:
+  * replicated: one NCCL all-reduce, then every rank applies the identical
+    SGHMC/Adam step (same Philox counters);
+  * sharded (ZeRO-1, §8(e) option 2, the default for R > 1): the buffer is
+    padded to R * ceil(P / R) planes, reduce-scattered by planes, each rank
+    updates only its planes (sss_sghmc_step's plane range; every plane's
+    update reads only the replicated pre-update parameters), and the ranks
+    all-gather the parameter planes.  Same bytes on the wire as the
+    all-reduce; the sampler's HBM work is divided by R.
+Either way replicas stay bit-identical.  torch.distributed is plumbing only
+(process group + NCCL); nothing here computes the method.
 """
 from __future__ import annotations
 
@@ -46,6 +53,44 @@ def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
+
+
+def plane_shard(P: int, rank: int, world: int):
+    """(planes per rank Pr, [begin, end) owned by `rank`) of a [R * Pr][n]
+    padded plane buffer."""
+    pr = -(-P // world)
+    return pr, (min(rank * pr, P), min((rank + 1) * pr, P))
+
+
+def _nccl(group=None) -> bool:
+    return dist.is_initialized() and dist.get_backend(group) == "nccl"
+
+
+def reduce_scatter_planes_(full: torch.Tensor, scratch: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum `full` [R * Pr][n] over ranks into this rank's plane slice (the
+    other slices are left stale).  NCCL reduce-scatter; gloo (CPU tests)
+    all-reduces, which leaves the same values in the slice."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pr = full.shape[0] // world
+    mine = full[rank * pr:(rank + 1) * pr]
+    if _nccl(group):
+        dist.reduce_scatter_tensor(scratch, full, op=dist.ReduceOp.SUM, group=group)
+        mine.copy_(scratch)
+    else:
+        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    return mine
+
+
+def all_gather_planes_(full: torch.Tensor, scratch: torch.Tensor, group=None) -> torch.Tensor:
+    """Every rank's plane slice of `full` [R * Pr][n] to every rank."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pr = full.shape[0] // world
+    scratch.copy_(full[rank * pr:(rank + 1) * pr])
+    if _nccl(group):
+        dist.all_gather_into_tensor(full, scratch, group=group)
+    else:
+        dist.all_gather(list(full.view(world, pr, -1).unbind(0)), scratch, group=group)
+    return full
 
 
 def allreduce_max(x: float, device=None) -> float:

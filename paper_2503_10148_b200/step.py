@@ -26,10 +26,27 @@ class TrainStep:
                  views_per_batch: int = 16, bg=(0.0, 0.0, 0.0), headroom: float = 1.25,
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
-                 eps_dssim: float = 0.0, variant: int = 0):
+                 eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None):
         dev = planes.device
-        self.params = A.Params(planes, sh_degree, variant)
-        self.grad = A.Params.zeros_like(self.params)
+        world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
+        # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
+        # to R * ceil(P / R) planes; the Params views cover the first P
+        self.shard = (world > 1) if shard_update is None else (bool(shard_update) and world > 1)
+        P = planes.shape[0]
+        self.world = world
+        if self.shard:
+            self.rank = D.dist.get_rank(group)
+            pr, (self.p0, self.p1) = D.plane_shard(P, self.rank, world)
+            pad = torch.zeros((pr * world, planes.shape[1]), dtype=planes.dtype, device=dev)
+            pad[:P].copy_(planes)
+            self.params_pad = pad
+            self.grad_pad = torch.zeros_like(pad)
+            self.scratch = torch.empty((pr, planes.shape[1]), dtype=planes.dtype, device=dev)
+            self.params = A.Params(pad[:P], sh_degree, variant)
+            self.grad = A.Params(self.grad_pad[:P], sh_degree, variant)
+        else:
+            self.params = A.Params(planes, sh_degree, variant)
+            self.grad = A.Params.zeros_like(self.params)
         self.m = A.Params(adam_m if adam_m is not None else torch.zeros_like(planes), sh_degree, variant)
         self.v = A.Params(adam_v if adam_v is not None else torch.zeros_like(planes), sh_degree, variant)
         n = self.params.n
@@ -151,12 +168,23 @@ class TrainStep:
     def step(self, targets: torch.Tensor) -> torch.Tensor:
         """One full iteration; returns the (device) loss of this rank."""
         self.forward_backward(targets)
-        D.allreduce_sum_(self.grad.planes, self.group)
-        self._mark("allreduce")
         self.hp.step = self.t
         self.hp.grad_scale = 1.0 / self.total_views
-        A.sss_sghmc_step(self.params, self.grad, self.m, self.v, self.r, self.hp)
-        self._mark("sghmc")
+        if self.shard:
+            D.reduce_scatter_planes_(self.grad_pad, self.scratch, self.group)
+            self._mark("allreduce")
+            self.hp.plane_begin, self.hp.plane_end = self.p0, self.p1
+            if self.p1 > self.p0:
+                A.sss_sghmc_step(self.params, self.grad, self.m, self.v, self.r, self.hp)
+            self._mark("sghmc")
+            D.all_gather_planes_(self.params_pad, self.scratch, self.group)
+            self._mark("allgather")
+        else:
+            D.allreduce_sum_(self.grad.planes, self.group)
+            self._mark("allreduce")
+            self.hp.plane_begin, self.hp.plane_end = 0, 0
+            A.sss_sghmc_step(self.params, self.grad, self.m, self.v, self.r, self.hp)
+            self._mark("sghmc")
         self.t += 1
         return self.loss
 

@@ -106,6 +106,8 @@ class SGHMCParams:
     eps_sigma: float = 0.0  # Eq. 8 sqrt-eigenvalue regularizer weight
     mu_mode: int = 0  # NEXT-3: 0 SGHMC, 1 SGLD (F disabled), 2 Adam on the means
     variant: int = 0  # parameter-set variant (oracle: opacity map of gate / regularizer)
+    plane_begin: int = 0  # planes updated by one call (0, 0 = all; ZeRO-1 shards)
+    plane_end: int = 0
 
 
 @dataclass

@@ -103,3 +103,66 @@ def test_checksum_is_bitwise():
     assert D.replica_checksum(a) == D.replica_checksum(b)
     b[17] = torch.nextafter(b[17], torch.tensor(10.0))
     assert D.replica_checksum(a) != D.replica_checksum(b)
+
+
+def _shard_worker(rank, world, port, out_q):
+    """ZeRO-1 plane-sharded step on gloo: reduce-scatter of the padded
+    gradient planes, each rank keeps the sampler update of its own planes
+    (computed here with the fp64 oracle, which updates every plane from the
+    pre-update state), all-gather of the parameter planes; the result must
+    equal the replicated full step on every rank, bit for bit."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    from oracle import oracle as O
+    from paper_2503_10148_b200 import dist as D
+
+    D.init(backend="gloo")
+    sc = make_custom_scene(300, 2, 16, 16, seed=23)
+    P, n = sc.params.shape
+    rng = np.random.default_rng(100 + rank)
+    g_local = rng.normal(size=(P, n))  # this rank's partial gradient
+    pr, (p0, p1) = D.plane_shard(P, rank, world)
+    gpad = torch.zeros((pr * world, n), dtype=torch.float64)
+    gpad[:P] = torch.from_numpy(g_local)
+    scratch = torch.empty((pr, n), dtype=torch.float64)
+    mine = D.reduce_scatter_planes_(gpad, scratch)
+    # reference gradient: the sum of every rank's partial
+    g_all = sum(np.random.default_rng(100 + r).normal(size=(P, n)) for r in range(world))
+    ok_rs = bool(np.allclose(mine.numpy()[:p1 - p0], g_all[p0:p1], rtol=1e-14, atol=1e-14))
+    hp = sghmc_params_for(sc, step=2, seed=9, eps_o=0.01, eps_sigma=0.01)
+    full, *_ = O.sghmc_step(sc.params, 2, g_all, np.zeros((P, n)), np.zeros((P, n)), np.zeros((3, n)), hp)
+    ppad = torch.zeros((pr * world, n), dtype=torch.float64)
+    ppad[:P] = torch.from_numpy(sc.params.astype(np.float64))
+    ppad[p0:p1] = torch.from_numpy(full[p0:p1])  # this rank's planes of the step
+    D.all_gather_planes_(ppad, scratch)
+    ok_ag = bool(np.array_equal(ppad[:P].numpy(), full))
+    out_q.put((rank, (p0, p1), ok_rs, ok_ag))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_plane_sharded_step(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spans = [r[1] for r in res]
+    assert spans[0][0] == 0 and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    for _, _, ok_rs, ok_ag in res:
+        assert ok_rs and ok_ag
+
+
+def test_plane_shard_partition():
+    from paper_2503_10148_b200 import dist as D
+
+    for P in (15, 24, 39, 60):
+        for R in (1, 2, 3, 4, 8):
+            spans = [D.plane_shard(P, r, R)[1] for r in range(R)]
+            covered = [p for a, b in spans for p in range(a, b)]
+            assert covered == list(range(P))

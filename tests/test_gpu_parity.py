@@ -383,3 +383,48 @@ def test_backward_tile_list_paths_agree(orc, sss, scenes):
             assert (fr.tile_count.cpu().numpy() > 4).any()  # the fallback is exercised
     assert rel_l2(grads[0], grads[2]) <= 1e-5
     assert rel_l2(grads[1], grads[2]) <= 1e-5
+
+
+def test_sghmc_plane_ranges_compose(sss):
+    """ZeRO-1 shards: updating plane ranges separately, each from the same
+    pre-update state, and assembling the owned planes equals the full step
+    bit for bit (parameters, moments, momentum)."""
+    import copy
+
+    import torch
+
+    from sss_synth import sghmc_params_for
+
+    sc = make_custom_scene(20000, 3, 32, 32, seed=33)
+    r, m, v = make_optimizer_state(sc, seed=7)
+    rng = np.random.default_rng(9)
+    grad = (rng.normal(size=sc.params.shape) * 1e-2).astype(np.float32)
+    sc.params[11] = np.arctanh(rng.uniform(-0.03, 0.03, sc.n)).astype(np.float32)
+    hp = _hp32(sghmc_params_for(sc, step=3, seed=4, noise=1e-4, eps_o=0.01, eps_sigma=0.02))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+
+    def run(p0, p1):
+        h = copy.copy(hp)
+        h.plane_begin, h.plane_end = p0, p1
+        ps, ms, vs, rs = sss.Params(dev(sc.params), 3), sss.Params(dev(m), 3), sss.Params(dev(v), 3), dev(r)
+        sss.sss_sghmc_step(ps, sss.Params(dev(grad), 3), ms, vs, rs, h)
+        torch.cuda.synchronize()
+        return ps.planes.cpu().numpy(), ms.planes.cpu().numpy(), vs.planes.cpu().numpy(), rs.cpu().numpy()
+
+    P = sc.params.shape[0]
+    full = run(0, 0)
+    for R in (2, 3, 8):
+        from paper_2503_10148_b200 import dist as D
+
+        out = [np.array(sc.params), np.array(m), np.array(v), np.array(r)]
+        for rank in range(R):
+            _, (p0, p1) = D.plane_shard(P, rank, R)
+            if p1 <= p0:
+                continue
+            part = run(p0, p1)
+            for k in range(3):
+                out[k][p0:p1] = part[k][p0:p1]
+            a0, a1 = min(p0, 3), min(p1, 3)
+            out[3][a0:a1] = part[3][a0:a1]
+        for k in range(4):
+            np.testing.assert_array_equal(out[k], full[k])
