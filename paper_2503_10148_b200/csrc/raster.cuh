@@ -26,8 +26,11 @@ constexpr int kLanesPerRow = kWarpW / kPX;
 #define SSS_FWD_MINB 20  // 48 registers: 40 warps per SM (measured: -7% vs 56 registers)
 #endif
 #ifndef SSS_BWD_MINB
-#define SSS_BWD_MINB 14  // 72 registers (measured: -1.3% vs 112; deferring the warp reduction
-                         // by one entry to overlap it with the next entry measured +9%)
+// bwd: <= 113 registers — no spills and the pixel coordinates stay in
+// registers (measured -5% vs 14 CTAs at 72 registers, where ptxas
+// rematerialises them every entry); deferring the warp reduction by one
+// entry to overlap it with the next entry measured +9%
+#define SSS_BWD_MINB 9
 #endif
 constexpr int kFwdMinBlocks = SSS_FWD_MINB;
 constexpr int kBwdMinBlocks = SSS_BWD_MINB;
