@@ -78,7 +78,7 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.vals_a = take(nv * 4);
   L.vals_b = take(nv * 4);
   L.n_vis = take((size_t)V * 4);
-  L.radix_hist = take((size_t)V * 256 * (size_t)L.tiles_per_view * 4);
+  L.radix_hist = take(radix_ws_words(L.tiles_per_view, V) * 4);
   L.chunk_hist = take((size_t)V * L.n_chunks * (size_t)g.n_bins * 4);
   L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
   L.bin_total = take((size_t)V * g.n_bins * 4);

@@ -63,7 +63,7 @@ RelocWs reloc_ws(int64_t n) {
   L.vals_a = take((size_t)L.cap * 4);
   L.keys_b = take((size_t)L.cap * 4);
   L.vals_b = take((size_t)L.cap * 4);
-  L.hist = take((size_t)256 * L.tiles * 4);
+  L.hist = take(radix_ws_words(L.tiles, 1) * 4);
   L.scal = take(64);                  // n_sel (int64), total (uint64)
   L.total = off;
   return L;
