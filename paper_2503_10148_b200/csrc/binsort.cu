@@ -161,15 +161,38 @@ __global__ void __launch_bounds__(256) chunk_hist_kernel(const int32_t* __restri
 }
 
 // per (view, bin): exclusive scan over chunks in place; bin totals
-__global__ void column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chunks, int n_bins,
-                                   uint32_t* __restrict__ bin_total) {
+// per (view, bin): exclusive scan over chunks in place; bin totals.  CTA =
+// 32 bins (lane = bin, coalesced rows) x 8 warps, each warp a contiguous
+// range of chunks: range sums, a prefix over warps, then the running write.
+__global__ void __launch_bounds__(256) column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chunks,
+                                                          int n_bins, uint32_t* __restrict__ bin_total) {
+  __shared__ uint32_t wsum[8][32];
   const int v = blockIdx.y;
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n_bins) return;
-  uint32_t* col = chunk_hist + (size_t)v * n_chunks * n_bins + b;
-  uint32_t run = 0;
-  int c = 0;
-  for (; c + 4 <= n_chunks; c += 4) {
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  const int b = blockIdx.x * 32 + lane;
+  const bool ok = b < n_bins;
+  const int per = (n_chunks + 7) / 8;
+  const int c0 = min(w * per, n_chunks), c1 = min(c0 + per, n_chunks);
+  uint32_t* col = chunk_hist + (size_t)v * n_chunks * n_bins + (ok ? b : 0);
+  uint32_t s = 0;
+  if (ok) {
+    int c = c0;
+    for (; c + 4 <= c1; c += 4)
+      s += col[(size_t)c * n_bins] + col[(size_t)(c + 1) * n_bins] + col[(size_t)(c + 2) * n_bins] +
+           col[(size_t)(c + 3) * n_bins];
+    for (; c < c1; ++c) s += col[(size_t)c * n_bins];
+  }
+  wsum[w][lane] = s;
+  __syncthreads();
+  uint32_t run = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    run += k < w ? wsum[k][lane] : 0u;
+    tot += wsum[k][lane];
+  }
+  if (!ok) return;
+  int c = c0;
+  for (; c + 4 <= c1; c += 4) {
     const uint32_t x0 = col[(size_t)(c + 0) * n_bins], x1 = col[(size_t)(c + 1) * n_bins];
     const uint32_t x2 = col[(size_t)(c + 2) * n_bins], x3 = col[(size_t)(c + 3) * n_bins];
     col[(size_t)(c + 0) * n_bins] = run; run += x0;
@@ -177,12 +200,12 @@ __global__ void column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chun
     col[(size_t)(c + 2) * n_bins] = run; run += x2;
     col[(size_t)(c + 3) * n_bins] = run; run += x3;
   }
-  for (; c < n_chunks; ++c) {
+  for (; c < c1; ++c) {
     const uint32_t x = col[(size_t)c * n_bins];
     col[(size_t)c * n_bins] = run;
     run += x;
   }
-  bin_total[(size_t)v * n_bins + b] = run;
+  if (w == 0) bin_total[(size_t)v * n_bins + b] = tot;
 }
 
 // per view: exclusive scan over bins -> bin_start, ranges, totals, overflow
@@ -416,7 +439,7 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     const dim3 gc(L.n_chunks, n_views);
     const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
     chunk_hist_kernel<<<gc, 256, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
-    column_scan_kernel<<<dim3(div_up(g.n_bins, 128), n_views), 128, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
+    column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 256, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
     count_launch(2);
   } else {
     cudaMemsetAsync(btot, 0, sizeof(uint32_t) * n_views * g.n_bins, s);
