@@ -112,6 +112,10 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
     }
     exm = mul2(lg, bc2(c.x - 1.f));
   }
+  if (!GENERAL) {  // an excluded pixel gets T = 0: every contribution and the replay step vanish
+    exm.x = inc0 ? exm.x : -INFINITY;
+    exm.y = inc1 ? exm.y : -INFINITY;
+  }
   const float2 Topt = make_float2(ex2_approx(exm.x), ex2_approx(exm.y));  // T / (1 + h/nu)
   const float2 T = mul2(Topt, opt);
   const float2 araw = mul2(T, bc2(b.z));
@@ -120,8 +124,7 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
     alpha.x = inc0 ? fminf(fmaxf(araw.x, -kAlphaMax), kAlphaMax) : 0.f;
     alpha.y = inc1 ? fminf(fmaxf(araw.y, -kAlphaMax), kAlphaMax) : 0.f;
   } else {
-    alpha.x = inc0 ? araw.x : 0.f;
-    alpha.y = inc1 ? araw.y : 0.f;
+    alpha = araw;  // 0 for excluded pixels (T = 0)
   }
   const float2 oma = sub2(bc2(1.f), alpha);  // 1 - a >= 0.01 (R10): no range fix-up
   const float2 Wi = mul2(p.W, make_float2(rcp_approx(oma.x), rcp_approx(oma.y)));
@@ -137,10 +140,7 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
   if (GENERAL) {  // R10: no gradient through the clamp
     da.x = (inc0 && fabsf(araw.x) <= kAlphaMax) ? da.x : 0.f;
     da.y = (inc1 && fabsf(araw.y) <= kAlphaMax) ? da.y : 0.f;
-  } else {
-    da.x = inc0 ? da.x : 0.f;
-    da.y = inc1 ? da.y : 0.f;
-  }
+  }  // (fast path: an excluded pixel's da multiplies T = 0 and Topt = 0 below)
   e.dO = fma2(da, T, e.dO);
   const float2 dT = mul2(da, bc2(b.z));
   const float2 dh = mul2(mul2(dT, bc2(einu)), Topt);
