@@ -20,7 +20,10 @@ namespace {
 
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixItems = 16;
+#ifndef SSS_RADIX_ITEMS
+#define SSS_RADIX_ITEMS 16
+#endif
+constexpr int kRadixItems = SSS_RADIX_ITEMS;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 keys per CTA
 constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStCount = (1u << 30) - 1u;
 
@@ -118,7 +121,10 @@ __global__ void __launch_bounds__(256) radix_digit_offsets_kernel(const uint32_t
 
 // One onesweep pass: stable scatter of one 4096-key tile by the digit at
 // 8 * pass (see the header).
-__global__ void __launch_bounds__(kRadixThreads, 3) radix_onesweep_kernel(
+#ifndef SSS_RADIX_MINB
+#define SSS_RADIX_MINB 5  // 5 CTAs/SM (measured -4% vs 3; the per-tile ranking is latency-bound)
+#endif
+__global__ void __launch_bounds__(kRadixThreads, SSS_RADIX_MINB) radix_onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in, int64_t n, int pass,
     int tiles, uint32_t* __restrict__ status, const uint32_t* __restrict__ goff,
     uint32_t* __restrict__ tickets, uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out) {
