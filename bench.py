@@ -32,8 +32,8 @@ METRIC = "fwd+bwd Mpixel/s and train iters/s at 1/2/4/8 B200; % of FP32/HBM roof
 
 # Algorithmic work per unit: FP32 lane-ops per composited
 # pair (forward / backward raster) and bytes per component-view (HBM kernels).
-FWD_OPS_PER_PAIR = 19
-BWD_OPS_PER_PAIR = 62
+FWD_OPS_PER_PAIR = 19  # DESIGN.md §5 derivation
+BWD_OPS_PER_PAIR = 58  # DESIGN.md §5 derivation
 
 
 def parse():
