@@ -30,8 +30,13 @@ class TrainStep:
         dev = planes.device
         world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
         # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
-        # to R * ceil(P / R) planes; the Params views cover the first P
-        self.shard = (world > 1) if shard_update is None else (bool(shard_update) and world > 1)
+        # to R * ceil(P / R) planes; the Params views cover the first P.
+        # shard_update=True forces it on any initialised group (tests run the
+        # NCCL path with one rank)
+        if shard_update is None:
+            self.shard = world > 1
+        else:
+            self.shard = bool(shard_update) and D.dist.is_initialized()
         P = planes.shape[0]
         self.world = world
         if self.shard:

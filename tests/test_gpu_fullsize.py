@@ -176,3 +176,43 @@ def test_trainstep_matches_the_abi_sequence(orc, sss):
                                     np.zeros((3, n)), hp)
     got = ts.params.planes.cpu().numpy().astype(np.float64)
     assert rel_l2(got[3:] - sc.params[3:], p_ref[3:] - sc.params[3:]) <= 5e-3
+
+
+def test_sharded_step_nccl_single_rank(orc, sss):
+    """The ZeRO-1 exchange (NCCL reduce-scatter of the padded gradient
+    planes, plane-range sampler step, NCCL all-gather) on a one-rank NCCL
+    group equals the replicated step (up to the order of the backward's
+    float atomics, which differs run to run) — exercising the collectives'
+    shapes and buffers on the GPU."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_10148_b200.step import TrainStep
+    from sss_synth import make_custom_scene, make_targets, sghmc_params_for
+    from test_gpu_parity import _hp32
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sc = make_custom_scene(3000, 1, 80, 64, n_views=2, seed=37, layout="blobs", nu_hi=16.0)
+        tg = torch.from_numpy(make_targets(sc)).cuda()
+        out = []
+        for shard in (False, True):
+            hp = _hp32(sghmc_params_for(sc, step=1, seed=3, noise=1e-4))
+            ts = TrainStep(torch.from_numpy(sc.params).cuda(), 1, sc.cameras, hp, bin_shift=1,
+                           views_per_batch=2, shard_update=shard)
+            assert ts.shard == shard
+            for _ in range(2):
+                ts.step(tg)
+            torch.cuda.synchronize()
+            out.append(ts.params.planes.cpu().numpy())
+        np.testing.assert_allclose(out[1], out[0], rtol=1e-6, atol=1e-7)
+    finally:
+        dist.destroy_process_group()
