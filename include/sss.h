@@ -52,6 +52,7 @@ typedef enum {
 #define SSS_MAX_BINS 5632    /* bins per view (tiles >> bin_shift); bounded by the scatter CTA's shared memory */
 #define SSS_REC_FLOATS 12    /* floats per projected record (48 B) */
 #define SSS_G2D_FLOATS 12    /* floats per screen-space gradient record (48 B) */
+#define SSS_TILE_LISTS 2     /* composited-entry lists per tile (one per 16x8 strip) */
 
 /* Pinhole camera (host struct).  p_cam = rot * x + trans (rot row-major,
  * world->camera; OpenCV axes x right, y down, z forward).  Pixel (i, j) has its
@@ -133,11 +134,12 @@ typedef struct {
  *                          does not read it)
  *  last      [V][H][W]     private: bin-list offset one past the last
  *                          composited entry (start of the backward replay)
- *  tile_list [V][tiles][tile_cap], tile_count [V][tiles]: private, nullable
- *            (both or neither): the bin-list offsets of the entries some
- *            pixel of the tile composited, in order; the backward replays
- *            only those (a tile with tile_count > tile_cap falls back to the
- *            full range) */
+ *  tile_list [V][tiles][SSS_TILE_LISTS][tile_cap],
+ *  tile_count [V][tiles][SSS_TILE_LISTS]: private, nullable (both or
+ *            neither): per 16x8 strip of a tile (rows 0-7, rows 8-15), the
+ *            bin-list offsets of the entries some pixel of the strip
+ *            composited, in order; the backward replays only those (a strip
+ *            with tile_count > tile_cap falls back to the full range) */
 typedef struct {
   float* rgb;
   float* final_T;

@@ -141,7 +141,7 @@ class Bins:
                           _ptr(self.overflow))
 
 
-TILE_CAP = 2048  # composited entries per tile the forward records for the backward
+TILE_CAP = 1536  # composited entries per 16x8 strip the forward records for the backward
 
 
 @dataclass
@@ -150,16 +150,16 @@ class Frame:
     final_T: torch.Tensor    # [V][H][W] f32
     n_contrib: Optional[torch.Tensor]  # [V][H][W] i32; None = not counted (diagnostic)
     last: torch.Tensor       # [V][H][W] i32
-    tile_list: Optional[torch.Tensor] = None   # private [V][tiles][cap] i32 (None: full replay)
-    tile_count: Optional[torch.Tensor] = None  # private [V][tiles] i32
+    tile_list: Optional[torch.Tensor] = None   # private [V][tiles][SSS_TILE_LISTS][cap] i32 (None: full replay)
+    tile_count: Optional[torch.Tensor] = None  # private [V][tiles][SSS_TILE_LISTS] i32
 
     @classmethod
     def empty(cls, V: int, H: int, W: int, device="cuda", tile_cap: int = TILE_CAP) -> "Frame":
         tiles = ((W + L.SSS_TILE - 1) // L.SSS_TILE) * ((H + L.SSS_TILE - 1) // L.SSS_TILE)
         tl = tc = None
         if tile_cap > 0:
-            tl = torch.empty((V, tiles, tile_cap), dtype=torch.int32, device=device)
-            tc = torch.empty((V, tiles), dtype=torch.int32, device=device)
+            tl = torch.empty((V, tiles, L.SSS_TILE_LISTS, tile_cap), dtype=torch.int32, device=device)
+            tc = torch.empty((V, tiles, L.SSS_TILE_LISTS), dtype=torch.int32, device=device)
         return cls(torch.empty((V, 3, H, W), dtype=torch.float32, device=device),
                    torch.empty((V, H, W), dtype=torch.float32, device=device),
                    torch.empty((V, H, W), dtype=torch.int32, device=device),

@@ -12,7 +12,7 @@ namespace sss {
 #define SSS_RASTER_PX 4
 #endif
 constexpr int kPX = SSS_RASTER_PX;
-static_assert(kPX == 2 || kPX == 4, "2 or 4 pixels per thread (processed as pairs)");
+static_assert(kPX == 4, "4 pixels per thread (processed as pairs): one warp per 16x8 strip");
 constexpr int kPairs = kPX / 2;
 constexpr int kRasterThreads = 256 / kPX;
 constexpr int kRasterWarps = kRasterThreads / 32;
@@ -35,6 +35,45 @@ constexpr int kLanesPerRow = kWarpW / kPX;
 constexpr int kFwdMinBlocks = SSS_FWD_MINB;
 constexpr int kBwdMinBlocks = SSS_BWD_MINB;
 constexpr int kWarpsPerRow = 16 / kWarpW;
+static_assert(kRasterWarps == SSS_TILE_LISTS, "one composited-entry list per warp strip");
+
+// Per-warp staging of the bin-list entries: batches of 32 entries, double
+// buffered, the 48-byte records gathered with cp.async (LDGSTS) one batch
+// ahead of the compute.
+constexpr int kWB = 32;
+struct WarpStage {
+  float4 r[2][3][kWB];  // [buffer][record float4][slot]
+  int32_t pos[2][kWB], id[2][kWB];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stages one batch: the lanes with `ok` are compacted in lane order (ballot)
+// into slots of buffer `buf`, their 48-byte records gathered by cp.async;
+// commits one async group (also when empty) and returns the entry count.
+__device__ __forceinline__ int stage_batch(WarpStage& S, int buf, bool ok, int32_t pos, int32_t id,
+                                           const float4* __restrict__ rv, unsigned lt) {
+  const unsigned bal = __ballot_sync(0xffffffffu, ok);
+  if (ok) {
+    const int slot = __popc(bal & lt);
+    const float4* src = rv + (int64_t)id * 3;
+    cp_async16(&S.r[buf][0][slot], src);
+    cp_async16(&S.r[buf][1][slot], src + 1);
+    cp_async16(&S.r[buf][2][slot], src + 2);
+    S.pos[buf][slot] = pos;
+    S.id[buf][slot] = id;
+  }
+  cp_async_commit();
+  return __popc(bal);
+}
+
+
 
 // Development counters (variant builds with -DSSS_COUNTERS only).
 #ifdef SSS_COUNTERS

@@ -3,9 +3,11 @@
 // (PAPER.md:165).
 //
 // a4 raster backward.  One CTA per tile and view, 64 threads with four
-// pixels each, replaying the tile's bin list back to front from the last
-// composited entry (the forward's `last`).  Per pair (PAPER.md:1230-1268
-// chain, R10, R13):
+// pixels each; each warp (a 16x8 strip) replays, back to front, the list of
+// entries its strip composited (the forward's per-strip list; or, if that
+// overflowed, the bin range below the strip's last composited entry) on its
+// own: no CTA barrier, records staged per warp by cp.async one 32-entry batch
+// ahead.  Per pair (PAPER.md:1230-1268 chain, R10, R13):
 //   W_i = W_{i+1} / (1 - a_i),  dL/dc = g a_i W_i,
 //   dL/da = W_i sum_k g_k (c_k - S_k),  S <- c a + (1 - a) S,
 //   dL/do = dL/da T,  dL/dT = dL/da o,
@@ -15,11 +17,8 @@
 // The replay keeps only W and the scalar g.S per pixel; a thread sums its
 // four pixels' contributions (the five geometry gradients from three row
 // sums), the warp reduces the 10 values with a butterfly reduce-scatter (12
-// shuffles instead of 50), warps whose pixels are all past their replay
-// start or all excluded skip the entry (warp-uniform), each warp stores its
-// partial sums in its own shared-memory slot (no shared atomics), and after
-// the batch one 3 x float4 RED per (component, tile) adds the warps' sums to
-// the screen-space gradient record g2d[v][i] (48 B) in the workspace.
+// shuffles instead of 50) and issues one RED (10 lanes, one 48-byte record)
+// into the screen-space gradient record g2d[v][i] in the workspace.
 //
 // a6: with target != NULL the L1 image gradient sign(C - target)/(3HW) is
 // formed in the same kernel (no image-gradient buffer) and the loss summed.
@@ -37,9 +36,9 @@ namespace sss {
 namespace {
 
 // 10-value butterfly reduce-scatter (12 shuffles): returns, in lane L, the
-// warp sum of value index idx (idx < 0: L holds nothing).  Both lanes of an
-// even/odd pair hold the same sum.
-__device__ __forceinline__ float warp_reduce10(const float* v, int lane, int& idx) {
+// warp sum of value index reduce10_index(L) (< 0: L holds nothing).  Both
+// lanes of an even/odd pair hold the same sum.
+__device__ __forceinline__ float warp_reduce10(const float* v, int lane) {
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
   float a[5];
 #pragma unroll
@@ -57,13 +56,14 @@ __device__ __forceinline__ float warp_reduce10(const float* v, int lane, int& id
   const float d1 = (b2 ? 0.f : c1) + __shfl_xor_sync(0xffffffffu, b2 ? c1 : 0.f, 4);
   // xor 2, xor 1
   const float e = (b1 ? d1 : d0) + __shfl_xor_sync(0xffffffffu, b1 ? d0 : d1, 2);
-  const int sub = b3 ? (b2 ? -1 : 3 + (b1 ? 1 : 0)) : (b2 ? (b1 ? -1 : 2) : (b1 ? 1 : 0));
-  idx = sub < 0 ? -1 : 5 * (b4 ? 1 : 0) + sub;
   return e + __shfl_xor_sync(0xffffffffu, e, 1);
 }
 
-constexpr int kAccPitch = kBatch + 1;  // conflict-free column writes
-constexpr size_t kAccBytes = (size_t)kRasterWarps * 10 * kAccPitch * sizeof(float);
+__device__ __forceinline__ int reduce10_index(int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  const int sub = b3 ? (b2 ? -1 : 3 + (b1 ? 1 : 0)) : (b2 ? (b1 ? -1 : 2) : (b1 ? 1 : 0));
+  return sub < 0 ? -1 : 5 * (b4 ? 1 : 0) + sub;
+}
 
 // Backward state of a horizontally adjacent pixel pair (packed FP32x2).
 // Only the scalar gS = g . S of the suffix colour S is needed:
@@ -162,12 +162,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
     float4* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
-  __shared__ int32_t spos[kBatch], sid[kBatch];
-  __shared__ int32_t wcnt[kRasterWarps];
-  __shared__ float wred[kRasterWarps];
-  __shared__ int32_t smax;
-  extern __shared__ float acc[];  // [warps][10][kAccPitch] per-warp partial sums, no atomics
+  __shared__ WarpStage stage[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
@@ -217,89 +212,79 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     }
     gS = fmaf(g0, bg0, fmaf(g1, bg1, g2 * bg2));  // S_n = bg (R12)
   }
-  // tile end = max over pixels of `last`; loss partial sums
+  // the warp's replay start = max over its pixels of `last`; loss partial sums
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (L1) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (loss_out && lane == 0) atomicAdd(loss_out, lsum * inv3P);
   }
-  const int32_t wlast = m;  // this warp's replay start (max over its pixels)
-  if (threadIdx.x == 0) smax = start;
-  __syncthreads();
-  if (lane == 0) {
-    atomicMax(&smax, m);
-    if (L1) wred[w] = lsum;
-  }
-  __syncthreads();
-  const int32_t end = smax;
-  if (threadIdx.x == 0) SSS_COUNT(7, end - start);
-  if (L1 && loss_out && threadIdx.x == 0) {
-    float s = 0.f;
-    for (int k = 0; k < kRasterWarps; ++k) s += wred[k];
-    atomicAdd(loss_out, s * inv3P);
-  }
+  const int32_t wlast = m;
+  if (lane == 0) SSS_COUNT(7, wlast - start);
 
   const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
-  float4* gv = g2d + (int64_t)v * G.n * 3;
-  float* myacc = acc + w * 10 * kAccPitch;
+  float* gvf = reinterpret_cast<float*>(g2d + (int64_t)v * G.n * 3);
+  WarpStage& S = stage[w];
+  const int ridx = reduce10_index(lane);
+  const bool writer = !(lane & 1) && ridx >= 0;
 
-  // the forward's list of the entries this tile composited (CTA-uniform
-  // choice): replay only those; else the whole [start, end) range
-  const int64_t tslot = (int64_t)v * G.tiles_x * G.tiles_y + tile;
-  const int32_t tcount = tile_list ? tile_count[tslot] : 0;
+  // The forward's list of the entries this warp's strip composited: replay
+  // only those; else (no lists, or this list overflowed) the whole
+  // [start, wlast) range.  Each warp walks its entries on its own (no CTA
+  // barrier): batches of 32 list indices from the top; lanes keep the
+  // entries before the warp's replay start (and, unlisted with bins, those
+  // whose rect covers the tile), compact them by ballot and gather their
+  // records into the next stage buffer.  Pipeline: positions two batches
+  // ahead, ids one batch ahead (registers), records one batch ahead
+  // (cp.async).
+  const int64_t lslot = ((int64_t)v * G.tiles_x * G.tiles_y + tile) * kRasterWarps + w;
+  const int32_t tcount = tile_list ? tile_count[lslot] : 0;
   const bool use_list = tile_list != nullptr && tcount <= tile_cap;
-  const int32_t* tl = use_list ? tile_list + tslot * tile_cap : nullptr;
+  const int32_t* tl = use_list ? tile_list + lslot * tile_cap : nullptr;
   const int32_t lbeg = use_list ? 0 : start;
-  const int32_t lend = use_list ? tcount : end;
-  for (int32_t hi = lend; hi > lbeg; hi -= kBatch) {
-    const int32_t lo = max(lbeg, hi - kBatch);
-    __syncthreads();  // previous batch fully consumed and flushed
-    if (threadIdx.x == 0) SSS_COUNT(0, 1);
-    const int32_t li = lo + (int32_t)threadIdx.x;
-    bool ok = (int)threadIdx.x < kBatch && li < hi;
-    const int32_t pos = ok ? (use_list ? tl[li] : li) : 0;
-    const int32_t id = ok ? idv[pos] : 0;
-    int slot, nb;
-    if (FILTER && !use_list) {
-      if (ok) {
-        const short4 r = rcv[id];
-        ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      if (lane == 0) wcnt[w] = __popc(bal);
-      __syncthreads();
-      int off = 0, tot = 0;
-#pragma unroll
-      for (int k = 0; k < kRasterWarps; ++k) {
-        const int c = wcnt[k];
-        off += k < w ? c : 0;
-        tot += c;
-      }
-      slot = off + __popc(bal & lt);
-      nb = tot;
-    } else {
-      slot = threadIdx.x;
-      nb = hi - lo;
+  const int32_t lend = use_list ? tcount : wlast;
+  auto pos_at = [&](int32_t h) -> int32_t {  // lane's entry of the batch [max(lbeg, h - 32), h)
+    const int32_t li = h - kWB + lane;
+    if (h <= lbeg || li < lbeg) return INT32_MAX;
+    return use_list ? __ldg(tl + li) : li;
+  };
+  auto id_at = [&](int32_t p) -> int32_t { return p < wlast ? __ldg(idv + p) : -1; };
+  auto issue = [&](int buf, int32_t p, int32_t id) -> int {
+    bool ok = id >= 0;
+    if (FILTER && !use_list && ok) {
+      const short4 r = rcv[id];
+      ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
     }
-    if (ok) {
-      spos[slot] = pos;
-      sid[slot] = id;
-      sa[slot] = rv[(int64_t)id * 3 + 0];
-      sb[slot] = rv[(int64_t)id * 3 + 1];
-      sc[slot] = rv[(int64_t)id * 3 + 2];
-    }
-    for (int k = threadIdx.x; k < kRasterWarps * 10 * kAccPitch; k += kRasterThreads) acc[k] = 0.f;
-    __syncthreads();
-    if (threadIdx.x == 0) SSS_COUNT(6, nb);
+    return stage_batch(S, buf, ok, p, id, rv, lt);
+  };
+
+  int32_t hi = lend;
+  int nb = 0;
+  int32_t p2, i2, p3;
+  {
+    const int32_t p1 = pos_at(hi);
+    nb = issue(0, p1, id_at(p1));
+    p2 = pos_at(hi - kWB);
+    i2 = id_at(p2);
+    p3 = pos_at(hi - 2 * kWB);
+  }
+  int buf = 0;
+  for (; hi > lbeg; hi -= kWB) {
+    const int nb_next = hi - kWB > lbeg ? issue(buf ^ 1, p2, i2) : (cp_async_commit(), 0);
+    i2 = id_at(p3);
+    p2 = p3;
+    p3 = pos_at(hi - 3 * kWB);
+    cp_async_wait1();  // this batch's records have landed
+    __syncwarp();
+    if (lane == 0) { SSS_COUNT(0, 1); SSS_COUNT(6, nb); }
     for (int j = nb - 1; j >= 0; --j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      const int32_t pj = spos[j];
-      if (pj >= wlast) continue;  // warp-uniform: past every pixel's replay start
-      const float4 a = sa[j];
-      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
+      const int32_t pj = S.pos[buf][j];
+      const float4 a = S.r[buf][0][j];
+      const float4 b = S.r[buf][1][j];  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
@@ -325,7 +310,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       }
 #endif
       if (!__any_sync(0xffffffffu, any)) continue;
-      const float4 c = sc[j];  // {e, r, g, b}
+      const float4 c = S.r[buf][2][j];  // {e, r, g, b}
       // e / nu = -(nu+2)/(2 nu): dT/dh = einu T/(1 + h/nu); -1/2 for the Gaussian variant
       const float einu = b.w == 0.f ? -0.5f : c.x * b.w;
       const float2 z2 = bc2(0.f);
@@ -352,30 +337,14 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       vals[7] = e2.dc2.x + e2.dc2.y;
       vals[8] = e2.dO.x + e2.dO.y;
       vals[9] = e2.dnu.x + e2.dnu.y;
-      int idx;
-      const float r = warp_reduce10(vals, lane, idx);
-      if (!(lane & 1) && idx >= 0) myacc[idx * kAccPitch + j] = r;
+      const float r = warp_reduce10(vals, lane);
+      // one RED per warp and entry: lanes 0, 2, .. hold the 10 sums of the
+      // 48-byte screen-space gradient record g2d[v][id]
+      if (writer && r != 0.f) atomicAdd(gvf + (int64_t)S.id[buf][j] * 12 + ridx, r);
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < nb; k += kRasterThreads) {
-      float s[10];
-#pragma unroll
-      for (int qq = 0; qq < 10; ++qq) {
-        float t = 0.f;
-#pragma unroll
-        for (int ww = 0; ww < kRasterWarps; ++ww) t += acc[(ww * 10 + qq) * kAccPitch + k];
-        s[qq] = t;
-      }
-      bool nz = false;
-#pragma unroll
-      for (int qq = 0; qq < 10; ++qq) nz |= s[qq] != 0.f;
-      if (nz) {
-        float4* dst = gv + (int64_t)sid[k] * 3;
-        atomicAdd(dst + 0, make_float4(s[0], s[1], s[2], s[3]));
-        atomicAdd(dst + 1, make_float4(s[4], s[5], s[6], s[7]));
-        atomicAdd(dst + 2, make_float4(s[8], s[9], 0.f, 0.f));
-      }
-    }
+    __syncwarp();  // this buffer is refilled two batches on
+    nb = nb_next;
+    buf ^= 1;
   }
 }
 
@@ -684,7 +653,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   const float4* rec = (const float4*)pr->rec;
   const short4* rect = (const short4*)pr->rect;
 #define SSS_BWD_LAUNCH(F, L, N)                                                                     \
-  render_bwd_kernel<F, L, N><<<grid, kRasterThreads, kAccBytes, s>>>(                              \
+  render_bwd_kernel<F, L, N><<<grid, kRasterThreads, 0, s>>>(                              \
       rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last, \
       d_rgb, target, loss_out, g2d, fwd->tile_list, fwd->tile_count, fwd->tile_cap)
 #define SSS_BWD_LAUNCH_N(F, L)              \

@@ -14,9 +14,12 @@
 // component that drives W below 1e-4 (R11); a warp leaves the batch when all
 // its pixels stopped, the CTA when no pixel is live.  The hot loop is
 // FP32-issue bound (~8 ops per h test, ~17 more + 2 MUFU per composited
-// pair).  (Measured and rejected: per-warp bounding-box or exact ellipse-
-// strip culling — the warps of a tile then drift apart at the batch barrier —
-// and register prefetching of the next batch.)
+// pair).  Each warp records the entries its 16x8 strip composited (bit masks
+// per batch, appended in order) for the backward's replay.  (Measured and
+// rejected: per-warp bounding-box or exact ellipse-strip culling — the warps
+// of a tile then drift apart at the batch barrier — register prefetching of
+// the next batch, and per-warp batches staged by cp.async without the CTA
+// barrier, +5%: each warp then gathers every record itself.)
 #include "raster.cuh"
 
 namespace sss {
@@ -75,11 +78,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int32_t tile_cap) {
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
-  // REC: per batch, the entries each warp composited; double-buffered with
-  // spos so the append of batch k runs after the top barrier of batch k+1
-  // without a barrier of its own
-  __shared__ unsigned wmask2[2][kRasterWarps][kBatch / 32];
-  __shared__ int32_t spos2[2][kBatch];
+  __shared__ int32_t spos[kBatch];
   __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
@@ -120,39 +119,17 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     for (int k = 0; k < kPX; ++k) d = d && !(lane_of(p[k >> 1].W, k) >= kWStop);
     return d;
   };
-  int32_t n_rec = 0;  // REC: entries of this tile composited by some warp so far
-  int32_t* tl = REC ? tile_list + ((int64_t)v * G.tiles_x * G.tiles_y + tile) * tile_cap : nullptr;
-  // append the entries of buffer `pb` composited by any warp, in list order
-  auto append = [&](int pb) {
-    unsigned u[kBatch / 32];
-#pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) {
-      u[q] = 0u;
-#pragma unroll
-      for (int ww = 0; ww < kRasterWarps; ++ww) u[q] |= wmask2[pb][ww][q];
-    }
-    int off = 0, tot = 0;
-#pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) {
-      off += q < w ? __popc(u[q]) : 0;
-      tot += __popc(u[q]);
-    }
-    const int slot = n_rec + off + __popc(u[w] & lt);
-    if (((u[w] >> lane) & 1u) && slot < tile_cap) tl[slot] = spos2[pb][threadIdx.x];
-    n_rec += tot;
-  };
-  int pb = 0;  // buffer of the current batch
-  bool pending = false;
-  for (int32_t b0 = start; b0 < end; b0 += kBatch, pb ^= 1) {
-    const int live = __syncthreads_count(!all_done());
-    if (REC && pending) append(pb ^ 1);
-    if (live == 0) { pending = false; break; }
+  // REC: this warp's list of the entries some pixel of its 16x8 strip
+  // composited, appended after each batch from warp-uniform bit masks
+  const int64_t lslot = ((int64_t)v * G.tiles_x * G.tiles_y + tile) * kRasterWarps + w;
+  int32_t* tl = REC ? tile_list + lslot * tile_cap : nullptr;
+  int32_t n_rec = 0;
+  for (int32_t b0 = start; b0 < end; b0 += kBatch) {
+    if (__syncthreads_count(!all_done()) == 0) break;
     if (threadIdx.x == 0) SSS_COUNT(0, 1);
-    pending = true;
     unsigned cm[kBatch / 32];  // REC: this warp's composited entries (warp-uniform bits)
 #pragma unroll
     for (int q = 0; q < kBatch / 32; ++q) cm[q] = 0u;
-    int32_t (&spos)[kBatch] = spos2[pb];
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? idv[pos] : 0;
@@ -238,17 +215,16 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
     }
-    if (REC && lane < kBatch / 32) {
+    if (REC) {  // spos is rewritten only after the next top barrier
 #pragma unroll
-      for (int q = 0; q < kBatch / 32; ++q)
-        if (q == lane) wmask2[pb][w][q] = cm[q];
+      for (int q = 0; q < kBatch / 32; ++q) {
+        const int slot = n_rec + __popc(cm[q] & lt);
+        if (((cm[q] >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
+        n_rec += __popc(cm[q]);
+      }
     }
   }
-  if (REC && pending) {
-    __syncthreads();
-    append(pb ^ 1);
-  }
-  if (REC && threadIdx.x == 0) tile_count[(int64_t)v * G.tiles_x * G.tiles_y + tile] = n_rec;
+  if (REC && lane == 0) tile_count[lslot] = n_rec;
   const int64_t HW = (int64_t)G.width * G.height;
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {

@@ -343,11 +343,11 @@ def test_render_fwd_without_count_is_identical(sss, scenes):
 
 
 def test_backward_tile_list_paths_agree(orc, sss, scenes):
-    """The backward replays the forward's per-tile list of composited entries;
-    a tile whose list overflowed (tiny cap) and a frame without lists replay
-    the full range.  All three give the same gradients (up to the order of
-    the float atomics) and the list holds exactly the entries some pixel of
-    the tile composited."""
+    """The backward replays the forward's per-strip lists of composited
+    entries (one per 16x8 half tile); a strip whose list overflowed (tiny cap)
+    and a frame without lists replay the full range.  All three give the same
+    gradients (up to the order of the float atomics) and a list holds exactly
+    the entries some pixel of its strip composited."""
     import torch
 
     from gpu_helpers import to_dev
@@ -375,10 +375,16 @@ def test_backward_tile_list_paths_agree(orc, sss, scenes):
             # full-range parity tests check; here: lists are increasing and
             # inside the bin ranges
             tl = fr.tile_list.cpu().numpy()
+            assert tc.shape == (V, tl.shape[1], sss._lib.SSS_TILE_LISTS)
+            last = fr.last.cpu().numpy()
+            tiles_x = (cam.width + 15) // 16
             for v in range(V):
-                for t in np.flatnonzero(tc[v] > 1)[:50]:
-                    seq = tl[v, t, :tc[v, t]]
+                for t, s in zip(*np.nonzero(tc[v] > 1)):
+                    seq = tl[v, t, s, :tc[v, t, s]]
                     assert np.all(np.diff(seq) > 0)
+                    # the strip's last listed entry is its pixels' last composited one
+                    y0, x0 = (t // tiles_x) * 16 + 8 * s, (t % tiles_x) * 16
+                    assert seq[-1] + 1 == last[v, y0:y0 + 8, x0:x0 + 16].max()
         if cap == 4:
             assert (fr.tile_count.cpu().numpy() > 4).any()  # the fallback is exercised
     assert rel_l2(grads[0], grads[2]) <= 1e-5
