@@ -14,11 +14,13 @@
 //   2. a stable counting scatter of the instances by bin, generated on the fly
 //      from the depth-sorted components: per-chunk bin histograms (shared
 //      memory), a column scan over chunks, a scan over bins, then a scatter in
-//      which each lane of a warp owns one component and walks its bin rect;
-//      the slot of (lane, bin) is the warp's running count plus the number of
-//      lower lanes covering the bin — a popcount of per-column and per-row
-//      lane ballots — so bins receive their entries in depth order without
-//      ever materialising 64-bit keys or serialising lanes.
+//      which a warp flattens the bin rects of 32 components into instances
+//      and writes 32 of them per step (balanced whatever the rect sizes); the
+//      slot of (component, bin) is the warp's running count plus the number
+//      of lower components covering the bin — a popcount of per-column and
+//      per-row ballots — so bins receive their entries in depth order without
+//      ever materialising 64-bit keys or serialising lanes.  A chunk's ids
+//      are staged in shared memory and stored bin run by bin run.
 // Every instance is written exactly once (4 B id, +8 B key if requested); the
 // radix passes touch only N keys per view.  All views are processed by the
 // same launches (grid.y = view).
@@ -57,6 +59,10 @@ inline BinGeom bin_geom(const sss_camera& c, int shift) {
 #endif
 constexpr int kChunk = SSS_CHUNK;  // depth-sorted components per histogram / scatter CTA
 constexpr size_t kScatterSmemMax = 225 * 1024;  // dynamic shared memory of a scatter CTA
+#ifndef SSS_SCATTER_STAGE_MAX
+#define SSS_SCATTER_STAGE_MAX 16384
+#endif
+constexpr int64_t kScatterStageMax = SSS_SCATTER_STAGE_MAX;  // staged ids per chunk (64 KB)
 
 struct WsLayout {
   size_t keys_a, keys_b, vals_a, vals_b, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start, total;
@@ -247,27 +253,49 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   }
 }
 
-// Walks the warp's depth-sorted components [wlo, whi), 32 at a time, one
-// component per lane; each lane loops over the bins of its component's bin
-// rect (row-major).
-//   The slot of (lane i, bin b) is cnt[b] + the number of lanes
-//   i' < i whose component also covers b.  The lanes covering b are
-//   colmask[bx] & rowmask[by] (one ballot per bin column and row), so the
-//   rank is a popcount and no lane order has to be serialised; the first
-//   lane covering b then advances cnt[b] by the number of covering lanes.
-//   The (depth, index) order within every bin follows.  The id is written
-//   straight to its global slot gofs[b] + slot (4-byte stores that L2
-//   merges; staging the chunk in shared memory for coalesced runs measured
-//   slower — it costs occupancy).
+// Per-warp scratch of the scatter walk (shared memory).
+struct alignas(16) WalkRec {  // one of the step's (compacted) components
+  int32_t excl;               // first instance index of the component in the step
+  int32_t id;
+  uint32_t packed;            // bx0 | by0 << 10 | (width - 1) << 20 (bins)
+  float inv_w;                // 1 / width, correctly rounded
+};
+struct alignas(16) WalkScratch {
+  WalkRec rec[32];
+  int4 stage[32];     // {bx0 | by0 << 16, bx1 | by1 << 16, id, depth bits}
+  uint32_t dbits[32];
+};
+
+// Walks the warp's depth-sorted components [wlo, whi), 32 at a time.  The
+// step's components with a non-empty bin rect are compacted to ranks
+// 0..K-1 (order kept) and their K rects flattened into T instances (rank-
+// major, row-major in each rect); the lanes then take 32 consecutive
+// instances at a time, so every lane writes one id per iteration whatever
+// the rect sizes (a lane per component would idle while the warp's largest
+// rect finishes).
+//   Instance t belongs to the rank whose first index excl is the last one
+//   <= t: a bit mask of the rank starts inside the 32-instance window
+//   (one OR-reduction) and a popcount give it.  Its bin comes from the
+//   rank's rect (division by the rect width through a correctly rounded
+//   reciprocal: exact for k < 2^20).
+//   The slot of (rank r, bin b) is wbase[b] + the number of lower ranks
+//   covering b — a popcount of per-column and per-row rank ballots — so
+//   bins receive their entries in depth order without 64-bit keys or
+//   serialised lanes; the highest covering rank then advances wbase[b]
+//   (every lower rank's instance of b lies earlier in the window order).
+//   STAGED: the slots are chunk-local and the ids land in shared memory, from
+//   where the CTA writes every bin's run of the chunk with coalesced stores;
+//   otherwise (keys requested, or a chunk larger than the stage) the id goes
+//   straight to its global slot.
+template <bool STAGED>
 __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
                                           const float* __restrict__ dv, int64_t wlo, int64_t whi,
-                                          const BinGeom& g, uint32_t* cnt, uint32_t* colmask,
-                                          uint32_t* rowmask, const uint32_t* gofs,
-                                          int32_t* __restrict__ idv, uint64_t* __restrict__ kv) {
+                                          const BinGeom& g, uint32_t* wbase, uint32_t* colmask,
+                                          uint32_t* rowmask, WalkScratch& S, int32_t* __restrict__ dst,
+                                          uint64_t* __restrict__ kv) {
   const int lane = lane_id();
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  const int by_max = g.bins_y - 1, bx_max = g.bins_x - 1;
   int id_n = 0;
   short4 r_n = make_short4(1, 1, 0, 0);
   if (wlo + lane < whi) {
@@ -275,47 +303,90 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
     r_n = rv[id_n];
   }
   for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
-    const int id = id_n;
+    const int id0 = id_n;
+    const short4 r0 = r_n;
     const bool valid = j0 + lane < whi;
-    const short4 r = r_n;
     if (j0 + 32 + lane < whi) {  // prefetch the next 32 components
       id_n = sid[j0 + 32 + lane];
       r_n = rv[id_n];
     }
-    int bx0 = r.x >> g.shift, by0 = r.y >> g.shift;
-    int bx1 = r.z >> g.shift, by1 = r.w >> g.shift;
-    if (!valid) { bx0 = by0 = 1; bx1 = by1 = 0; }  // empty
     {
-    // covering lanes per bin column / row
-    for (int x = 0; x <= bx_max; ++x) {
-      const unsigned m = __ballot_sync(full, bx0 <= x && x <= bx1);
-      if (lane == 0) colmask[x] = m;
-    }
-    for (int y = 0; y <= by_max; ++y) {
-      const unsigned m = __ballot_sync(full, by0 <= y && y <= by1);
-      if (lane == 0) rowmask[y] = m;
-    }
-    __syncwarp();
-    uint32_t dbits = 0;
-    if (kv && valid) dbits = __float_as_uint(dv[id]);
-    for (int by = by0; by <= by1; ++by) {
-      const unsigned rm = rowmask[by];
-      for (int bx = bx0; bx <= bx1; ++bx) {
-        const int b = by * g.bins_x + bx;
-        const uint32_t pos = gofs[b] + cnt[b] + __popc(colmask[bx] & rm & lt);
-        idv[pos] = id;
-        if (kv) kv[pos] = ((uint64_t)b << 32) | dbits;
+      const int bx0 = r0.x >> g.shift, by0 = r0.y >> g.shift;
+      const int bx1 = r0.z >> g.shift, by1 = r0.w >> g.shift;
+      const bool ne = valid && bx0 <= bx1 && by0 <= by1;
+      const unsigned NE = __ballot_sync(full, ne);
+      if (ne)
+        S.stage[__popc(NE & lt)] = make_int4(bx0 | (by0 << 16), bx1 | (by1 << 16), id0,
+                                             kv ? (int)__float_as_uint(dv[id0]) : 0);
+      __syncwarp();
+      const bool act = lane < __popc(NE);
+      int cbx0 = 1, cby0 = 1, cbx1 = 0, cby1 = 0, n_i = 0;
+      if (act) {
+        const int4 st = S.stage[lane];
+        cbx0 = st.x & 0xffff; cby0 = st.x >> 16; cbx1 = st.y & 0xffff; cby1 = st.y >> 16;
+        const int wd = cbx1 - cbx0 + 1;
+        n_i = wd * (cby1 - cby0 + 1);
+        WalkRec rr;
+        rr.id = st.z;
+        rr.packed = (uint32_t)cbx0 | ((uint32_t)cby0 << 10) | ((uint32_t)(wd - 1) << 20);
+        rr.inv_w = __frcp_rn((float)wd);
+        S.rec[lane] = rr;  // excl below
+        if (kv) S.dbits[lane] = (uint32_t)st.w;
       }
-    }
-    __syncwarp();
-    for (int by = by0; by <= by1; ++by) {
-      const unsigned rm = rowmask[by];
-      for (int bx = bx0; bx <= bx1; ++bx) {
-        const unsigned m = colmask[bx] & rm;
-        if ((m & lt) == 0) cnt[by * g.bins_x + bx] += __popc(m);
+      int incl = n_i;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += t;
       }
-    }
-    __syncwarp();
+      const int T = __shfl_sync(full, incl, 31);
+      const int excl = incl - n_i;
+      if (act) S.rec[lane].excl = excl;
+      // covering ranks per bin column / row, over the step's union rect
+      const int ux0 = (int)__reduce_min_sync(full, act ? (unsigned)cbx0 : 0xffffu);
+      const int ux1 = (int)__reduce_max_sync(full, act ? (unsigned)cbx1 : 0u);
+      const int uy0 = (int)__reduce_min_sync(full, act ? (unsigned)cby0 : 0xffffu);
+      const int uy1 = (int)__reduce_max_sync(full, act ? (unsigned)cby1 : 0u);
+      for (int x = ux0; x <= ux1; ++x) {
+        const unsigned m = __ballot_sync(full, cbx0 <= x && x <= cbx1);
+        if (lane == 0) colmask[x] = m;
+      }
+      for (int y = uy0; y <= uy1; ++y) {
+        const unsigned m = __ballot_sync(full, cby0 <= y && y <= cby1);
+        if (lane == 0) rowmask[y] = m;
+      }
+      __syncwarp();
+      int base = 0;  // ranks starting before the window
+      for (int t0 = 0; t0 < T; t0 += 32) {
+        const unsigned bit = (act && excl >= t0 && excl < t0 + 32) ? 1u << (excl - t0) : 0u;
+        const unsigned B = __reduce_or_sync(full, bit);
+        const int own = base + __popc(B & ((2u << lane) - 1u)) - 1;
+        base += __popc(B);
+        const int t = t0 + lane;
+        int upd_b = -1;
+        uint32_t upd_v = 0;
+        if (t < T) {
+          const WalkRec R = S.rec[own];
+          const int k = t - R.excl;
+          const int q = (int)(((float)k + 0.5f) * R.inv_w);
+          const int wd = (int)(R.packed >> 20) + 1;
+          const int bx = (int)(R.packed & 1023u) + (k - q * wd);
+          const int by = (int)((R.packed >> 10) & 1023u) + q;
+          const int b = by * g.bins_x + bx;
+          const unsigned m = colmask[bx] & rowmask[by];
+          const uint32_t w0 = wbase[b];
+          const uint32_t pos = w0 + __popc(m & ((1u << own) - 1u));
+          dst[pos] = R.id;
+          if (!STAGED && kv) kv[pos] = ((uint64_t)b << 32) | S.dbits[own];
+          if (((m >> own) >> 1) == 0u) {  // highest covering rank: advance the bin
+            upd_b = b;
+            upd_v = w0 + __popc(m);
+          }
+        }
+        __syncwarp();
+        if (upd_b >= 0) wbase[upd_b] = upd_v;
+        __syncwarp();
+      }
     }
   }
 }
@@ -323,41 +394,79 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
 // stable scatter: CTA per (chunk of kChunk depth-sorted components, view);
 // warp w owns kChunk/8 consecutive components.  The per-(warp, bin) counts of
 // chunk_hist_kernel, prefix-summed over warps, give each warp's first slot in
-// the chunk's segment of every bin; the warps then write their ids.
+// the chunk's run of every bin.  The chunk's runs are laid out back to back
+// in shared memory (an exclusive scan of the chunk's bin counts), the warps
+// write their ids there, and the CTA then stores each run to its global
+// segment bs[b] + ch[b] with consecutive lanes on consecutive slots (a
+// 4-byte store per instance scattered over the bins' segments leaves
+// partial sectors that L2 has to merge or read-modify-write).
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
     const uint32_t* __restrict__ chunk_hist, const uint8_t* __restrict__ warp_hist,
     const uint32_t* __restrict__ bin_start, const int64_t* __restrict__ totals, int64_t capacity,
-    int32_t* __restrict__ ids, uint64_t* __restrict__ keys) {
-  extern __shared__ uint32_t sm[];
+    int stage_cap, int32_t* __restrict__ ids, uint64_t* __restrict__ keys) {
+  extern __shared__ uint4 sm4[];
+  __shared__ uint32_t red[kScatterWarps];
   const int v = blockIdx.y, c = blockIdx.x;
   if (totals[v] > capacity) return;
   const int64_t lo = (int64_t)c * kChunk;
   const int64_t nvis = n_vis[v];
   if (lo >= nvis) return;
   const int nb = g.n_bins;
-  uint32_t* cnt = sm;                                  // [8][n_bins] per-warp counters / slots
-  uint32_t* gofs = cnt + (size_t)kScatterWarps * nb;  // [n_bins] the chunk's first slot per bin
-  uint32_t* masks = gofs + nb;                         // [8][bins_x + bins_y] lane masks
+  WalkScratch* scratch = reinterpret_cast<WalkScratch*>(sm4);             // [8]
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(scratch + kScatterWarps);  // [8][n_bins] next slot per bin
+  uint32_t* masks = wbase + (size_t)kScatterWarps * nb;                    // [8][bins_x + bins_y] rank masks
+  uint32_t* soff = masks + kScatterWarps * (g.bins_x + g.bins_y);          // [n_bins + 1] run starts (stage)
+  uint32_t* gst = soff + nb + 1;                                           // [n_bins] run starts (global)
+  int32_t* sids = reinterpret_cast<int32_t*>(gst + nb);                   // [stage_cap] staged ids
   const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
   const uint8_t* wh = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
   const uint32_t* bs = bin_start + (size_t)v * nb;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    gofs[b] = bs[b] + ch[b];
-    uint32_t acc = 0;  // exclusive prefix of the per-warp counts (chunk_hist_kernel)
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  // the chunk's bin counts, scanned over bins: thread t owns bins [b0, b1)
+  const int per = (nb + kScatterThreads - 1) / kScatterThreads;
+  const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
+  uint32_t mine = 0;
+  for (int b = b0; b < b1; ++b) {
+    uint32_t cb = 0;
+#pragma unroll
+    for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
+    mine += cb;
+  }
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) red[w] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, total = 0;
+#pragma unroll
+  for (int ww = 0; ww < kScatterWarps; ++ww) {
+    wpre += ww < w ? red[ww] : 0u;
+    total += red[ww];
+  }
+  const bool staged = keys == nullptr && total <= (uint32_t)stage_cap;  // CTA-uniform
+  uint32_t run = wpre + incl - mine;
+  for (int b = b0; b < b1; ++b) {
+    const uint32_t gb = bs[b] + ch[b];
+    soff[b] = run;
+    gst[b] = gb;
+    uint32_t acc = staged ? run : gb;  // + exclusive prefix of the per-warp counts
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
-      cnt[(size_t)ww * nb + b] = acc;
+      wbase[(size_t)ww * nb + b] = acc;
       acc += wh[(size_t)ww * nb + b];
     }
+    run += acc - (staged ? run : gb);
   }
+  if (threadIdx.x == 0) soff[nb] = total;
   __syncthreads();
-  const int w = threadIdx.x >> 5;
   constexpr int per_warp = kChunk / kScatterWarps;
   const int64_t wlo = lo + (int64_t)w * per_warp;
   const int64_t whi = min(wlo + per_warp, nvis);
-  uint32_t* my = cnt + (size_t)w * nb;
   uint32_t* colmask = masks + w * (g.bins_x + g.bins_y);
   uint32_t* rowmask = colmask + g.bins_x;
   const int32_t* sid = sorted_ids + (int64_t)v * n;
@@ -365,7 +474,17 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  warp_walk(sid, rv, dv, wlo, whi, g, my, colmask, rowmask, gofs, idv, kv);
+  if (!staged) {
+    warp_walk<false>(sid, rv, dv, wlo, whi, g, wbase + (size_t)w * nb, colmask, rowmask, scratch[w], idv, kv);
+    return;
+  }
+  warp_walk<true>(sid, rv, dv, wlo, whi, g, wbase + (size_t)w * nb, colmask, rowmask, scratch[w], sids, nullptr);
+  __syncthreads();
+  for (int b = w; b < nb; b += kScatterWarps) {  // one bin's run per warp, consecutive lanes
+    const uint32_t s0 = soff[b], cnt = soff[b + 1] - s0;
+    int32_t* out = idv + gst[b];
+    for (uint32_t i = lane; i < cnt; i += 32) out[i] = sids[s0 + i];
+  }
 }
 
 }  // namespace
@@ -392,8 +511,9 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   }
   if (out->bin_shift < 0 || out->bin_shift > 6) { set_error("sss_bin_sort: bin_shift outside [0,6]"); return SSS_ERR_ARG; }
   const BinGeom g = bin_geom(cams[0], out->bin_shift);
-  if (g.n_bins > SSS_MAX_BINS) {
-    set_error("sss_bin_sort: %d bins > SSS_MAX_BINS (%d); raise bin_shift", g.n_bins, SSS_MAX_BINS);
+  if (g.n_bins > SSS_MAX_BINS || g.bins_x > 1024 || g.bins_y > 1024) {
+    set_error("sss_bin_sort: %d x %d bins: need <= SSS_MAX_BINS (%d) and <= 1024 per axis; raise bin_shift",
+              g.bins_x, g.bins_y, SSS_MAX_BINS);
     return SSS_ERR_SHAPE;
   }
   const int64_t n = pr->n;
@@ -448,10 +568,20 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
                                             out->overflow);
   count_launch();
   if (n > 0) {
-    const size_t ssm = ((size_t)(kScatterWarps + 1) * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y)) * 4;
+    // stage: the chunk's mean share of the capacity (the caller sizes the
+    // capacity with headroom over the measured instance count), within the
+    // shared memory left; larger chunks take the direct path
+    const size_t fixed = sizeof(WalkScratch) * kScatterWarps +
+                         ((size_t)kScatterWarps * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y) +
+                          2 * (size_t)g.n_bins + 1) * 4;
+    int64_t want = (out->capacity + L.n_chunks - 1) / L.n_chunks;
+    want = std::min<int64_t>(std::max<int64_t>(want, 256), kScatterStageMax);
+    const int64_t room = ((int64_t)kScatterSmemMax - (int64_t)fixed) / 4;
+    const int stage_cap = (int)std::max<int64_t>(0, std::min<int64_t>((want + 31) & ~31, room));
+    const size_t ssm = fixed + (size_t)stage_cap * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
         vals_a, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, out->totals, out->capacity,
-        out->ids, out->keys);
+        stage_cap, out->ids, out->keys);
     count_launch();
   }
   return check_launch("sss_bin_sort");

@@ -89,6 +89,38 @@ def test_bin_sort_parity_bit_exact(orc, sss, scenes):
             assert np.array_equal(gk, keys), name
 
 
+@pytest.mark.parametrize("shift", [0, 2])
+def test_scatter_staged_and_direct_paths_agree(orc, sss, shift):
+    """The scatter stages a chunk's ids in shared memory when the chunk fits
+    the stage (sized from capacity / chunks) and writes straight to the bin
+    lists otherwise (or when keys are requested).  Capacity = the exact total
+    mixes both paths in one launch (chunks above the mean go direct); a large
+    capacity stages every chunk; keys=True goes direct everywhere.  All three
+    give the same lists, and at bin_shift 0 the oracle's."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    sc = make_custom_scene(9000, 1, 160, 96, seed=41, log_scale_mean=-2.2)
+    cam = sc.cameras
+    params = to_dev(sc)
+    pr = sss.sss_project(params, cam)
+    ref = sss.sss_bin_sort(pr, cam, bin_shift=shift, keys=True)
+    M = int(ref.totals[0].item())
+    assert M > 9000  # nine chunks of 1024 depth-sorted components
+    runs = [sss.sss_bin_sort(pr, cam, bin_shift=shift, capacity=M),
+            sss.sss_bin_sort(pr, cam, bin_shift=shift, capacity=40 * M)]
+    for b in runs:
+        assert not sss.sss_check_overflow(b)
+        assert int(b.totals[0].item()) == M
+        assert torch.equal(b.ranges, ref.ranges)
+        assert torch.equal(b.ids[0, :M], ref.ids[0, :M])
+    if shift == 0:
+        counts, ids, _ = orc.bin_sort(sc.params, sc.sh_degree, cam[0])
+        assert len(ids) == M
+        assert np.array_equal(ref.ids[0, :M].cpu().numpy(), ids)
+
+
 @pytest.mark.parametrize("shift", [1, 2, 3])
 def test_coarse_bins_are_stable_and_complete(orc, sss, scenes, shift):
     """bin_shift > 0: each bin lists exactly the components whose tile rect
