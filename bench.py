@@ -150,8 +150,8 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, ker
     table["project"] = ("hbm", counts["launches_per_step"] * n * 4 * P + views * n * 60, hbm_peak, "GB/s")
     # bin/sort: lower bound = 4 B id written per instance + 4 B depth key read per comp-view
     table["bin_sort"] = ("hbm", counts["instances"] * 4 + views * n * 4, hbm_peak, "GB/s")
-    # projection backward: g2d 48 B read per comp-view + params 240 B + grad RMW 480 B per launch
-    table["render_bwd_projection"] = ("hbm", views * n * 48 + counts["launches_per_step"] * n * 4 * P * 3,
+    # projection backward: g2d 40 B read per comp-view + params 240 B + grad RMW 480 B per launch
+    table["render_bwd_projection"] = ("hbm", views * n * 40 + counts["launches_per_step"] * n * 4 * P * 3,
                                       hbm_peak, "GB/s")
     table["sghmc"] = ("hbm", n * 4 * (P * 7 + 6), hbm_peak, "GB/s")
     # image loss (L1 + D-SSIM): 132 B per pixel

@@ -51,7 +51,7 @@ typedef enum {
 #define SSS_TILE 16          /* tile edge in pixels */
 #define SSS_MAX_BINS 5632    /* bins per view (tiles >> bin_shift); bounded by the scatter CTA's shared memory */
 #define SSS_REC_FLOATS 12    /* floats per projected record (48 B) */
-#define SSS_G2D_FLOATS 12    /* floats per screen-space gradient record (48 B) */
+#define SSS_G2D_FLOATS 10    /* floats per screen-space gradient record (40 B) */
 #define SSS_TILE_LISTS 2     /* composited-entry lists per tile (one per 16x8 strip) */
 
 /* Pinhole camera (host struct).  p_cam = rot * x + trans (rot row-major,
@@ -221,7 +221,8 @@ SSS_API sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bins,
                           int32_t n_views, const float* bg, sss_frame* out, void* stream);
 
 /* Bytes of device scratch sss_render_bwd needs (screen-space gradient records
- * [V][n][12] floats).  The scratch must be ZERO before the first call; every
+ * [V][n][SSS_G2D_FLOATS] floats: d mu2D (2), d conic A, 2B, C (3), d colour (3),
+ * d o, d nu).  The scratch must be ZERO before the first call; every
  * call leaves it zero again (the projection-backward consumes and clears it). */
 SSS_API size_t sss_render_bwd_workspace(int64_t n, int32_t n_views);
 

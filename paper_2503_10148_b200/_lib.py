@@ -16,7 +16,7 @@ SSS_OK, SSS_ERR_ARG, SSS_ERR_SHAPE, SSS_ERR_CAPACITY, SSS_ERR_CUDA = range(5)
 SSS_TILE = 16
 SSS_MAX_BINS = 5632
 SSS_REC_FLOATS = 12
-SSS_G2D_FLOATS = 12
+SSS_G2D_FLOATS = 10
 SSS_TILE_LISTS = 2
 SSS_VARIANT_POSITIVE, SSS_VARIANT_GAUSSIAN, SSS_VARIANT_LOWPASS = 1, 2, 4
 SSS_BWD_NU_GRAD_PAPER = 1

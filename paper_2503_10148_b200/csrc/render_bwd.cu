@@ -17,7 +17,7 @@
 // The replay keeps only W and the scalar g.S per pixel; a thread sums its
 // four pixels' contributions (the five geometry gradients from three row
 // sums), the warp reduces the 10 values with a butterfly reduce-scatter (12
-// shuffles instead of 50) and issues one RED (10 lanes, one 48-byte record)
+// shuffles instead of 50) and issues one RED (10 lanes, one 40-byte record)
 // into the screen-space gradient record g2d[v][i] in the workspace.
 //
 // a6: with target != NULL the L1 image gradient sign(C - target)/(3HW) is
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
-    float4* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
+    float* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
   __shared__ WarpStage stage[kRasterWarps];
   const int v = blockIdx.y;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
-  float* gvf = reinterpret_cast<float*>(g2d + (int64_t)v * G.n * 3);
+  float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
   const bool writer = !(lane & 1) && ridx >= 0;
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       vals[9] = e2.dnu.x + e2.dnu.y;
       const float r = warp_reduce10(vals, lane);
       // one RED per warp and entry: lanes 0, 2, .. hold the 10 sums of the
-      // 48-byte screen-space gradient record g2d[v][id]
-      if (writer && r != 0.f) atomicAdd(gvf + (int64_t)S.id[buf][j] * 12 + ridx, r);
+      // 40-byte screen-space gradient record g2d[v][id]
+      if (writer && r != 0.f) atomicAdd(gvf + (int64_t)S.id[buf][j] * SSS_G2D_FLOATS + ridx, r);
     }
     __syncwarp();  // this buffer is refilled two batches on
     nb = nb_next;
@@ -419,7 +419,7 @@ template <int DEG>
 #define SSS_PROJB_MINB 4  // 128 registers (measured -12% vs 189)
 #endif
 __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_params P, const __grid_constant__ CamPack cp,
-                                                           int nv, int v0, float4* __restrict__ g2d,
+                                                           int nv, int v0, float2* __restrict__ g2d,
                                                            sss_params Gd) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int64_t n = P.n;
@@ -462,26 +462,33 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
   float g_o = 0.f, g_nu = 0.f;
   bool any = false;
 
-  // software pipeline: the next view's 48-byte record is in flight while this
+  // software pipeline: the next view's 40-byte record is in flight while this
   // view's chain runs (streaming loads: each record is read once)
-  float4 N0 = make_float4(0.f, 0.f, 0.f, 0.f), N1 = N0, N2 = N0;
+  float2 N[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) N[k] = make_float2(0.f, 0.f);
   if (nv > 0) {
-    const float4* gp0 = g2d + ((int64_t)v0 * n + i) * 3;
-    N0 = __ldcs(gp0); N1 = __ldcs(gp0 + 1); N2 = __ldcs(gp0 + 2);
+    const float2* gp0 = g2d + ((int64_t)v0 * n + i) * 5;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) N[k] = __ldcs(gp0 + k);
   }
   for (int vv = 0; vv < nv; ++vv) {
-    float4* gp = g2d + ((int64_t)(v0 + vv) * n + i) * 3;
-    const float4 G0 = N0, G1 = N1, G2 = N2;
+    float2* gp = g2d + ((int64_t)(v0 + vv) * n + i) * 5;
+    const float4 G0 = make_float4(N[0].x, N[0].y, N[1].x, N[1].y);
+    const float4 G1 = make_float4(N[2].x, N[2].y, N[3].x, N[3].y);
+    const float2 G2 = N[4];
     if (vv + 1 < nv) {
-      const float4* gq = gp + (int64_t)n * 3;
-      N0 = __ldcs(gq); N1 = __ldcs(gq + 1); N2 = __ldcs(gq + 2);
+      const float2* gq = gp + (int64_t)n * 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) N[k] = __ldcs(gq + k);
     }
     const bool nz = (G0.x != 0.f) | (G0.y != 0.f) | (G0.z != 0.f) | (G0.w != 0.f) | (G1.x != 0.f) |
                     (G1.y != 0.f) | (G1.z != 0.f) | (G1.w != 0.f) | (G2.x != 0.f) | (G2.y != 0.f);
     if (!nz) continue;
     any = true;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    __stcs(gp, z4); __stcs(gp + 1, z4); __stcs(gp + 2, z4);  // consume-and-clear (workspace stays zero)
+    const float2 z2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) __stcs(gp + k, z2);  // consume-and-clear (workspace stays zero)
     const DevCamera& cam = cp.cam[vv];
     float p[3];
     for (int a = 0; a < 3; ++a) p[a] = cam.R[a * 3 + 0] * mu[0] + cam.R[a * 3 + 1] * mu[1] + cam.R[a * 3 + 2] * mu[2] + cam.t[a];
@@ -648,7 +655,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   }
   if (!fwd->rgb || !fwd->final_T || !fwd->last) { set_error("sss_render_bwd: null frame buffer"); return SSS_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
-  float4* g2d = (float4*)ws;
+  float* g2d = (float*)ws;
   const dim3 grid(G.tiles_x * G.tiles_y, n_views);
   const float4* rec = (const float4*)pr->rec;
   const short4* rect = (const short4*)pr->rect;
@@ -682,10 +689,10 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
     CamPack cp;
     fill_campack(cams, v0, nv, cp);
     switch (p->sh_degree) {
-      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
-      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
-      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
-      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, g2d, *grad); break;
+      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
+      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
+      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
+      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
     }
     count_launch();
     if ((st = check_launch("sss_render_bwd(projection)")) != SSS_OK) return st;

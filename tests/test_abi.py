@@ -75,7 +75,7 @@ def test_argument_validation_is_synchronous(lib):
     assert lib.sss_project(C.byref(p), two, 2, C.byref(out2), None) == L.SSS_ERR_SHAPE
     assert lib.sss_bin_sort_workspace(-1, 1, C.byref(cam), 0) == 0
     assert lib.sss_bin_sort_workspace(1000, 1, C.byref(cam), 0) > 0
-    assert lib.sss_render_bwd_workspace(1000, 2) == 1000 * 2 * 48
+    assert lib.sss_render_bwd_workspace(1000, 2) == 1000 * 2 * L.SSS_G2D_FLOATS * 4 == 80000
     h = L.sss_sghmc_hparams()
     pp = L.sss_params(0, 0, 0, None, None, None, None, None, None)
     assert lib.sss_sghmc_step(C.byref(pp), C.byref(pp), C.byref(pp), C.byref(pp), None,
