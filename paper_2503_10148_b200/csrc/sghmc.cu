@@ -28,6 +28,11 @@
 namespace sss {
 namespace {
 
+#ifndef SSS_SGHMC_SH_BATCH
+#define SSS_SGHMC_SH_BATCH 8
+#endif
+constexpr int kShBatch = SSS_SGHMC_SH_BATCH;  // SH planes whose loads are in flight together
+
 struct HP {
   float lr, friction, noise, gate_k, gate_t;
   int burn_in, g_adam;
@@ -53,6 +58,43 @@ __device__ __forceinline__ void adam_plane(float* theta, const float* grad, floa
                                            float lr, const HP& hp, float reg = 0.f) {
   const float g = fmaf(grad[i], hp.grad_scale, reg);
   theta[i] -= lr * adam_dir(g, m, v, i, hp);
+}
+
+// Adam on planes [k0, k1) (k1 - k0 <= U) of one group: every load is issued
+// before the first store (the planes of a parameter struct may alias as far
+// as the compiler knows, which would otherwise serialise each plane's loads
+// behind the previous plane's stores).  `first` is the group's first plane
+// index in the [P] numbering (the ZeRO plane range).
+template <int U, bool EXPREG = false>
+__device__ __forceinline__ void adam_planes(float* theta, const float* grad, float* m, float* v, int64_t i,
+                                            int64_t n, int k0, int k1, int first, float lr, const HP& hp) {
+  float t[U], g[U], mo[U], vo[U];
+  bool on[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int k = k0 + u;
+    on[u] = k < k1 && first + k >= hp.p0 && first + k < hp.p1;
+    if (on[u]) {
+      const int64_t idx = (int64_t)k * n + i;
+      t[u] = theta[idx];
+      g[u] = grad[idx];
+      mo[u] = m[idx];
+      vo[u] = v[idx];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!on[u]) continue;
+    const int64_t idx = (int64_t)(k0 + u) * n + i;
+    // EXPREG: Eq. 8's eps_Sigma exp(s) on the log-scales (R27)
+    const float reg = EXPREG && hp.eps_sigma != 0.f ? hp.eps_sigma * expf(t[u]) : 0.f;
+    const float gg = fmaf(g[u], hp.grad_scale, reg);
+    const float mm = hp.beta1 * mo[u] + (1.f - hp.beta1) * gg;
+    const float vv = hp.beta2 * vo[u] + (1.f - hp.beta2) * gg * gg;
+    m[idx] = mm;
+    v[idx] = vv;
+    theta[idx] = t[u] - lr * ((mm * hp.inv_b1t) / (sqrtf(vv * hp.inv_b2t) + hp.adam_eps));
+  }
 }
 
 __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr, sss_params Mo,
@@ -117,21 +159,15 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
   }
   // ---- Adam on the other groups
-  for (int a = 0; a < 3; ++a) {
-    if (!mine(3 + a)) continue;
-    const int64_t idx = a * n + i;
-    const float reg = hp.eps_sigma != 0.f ? hp.eps_sigma * expf(P.log_scale[idx]) : 0.f;
-    adam_plane(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, idx, hp.lr_group[0], hp, reg);
-  }
-  for (int a = 0; a < 4; ++a)
-    if (mine(6 + a)) adam_plane(P.rot, Gr.rot, Mo.rot, Vo.rot, a * n + i, hp.lr_group[1], hp);
+  adam_planes<3, true>(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, i, n, 0, 3, 3, hp.lr_group[0], hp);
+  adam_planes<4>(P.rot, Gr.rot, Mo.rot, Vo.rot, i, n, 0, 4, 6, hp.lr_group[1], hp);
   if (mine(10)) adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
   if (mine(11)) {
     const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (positive ? o * (1.f - o) : 1.f - o * o);
     adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
   }
-  for (int k = 0; k < 3 * K; ++k)
-    if (mine(12 + k)) adam_plane(P.sh, Gr.sh, Mo.sh, Vo.sh, k * n + i, hp.lr_group[4], hp);
+  for (int k = 0; k < 3 * K; k += kShBatch)
+    adam_planes<kShBatch>(P.sh, Gr.sh, Mo.sh, Vo.sh, i, n, k, min(k + kShBatch, 3 * K), 12, hp.lr_group[4], hp);
 }
 
 }  // namespace
