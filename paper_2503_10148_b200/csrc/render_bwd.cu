@@ -607,13 +607,42 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
   const float o = positive ? 1.f / (1.f + expf(-raw_o)) : tanhf(raw_o);
   const float sp = raw_nu > 30.f ? raw_nu : log1pf(expf(raw_nu));
   const float dnu = (1.f + sp >= (float)kNuMax) ? 0.f : 1.f / (1.f + expf(-raw_nu));
-  for (int a = 0; a < 3; ++a) Gd.mean[a * n + i] += gmu[a];
-  for (int a = 0; a < 3; ++a) Gd.log_scale[a * n + i] += gls[a];
-  for (int a = 0; a < 4; ++a) Gd.rot[a * n + i] += (gq[a] - qh[a] * dotq) / qn;
-  Gd.raw_nu[i] += g_nu * dnu;
-  Gd.raw_opacity[i] += g_o * (positive ? o * (1.f - o) : 1.f - o * o);
+  // grad += result: every plane's load is issued before the first store (the
+  // planes may alias as far as the compiler knows, which would otherwise
+  // serialise each read-modify-write behind the previous store)
+  float grot[4];
 #pragma unroll
-  for (int k = 0; k < 3 * K; ++k) Gd.sh[k * n + i] += gsh[k];
+  for (int a = 0; a < 4; ++a) grot[a] = (gq[a] - qh[a] * dotq) / qn;
+  const float gnu = g_nu * dnu, gro = g_o * (positive ? o * (1.f - o) : 1.f - o * o);
+  {
+    float cur[12];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cur[a] = Gd.mean[a * n + i];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cur[3 + a] = Gd.log_scale[a * n + i];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) cur[6 + a] = Gd.rot[a * n + i];
+    cur[10] = Gd.raw_nu[i];
+    cur[11] = Gd.raw_opacity[i];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Gd.mean[a * n + i] = cur[a] + gmu[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Gd.log_scale[a * n + i] = cur[3 + a] + gls[a];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) Gd.rot[a * n + i] = cur[6 + a] + grot[a];
+    Gd.raw_nu[i] = cur[10] + gnu;
+    Gd.raw_opacity[i] = cur[11] + gro;
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < 3 * K; k0 += 8) {
+    float cur[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < 3 * K) cur[u] = Gd.sh[(k0 + u) * n + i];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < 3 * K) Gd.sh[(k0 + u) * n + i] = cur[u] + gsh[k0 + u];
+  }
 }
 
 }  // namespace
