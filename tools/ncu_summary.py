@@ -15,7 +15,10 @@ WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram r
         ("launch__registers_per_thread", "registers / thread"),
         ("launch__grid_size", "grid"), ("launch__block_size", "block")]
 for rep in sys.argv[1:]:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # an exported raw page (ncu -i X --page raw --csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h, u = r[0], r[1]
     rows = r[2:]
