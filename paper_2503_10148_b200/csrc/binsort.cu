@@ -31,10 +31,10 @@
 namespace sss {
 namespace {
 
-#ifndef SSS_RADIX_MATCH
-#define SSS_RADIX_MATCH 0  // warp peers of a digit: 0 = 8 ballots, 1 = match.any
+#ifndef SSS_SCATTER_THREADS
+#define SSS_SCATTER_THREADS 256
 #endif
-constexpr int kScatterThreads = 256;
+constexpr int kScatterThreads = SSS_SCATTER_THREADS;  // chunk_hist and scatter CTAs
 constexpr int kScatterWarps = kScatterThreads / 32;
 
 struct BinGeom {
@@ -128,7 +128,7 @@ __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0
 // components).  Writes the chunk totals (u32, for the scans) and the per-warp
 // counts (u8: a warp's 128 components hit a bin at most 128 times), so the
 // scatter needs no counting pass of its own.
-__global__ void __launch_bounds__(256) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
+__global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
                                                          const int32_t* __restrict__ n_vis,
                                                          const short4* __restrict__ rect, int64_t n,
                                                          int chunk, int n_chunks, BinGeom g,
@@ -558,7 +558,7 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     // after 4 passes the sorted ids are in vals_a
     const dim3 gc(L.n_chunks, n_views);
     const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
-    chunk_hist_kernel<<<gc, 256, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
+    chunk_hist_kernel<<<gc, kScatterThreads, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
     column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 256, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
     count_launch(2);
   } else {
