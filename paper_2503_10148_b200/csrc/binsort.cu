@@ -166,18 +166,23 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
   }
 }
 
-// per (view, bin): exclusive scan over chunks in place; bin totals
 // per (view, bin): exclusive scan over chunks in place; bin totals.  CTA =
-// 32 bins (lane = bin, coalesced rows) x 8 warps, each warp a contiguous
-// range of chunks: range sums, a prefix over warps, then the running write.
-__global__ void __launch_bounds__(256) column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chunks,
+// 32 bins (lane = bin, coalesced rows) x kColWarps warps, each warp a
+// contiguous range of chunks: range sums, a prefix over warps, then the
+// running write (32 warps: the short serial chains of loads per warp keep
+// this latency-bound pass at 1.4% of bin_sort less than with 8).
+#ifndef SSS_COLSCAN_WARPS
+#define SSS_COLSCAN_WARPS 32
+#endif
+constexpr int kColWarps = SSS_COLSCAN_WARPS;  // warps splitting the chunk range of 32 bins
+__global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chunks,
                                                           int n_bins, uint32_t* __restrict__ bin_total) {
-  __shared__ uint32_t wsum[8][32];
+  __shared__ uint32_t wsum[kColWarps][32];
   const int v = blockIdx.y;
   const int w = threadIdx.x >> 5, lane = lane_id();
   const int b = blockIdx.x * 32 + lane;
   const bool ok = b < n_bins;
-  const int per = (n_chunks + 7) / 8;
+  const int per = (n_chunks + kColWarps - 1) / kColWarps;
   const int c0 = min(w * per, n_chunks), c1 = min(c0 + per, n_chunks);
   uint32_t* col = chunk_hist + (size_t)v * n_chunks * n_bins + (ok ? b : 0);
   uint32_t s = 0;
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(256) column_scan_kernel(uint32_t* __restrict__
   __syncthreads();
   uint32_t run = 0, tot = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < kColWarps; ++k) {
     run += k < w ? wsum[k][lane] : 0u;
     tot += wsum[k][lane];
   }
@@ -559,7 +564,7 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     const dim3 gc(L.n_chunks, n_views);
     const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
     chunk_hist_kernel<<<gc, kScatterThreads, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
-    column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 256, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
+    column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 32 * kColWarps, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
     count_launch(2);
   } else {
     cudaMemsetAsync(btot, 0, sizeof(uint32_t) * n_views * g.n_bins, s);
