@@ -204,7 +204,11 @@ SSS_API size_t sss_bin_sort_workspace(int64_t n, int32_t n_views, const sss_came
  * stable LSD radix sort of the depth keys followed by a stable counting
  * scatter by bin.  ws: device scratch of at least sss_bin_sort_workspace()
  * bytes.  out->bin_shift, capacity, ids, ranges, totals, overflow must be set
- * (keys optional).  Overflow is device-side (see sss_bins). */
+ * (keys optional).  Overflow is device-side (see sss_bins).  SSS_ERR_SHAPE if
+ * the view has more than SSS_MAX_BINS bins or more than 1024 bins along an
+ * axis (raise bin_shift).  The capacity also sizes the scatter's shared-
+ * memory stage (capacity / chunks of 1024 components); chunks above it take
+ * a slower direct path, so size it near the instance count. */
 SSS_API sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* cams, int32_t n_views,
                         void* ws, size_t ws_bytes, sss_bins* out, void* stream);
 

@@ -73,6 +73,14 @@ def test_argument_validation_is_synchronous(lib):
     two[1].width = 32
     out2 = L.sss_projected(0, 2, 0, None, None, None)
     assert lib.sss_project(C.byref(p), two, 2, C.byref(out2), None) == L.SSS_ERR_SHAPE
+    # the scatter packs bin coordinates in 10 bits: > 1024 bins per axis is a shape error
+    wide = L.sss_camera()
+    wide.fx = wide.fy = 100.0
+    wide.width, wide.height, wide.z_near = 16 * 1025, 16, 0.2
+    prw = L.sss_projected(0, 1, 0, None, None, None)
+    bw = L.sss_bins(0, 1, 0, None, None, None, None, None)
+    assert lib.sss_bin_sort(C.byref(prw), C.byref(wide), 1, None, 0, C.byref(bw), None) == L.SSS_ERR_SHAPE
+    assert b"1024 per axis" in lib.sss_last_error()
     assert lib.sss_bin_sort_workspace(-1, 1, C.byref(cam), 0) == 0
     assert lib.sss_bin_sort_workspace(1000, 1, C.byref(cam), 0) > 0
     assert lib.sss_render_bwd_workspace(1000, 2) == 1000 * 2 * L.SSS_G2D_FLOATS * 4 == 80000
