@@ -121,6 +121,30 @@ def test_scatter_staged_and_direct_paths_agree(orc, sss, shift):
         assert np.array_equal(ref.ids[0, :M].cpu().numpy(), ids)
 
 
+def test_scatter_large_rects_bit_exact(orc, sss):
+    """Components covering most of a 1297x840 view (rects of up to 82 x 53
+    tiles): the flattened walk's rank/bin arithmetic (division of the
+    instance index by the rect width, 10-bit packed coordinates) over
+    thousands of instances per component, against the oracle's lists."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    sc = make_custom_scene(300, 0, 1297, 840, seed=43, log_scale_mean=0.3)
+    cam = sc.cameras
+    params = to_dev(sc)
+    pr = sss.sss_project(params, cam)
+    bins = sss.sss_bin_sort(pr, cam, bin_shift=0)
+    assert not sss.sss_check_overflow(bins)
+    counts, ids, _ = orc.bin_sort(sc.params, sc.sh_degree, cam[0])
+    M = len(ids)
+    assert M > 300 * 1000  # large rects: > 1000 tiles per component on average
+    assert int(bins.totals[0].item()) == M
+    rg = bins.ranges[0].cpu().numpy()
+    assert np.array_equal(rg[:, 1] - rg[:, 0], counts)
+    assert torch.equal(bins.ids[0, :M].cpu(), torch.from_numpy(ids))
+
+
 @pytest.mark.parametrize("shift", [1, 2, 3])
 def test_coarse_bins_are_stable_and_complete(orc, sss, scenes, shift):
     """bin_shift > 0: each bin lists exactly the components whose tile rect
