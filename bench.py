@@ -153,7 +153,8 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, ker
     # projection backward: g2d 40 B read per comp-view + params 240 B + grad RMW 480 B per launch
     table["render_bwd_projection"] = ("hbm", views * n * 40 + counts["launches_per_step"] * n * 4 * P * 3,
                                       hbm_peak, "GB/s")
-    table["sghmc"] = ("hbm", n * 4 * (P * 7 + 6), hbm_peak, "GB/s")
+    Pu = counts.get("sghmc_planes", P)  # this rank's planes (ZeRO-1 shard for R > 1)
+    table["sghmc"] = ("hbm", counts.get("steps", 1) * n * 4 * (Pu * 7 + 6), hbm_peak, "GB/s")
     # image loss (L1 + D-SSIM): 132 B per pixel
     table["image_loss"] = ("hbm", counts.get("pixels", 0) * 132, hbm_peak, "GB/s")
     dom = kernel or max((k for k in phase_ms if k in table), key=lambda k: phase_ms[k])
@@ -373,12 +374,23 @@ def main():
     ts.forward_backward(targets)
     pairs, inst = float(ts.stats["pairs"].item()), float(ts.stats["instances"].item())
     ts.stats = None
-    counts = {"pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
+    counts = {"steps": a.steps, "sghmc_planes": (ts.p1 - ts.p0) if ts.shard else sc.params.shape[0],
+              "pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
               "launches_per_step": len(ts.batches) * a.steps,
               "pixels": len(mine) * a.steps * sc.cameras[0].width * sc.cameras[0].height}
     pk = peaks()
     dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
                              views_per_launch=len(ts.batches[0]))
+    # every timed phase against its own bound (informational; `roofline` is
+    # the dominant one)
+    all_roof = {}
+    for ph in phases:
+        try:
+            r = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
+                             views_per_launch=len(ts.batches[0]), kernel=ph)[1]
+        except KeyError:
+            continue
+        all_roof[ph] = {k: r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "share_of_step")}
     extra_roof = {}
     if "image_loss" in phases:
         extra_roof["image_loss"] = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
@@ -450,6 +462,7 @@ def main():
             "mpix_per_s_fwd_bwd": round(mpix, 2),
             "phase_ms_per_step": {k: round(v / a.steps, 3) for k, v in phases.items()},
             "roofline": roof,
+            "roofline_all_phases": all_roof,
             **({"roofline_next": extra_roof} if extra_roof else {}),
             "cpu_baseline": cb,
             "e2e": e2e,
