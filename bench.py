@@ -285,6 +285,21 @@ def cpu_baseline_sample(scene, targets_np, budget_s, views_total):
             "seconds_per_iter": round(t_iter, 1)}
 
 
+def arm_config(a, sc, world):
+    """The workload's config (both arms print the same one)."""
+    from sss_synth import CONFIG_NAMES
+
+    cam = sc.cameras[0]
+    return {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": sc.n_views,
+            "width": cam.width, "height": cam.height, "sh_degree": sc.sh_degree,
+            "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch,
+            "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
+                     if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
+            "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
+            "parallelism": f"view-dp{world}",
+            "l2": "no flush: inputs > L2 (params 720 MB, targets 837 MB, bins GBs)"}
+
+
 def run_reference(a):
     """--impl reference: the oracle, timed as it stands, on bounded samples."""
     rank, world, local = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
@@ -304,7 +319,7 @@ def run_reference(a):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "it/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 / v, 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": CONFIG_NAMES[a.config]},
+            "data": "synthetic", "config": arm_config(a, sc, a.gpus),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -451,14 +466,7 @@ def main():
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_max / a.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": V,
-                       "width": W, "height": H, "sh_degree": sc.sh_degree,
-                       "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch,
-                       "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
-                                if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
-                       "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
-                       "parallelism": f"view-dp{world}",
-                       "l2": "no flush: inputs > L2 (params 720 MB, targets 837 MB, bins GBs)"},
+            "config": arm_config(a, sc, world),
             "mpix_per_s_fwd_bwd": round(mpix, 2),
             "phase_ms_per_step": {k: round(v / a.steps, 3) for k, v in phases.items()},
             "roofline": roof,
