@@ -35,6 +35,10 @@ namespace {
 #define SSS_SCATTER_THREADS 256
 #endif
 constexpr int kScatterThreads = SSS_SCATTER_THREADS;  // chunk_hist and scatter CTAs
+#ifndef SSS_SCATTER_RUN_LANES
+#define SSS_SCATTER_RUN_LANES 8
+#endif
+constexpr int kRunLanes = SSS_SCATTER_RUN_LANES;  // lanes storing one bin's staged run
 constexpr int kScatterWarps = kScatterThreads / 32;
 
 struct BinGeom {
@@ -485,10 +489,14 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   }
   warp_walk<true>(sid, rv, dv, wlo, whi, g, wbase + (size_t)w * nb, colmask, rowmask, scratch[w], sids, nullptr);
   __syncthreads();
-  for (int b = w; b < nb; b += kScatterWarps) {  // one bin's run per warp, consecutive lanes
+  // copy-out: each group of kRunLanes lanes stores one bin's run (runs
+  // average ~30 ids at bin_shift 2) with consecutive lanes on consecutive slots
+  constexpr int kGroups = 32 / kRunLanes;
+  const int gl = lane % kRunLanes;
+  for (int b = kGroups * w + lane / kRunLanes; b < nb; b += kGroups * kScatterWarps) {
     const uint32_t s0 = soff[b], cnt = soff[b + 1] - s0;
     int32_t* out = idv + gst[b];
-    for (uint32_t i = lane; i < cnt; i += 32) out[i] = sids[s0 + i];
+    for (uint32_t i = gl; i < cnt; i += kRunLanes) out[i] = sids[s0 + i];
   }
 }
 
