@@ -423,6 +423,9 @@ def main():
     comp_s = torch.cuda.current_stream()
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     used = [torch.cuda.Event(), torch.cuda.Event()]
+    got = [torch.cuda.Event(), torch.cuda.Event()]
+    loss_host = torch.zeros(2, dtype=torch.float32).pin_memory()
+    losses_e2e = []
     torch.cuda.synchronize()
     D.barrier()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -442,13 +445,23 @@ def main():
         comp_s.wait_event(copied[cur])
         loss = ts.step(bufs[cur])
         used[cur].record()
-        _ = float(loss.item())
+        # every step's loss goes device->host (pinned); the host reads step
+        # k's value while step k+1 runs (the GPU never waits for the host)
+        loss_host[cur:cur + 1].copy_(loss, non_blocking=True)
+        got[cur].record()
+        if k >= 1:
+            got[nxt].synchronize()
+            losses_e2e.append(float(loss_host[nxt]))
     s1.record()
+    got[(e2e_steps - 1) % 2].synchronize()
+    losses_e2e.append(float(loss_host[(e2e_steps - 1) % 2]))
     torch.cuda.synchronize()
     e2e_ms = D.allreduce_max(s0.elapsed_time(s1), device=torch.device("cuda", local))
     e2e = {"value": round(e2e_steps / (e2e_ms / 1e3), 4), "unit": "it/s",
            "h2d_bytes_per_step": int(host_t.numel() * 4), "d2h_bytes_per_step": 4,
-           "pipeline": "next step's targets copied (pinned H2D) on a second stream during the current step"}
+           "pipeline": ("next step's targets copied (pinned H2D) on a second stream during the current step; "
+                        "each step's loss copied D2H (pinned) and read by the host while the next step runs"),
+           "losses_read": len(losses_e2e)}
     del bufs, host_t
     # ---- NEXT rows, timed outside the step (CUDA events, 5 repeats, median)
     next_rows = {}
