@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     PixF2& pp = p[k >> 1];
     lane_of(pp.W, k) = inside ? 1.f : 0.f;
     lane_of(pp.C0, k) = lane_of(pp.C1, k) = lane_of(pp.C2, k) = 0.f;
-    lane_of(px[k >> 1], k) = (float)(x0 + k) + 0.5f;
+    // a stopped (or outside) pixel's coordinate is NaN: its h is NaN and
+    // fails h <= hmax, so the inclusion test needs no liveness term
+    lane_of(px[k >> 1], k) = inside ? (float)(x0 + k) + 0.5f : __int_as_float(0x7fffffff);
     cnt[k] = 0;
     lastc[k] = start;
   }
@@ -178,8 +180,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       for (int k = 0; k < kPairs; ++k) {
         float2 dx;
         h[k] = h_f32_pair(px[k], a.x, a.z, bdy, cdy2, dx);
-        inc[2 * k] = p[k].W.x >= kWStop && h[k].x <= b.y;
-        inc[2 * k + 1] = p[k].W.y >= kWStop && h[k].y <= b.y;
+        inc[2 * k] = h[k].x <= b.y;  // false for stopped pixels (px NaN)
+        inc[2 * k + 1] = h[k].y <= b.y;
         any = any || inc[2 * k] || inc[2 * k + 1];
       }
 #ifdef SSS_COUNTERS
@@ -211,6 +213,9 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
         for (int k = 0; k < kPX; ++k) {
           lastc[k] = inc[k] ? pj1 : lastc[k];
           if (COUNT) cnt[k] += inc[k] ? 1 : 0;
+          // R11: the pixel stops after the component that drives W below 1e-4
+          float& xk = lane_of(px[k >> 1], k);
+          xk = lane_of(p[k >> 1].W, k) >= kWStop ? xk : __int_as_float(0x7fffffff);
         }
       }
       if ((j & 7) == 7 && __all_sync(0xffffffffu, all_done())) break;
