@@ -225,8 +225,8 @@ SSS_API sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bins,
                           int32_t n_views, const float* bg, sss_frame* out, void* stream);
 
 /* Bytes of device scratch sss_render_bwd needs (screen-space gradient records
- * [V][n][SSS_G2D_FLOATS] floats: d mu2D (2), d conic A, 2B, C (3), d colour (3),
- * d o, d nu).  The scratch must be ZERO before the first call; every
+ * [V][n][SSS_G2D_FLOATS] floats, private layout: the geometry moments
+ * sum dh (dx, dy, dx^2, dx dy, dy^2) (5), d colour (3), d o, d nu).  The scratch must be ZERO before the first call; every
  * call leaves it zero again (the projection-backward consumes and clears it). */
 SSS_API size_t sss_render_bwd_workspace(int64_t n, int32_t n_views);
 

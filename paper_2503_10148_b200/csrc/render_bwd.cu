@@ -74,10 +74,10 @@ struct PixB2 {
 
 // Per-thread sums over its pixels for one entry (lane-wise over the pairs;
 // the two lanes are added once per entry).  The thread's pixels share a row
-// (one dy), so the five screen-space geometry gradients follow from sum dh,
-// sum dh dx and sum dh dx^2:
-//   d mu2D = -(2A sum dh dx + B2 dy sum dh, B2 sum dh dx + 2C dy sum dh),
-//   d(A, B, C) = (sum dh dx^2, 2 dy sum dh dx, dy^2 sum dh).
+// (one dy), so the five geometry moments S1..S5 = sum dh (dx, dy, dx^2,
+// dx dy, dy^2) follow from sum dh, sum dh dx and sum dh dx^2; the record
+// stores them and the projection backward maps them once per record:
+//   d mu2D = -2 Q (S1, S2),  d(A, B, C) = (S3, 2 S4, S5).
 struct EntrySums2 {
   float2 sdh, sdhdx, sdhdx2, dc0, dc1, dc2, dO, dnu;
 };
@@ -324,14 +324,17 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
         for (int k = 0; k < kPairs; ++k)
           pair_grad2<NUP, false>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
       }
+      // geometry: the five moments sum dh (dx, dy, dx^2, dx dy, dy^2); the
+      // linear map to d mu2D (through the conic) is applied once per record
+      // by the projection backward
       const float sdh = e2.sdh.x + e2.sdh.y, sdhdx = e2.sdhdx.x + e2.sdhdx.y;
       const float dysdh = dy * sdh;
       float vals[10];
-      vals[0] = -fmaf(2.f * a.z, sdhdx, a.w * dysdh);   // d mu2D_x
-      vals[1] = -fmaf(a.w, sdhdx, 2.f * b.x * dysdh);   // d mu2D_y
-      vals[2] = e2.sdhdx2.x + e2.sdhdx2.y;              // d A
-      vals[3] = 2.f * dy * sdhdx;                       // d B (conic_xy)
-      vals[4] = dy * dysdh;                             // d C
+      vals[0] = sdhdx;                                  // S1 = sum dh dx
+      vals[1] = dysdh;                                  // S2 = sum dh dy
+      vals[2] = e2.sdhdx2.x + e2.sdhdx2.y;              // S3 = sum dh dx^2 = d A
+      vals[3] = dy * sdhdx;                             // S4 = sum dh dx dy = d B / 2
+      vals[4] = dy * dysdh;                             // S5 = sum dh dy^2 = d C
       vals[5] = e2.dc0.x + e2.dc0.y;
       vals[6] = e2.dc1.x + e2.dc1.y;
       vals[7] = e2.dc2.x + e2.dc2.y;
@@ -517,8 +520,10 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
     }
     const float idet = 1.f / (cxx * cyy - cxy * cxy);
     const float QA = cyy * idet, QB = -cxy * idet, QC = cxx * idet;
+    // the raster's moments S1..S5 (G0.xyzw, G1.x): dA = S3, dB/2 = S4,
+    // dC = S5, d mu2D = -2 Q (S1, S2) (h = d^T Q d, dh/dmu2D = -2 Q d)
     // G_S = -Q G_Q Q with G_Q = [[dA, dB/2], [dB/2, dC]]
-    const float gA = G0.z, gB = 0.5f * G0.w, gC = G1.x;
+    const float gA = G0.z, gB = G0.w, gC = G1.x;
     const float QG00 = QA * gA + QB * gB, QG01 = QA * gB + QB * gC;
     const float QG10 = QB * gA + QC * gB, QG11 = QB * gB + QC * gC;
     const float GS00 = -(QG00 * QA + QG01 * QB);
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
         gSig[a * 3 + b] += acc;
       }
     // camera-space mean through mean2d and J(p)
-    const float dmx = G0.x, dmy = G0.y;
+    const float dmx = -2.f * (QA * G0.x + QB * G0.y), dmy = -2.f * (QB * G0.x + QC * G0.y);
     const float iz2 = iz * iz, iz3 = iz2 * iz;
     float dp0 = cam.fx * iz * dmx + GJ[2] * (-cam.fx * iz2);
     float dp1 = cam.fy * iz * dmy + GJ[5] * (-cam.fy * iz2);
