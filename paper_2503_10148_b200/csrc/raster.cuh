@@ -43,7 +43,7 @@ static_assert(kRasterWarps == SSS_TILE_LISTS, "one composited-entry list per war
 constexpr int kWB = 32;
 struct WarpStage {
   float4 r[2][3][kWB];  // [buffer][record float4][slot]
-  int32_t pos[2][kWB], id[2][kWB];
+  int32_t pos[2][kWB], id[2][kWB];  // id: the caller's tag of the entry
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -55,10 +55,11 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Stages one batch: the lanes with `ok` are compacted in lane order (ballot)
-// into slots of buffer `buf`, their 48-byte records gathered by cp.async;
+// into slots of buffer `buf` (position and tag), their 48-byte records
+// gathered by cp.async;
 // commits one async group (also when empty) and returns the entry count.
 __device__ __forceinline__ int stage_batch(WarpStage& S, int buf, bool ok, int32_t pos, int32_t id,
-                                           const float4* __restrict__ rv, unsigned lt) {
+                                           const float4* __restrict__ rv, unsigned lt, int32_t tag) {
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   if (ok) {
     const int slot = __popc(bal & lt);
@@ -67,7 +68,7 @@ __device__ __forceinline__ int stage_batch(WarpStage& S, int buf, bool ok, int32
     cp_async16(&S.r[buf][1][slot], src + 1);
     cp_async16(&S.r[buf][2][slot], src + 2);
     S.pos[buf][slot] = pos;
-    S.id[buf][slot] = id;
+    S.id[buf][slot] = tag;
   }
   cp_async_commit();
   return __popc(bal);

@@ -229,7 +229,12 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
-  const bool writer = !(lane & 1) && ridx >= 0;
+  // opaque copies of the lane and of the lane's slot in the 10-float record
+  // (-1: not a writer): otherwise the compiler re-derives them from %tid in
+  // every entry (an S2R and ~15 integer ops)
+  int lane_o, roff;
+  asm volatile("mov.b32 %0, %1;" : "=r"(lane_o) : "r"(lane));
+  asm volatile("mov.b32 %0, %1;" : "=r"(roff) : "r"(!(lane & 1) && ridx >= 0 ? ridx : -1));
 
   // The forward's list of the entries this warp's strip composited: replay
   // only those; else (no lists, or this list overflowed) the whole
@@ -258,7 +263,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       const short4 r = rcv[id];
       ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
     }
-    return stage_batch(S, buf, ok, p, id, rv, lt);
+    // tag: the entry's g2d record offset (uint32: n < 2^32 / SSS_G2D_FLOATS, checked by the API)
+    return stage_batch(S, buf, ok, p, id, rv, lt, (int32_t)((uint32_t)id * SSS_G2D_FLOATS));
   };
 
   int32_t hi = lend;
@@ -340,10 +346,10 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       vals[7] = e2.dc2.x + e2.dc2.y;
       vals[8] = e2.dO.x + e2.dO.y;
       vals[9] = e2.dnu.x + e2.dnu.y;
-      const float r = warp_reduce10(vals, lane);
+      const float r = warp_reduce10(vals, lane_o);
       // one RED per warp and entry: lanes 0, 2, .. hold the 10 sums of the
       // 40-byte screen-space gradient record g2d[v][id]
-      if (writer && r != 0.f) atomicAdd(gvf + (int64_t)S.id[buf][j] * SSS_G2D_FLOATS + ridx, r);
+      if (roff >= 0 && r != 0.f) atomicAdd(gvf + ((uint32_t)S.id[buf][j] + (uint32_t)roff), r);
     }
     __syncwarp();  // this buffer is refilled two batches on
     nb = nb_next;
@@ -682,6 +688,10 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   }
   RasterGeom G;
   if (!raster_geom(pr, bins, cams, n_views, G)) { set_error("sss_render_bwd: geometry mismatch"); return SSS_ERR_SHAPE; }
+  if (p->n > (int64_t)(0xffffffffu / SSS_G2D_FLOATS)) {  // 32-bit record offsets in the raster
+    set_error("sss_render_bwd: n = %lld > %u components", (long long)p->n, 0xffffffffu / SSS_G2D_FLOATS);
+    return SSS_ERR_SHAPE;
+  }
   const size_t need = sss_render_bwd_workspace(p->n, n_views);
   if (ws_bytes < need || (need > 0 && !ws)) {
     set_error("sss_render_bwd: workspace %zu < %zu bytes", ws_bytes, need);
