@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
   float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
+  asm volatile("mov.b64 %0, %0;" : "+l"(gvf));  // opaque: kept in registers, not re-derived per entry
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
   // opaque copies of the lane and of the lane's slot in the 10-float record
