@@ -138,25 +138,6 @@ __device__ __forceinline__ float2 h_f32_pair(float2 px, float mx, float A, float
   return __ffma2_rn(dx, __ffma2_rn(bc2(A), dx, bc2(bdy)), bc2(cdy2));
 }
 
-// Shared-memory loads at an opaque 32-bit shared address (the compiler
-// otherwise re-derives a __shared__ array's address, CTA-in-cluster id
-// included, at every use inside the hot loops).
-__device__ __forceinline__ uint32_t opaque_smem_addr(const void* p) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("mov.b32 %0, %0;" : "+r"(a));
-  return a;
-}
-__device__ __forceinline__ float4 lds_f4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
-  int32_t v;
-  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

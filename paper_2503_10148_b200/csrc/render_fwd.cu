@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
-  const uint32_t sc_a = opaque_smem_addr(sc), spos_a = opaque_smem_addr(spos);
 
   if (threadIdx.x == 0) SSS_COUNT(7, end - start);
   PixF2 p[kPairs];
@@ -201,8 +200,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
 #pragma unroll
           for (int q = 0; q < kBatch / 32; ++q) cm[q] |= (j >> 5) == q ? 1u << (j & 31) : 0u;
         }
-        const float4 c = lds_f4(sc_a + 16u * (uint32_t)j);  // sc[j] = {e, r, g, b}
-        const int32_t pj1 = lds_s32(spos_a + 4u * (uint32_t)j) + 1;
+        const float4 c = sc[j];  // {e, r, g, b}
+        const int32_t pj1 = spos[j] + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
           for (int k = 0; k < kPairs; ++k) composite2<true>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
