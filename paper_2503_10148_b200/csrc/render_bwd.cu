@@ -95,7 +95,8 @@ __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v
 // (accurate log1p), the Gaussian kernel of the ablation variant (inv_nu = 0:
 // T = exp(-h/2), dT/dh = -T/2, dT/dnu = 0) and |o| > 0.989, where the +-0.99
 // clamp (R10) can bind and then cuts the gradient.
-template <bool NU_PAPER, bool GENERAL>
+// FIRST: the entry's sums start at this pair (assigned, not added to zeros)
+template <bool NU_PAPER, bool GENERAL, bool FIRST>
 __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4 b, float4 c, float einu,
                                            EntrySums2& e, bool inc0, bool inc1) {
   const float2 t = mul2(h, bc2(b.w));
@@ -129,9 +130,9 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
   const float2 oma = sub2(bc2(1.f), alpha);  // 1 - a >= 0.01 (R10): no range fix-up
   const float2 Wi = mul2(p.W, make_float2(rcp_approx(oma.x), rcp_approx(oma.y)));
   const float2 aw = mul2(alpha, Wi);
-  e.dc0 = fma2(p.g0, aw, e.dc0);
-  e.dc1 = fma2(p.g1, aw, e.dc1);
-  e.dc2 = fma2(p.g2, aw, e.dc2);
+  e.dc0 = FIRST ? mul2(p.g0, aw) : fma2(p.g0, aw, e.dc0);
+  e.dc1 = FIRST ? mul2(p.g1, aw) : fma2(p.g1, aw, e.dc1);
+  e.dc2 = FIRST ? mul2(p.g2, aw) : fma2(p.g2, aw, e.dc2);
   const float2 gc = fma2(p.g0, bc2(c.y), fma2(p.g1, bc2(c.z), mul2(p.g2, bc2(c.w))));
   const float2 diff = sub2(gc, p.gS);
   float2 da = mul2(diff, Wi);
@@ -141,17 +142,17 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
     da.x = (inc0 && fabsf(araw.x) <= kAlphaMax) ? da.x : 0.f;
     da.y = (inc1 && fabsf(araw.y) <= kAlphaMax) ? da.y : 0.f;
   }  // (fast path: an excluded pixel's da multiplies T = 0 and Topt = 0 below)
-  e.dO = fma2(da, T, e.dO);
+  e.dO = FIRST ? mul2(da, T) : fma2(da, T, e.dO);
   const float2 dT = mul2(da, bc2(b.z));
   const float2 dh = mul2(mul2(dT, bc2(einu)), Topt);
   const float2 met = mul2(t, bc2(-einu));
   const float2 dTdnu = NU_PAPER ? mul2(met, Topt)
                                 : fma2(met, Topt, mul2(T, mul2(lg, bc2(-0.34657359027997264f))));
-  e.dnu = fma2(dT, dTdnu, e.dnu);
+  e.dnu = FIRST ? mul2(dT, dTdnu) : fma2(dT, dTdnu, e.dnu);
   const float2 dhdx = mul2(dh, dx);
-  e.sdh = add2(e.sdh, dh);
-  e.sdhdx = add2(e.sdhdx, dhdx);
-  e.sdhdx2 = fma2(dhdx, dx, e.sdhdx2);
+  e.sdh = FIRST ? dh : add2(e.sdh, dh);
+  e.sdhdx = FIRST ? dhdx : add2(e.sdhdx, dhdx);
+  e.sdhdx2 = FIRST ? mul2(dhdx, dx) : fma2(dhdx, dx, e.sdhdx2);
 }
 
 template <bool FILTER, bool L1, bool NUP>
@@ -227,7 +228,6 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
   float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
-  asm volatile("mov.b64 %0, %0;" : "+l"(gvf));  // opaque: kept in registers, not re-derived per entry
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
   // opaque copies of the lane and of the lane's slot in the 10-float record
@@ -320,16 +320,14 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       const float4 c = S.r[buf][2][j];  // {e, r, g, b}
       // e / nu = -(nu+2)/(2 nu): dT/dh = einu T/(1 + h/nu); -1/2 for the Gaussian variant
       const float einu = b.w == 0.f ? -0.5f : c.x * b.w;
-      const float2 z2 = bc2(0.f);
-      EntrySums2 e2{z2, z2, z2, z2, z2, z2, z2, z2};
+      static_assert(kPairs == 2, "two pixel pairs per thread");
+      EntrySums2 e2;
       if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
-#pragma unroll
-        for (int k = 0; k < kPairs; ++k)
-          pair_grad2<NUP, true>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+        pair_grad2<NUP, true, true>(q[0], dx[0], h[0], b, c, einu, e2, inc[0], inc[1]);
+        pair_grad2<NUP, true, false>(q[1], dx[1], h[1], b, c, einu, e2, inc[2], inc[3]);
       } else {
-#pragma unroll
-        for (int k = 0; k < kPairs; ++k)
-          pair_grad2<NUP, false>(q[k], dx[k], h[k], b, c, einu, e2, inc[2 * k], inc[2 * k + 1]);
+        pair_grad2<NUP, false, true>(q[0], dx[0], h[0], b, c, einu, e2, inc[0], inc[1]);
+        pair_grad2<NUP, false, false>(q[1], dx[1], h[1], b, c, einu, e2, inc[2], inc[3]);
       }
       // geometry: the five moments sum dh (dx, dy, dx^2, dx dy, dy^2); the
       // linear map to d mu2D (through the conic) is applied once per record
