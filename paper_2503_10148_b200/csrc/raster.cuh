@@ -26,11 +26,11 @@ constexpr int kLanesPerRow = kWarpW / kPX;
 #define SSS_FWD_MINB 20  // 48 registers: 40 warps per SM (measured: -7% vs 56 registers)
 #endif
 #ifndef SSS_BWD_MINB
-// bwd: <= 113 registers — no spills and the pixel coordinates stay in
-// registers (measured -5% vs 14 CTAs at 72 registers, where ptxas
-// rematerialises them every entry); deferring the warp reduction by one
-// entry to overlap it with the next entry measured +9%
-#define SSS_BWD_MINB 9
+// bwd: <= 93 registers (80 + 8 B of stack): 11 CTAs/SM, -0.6% vs 10 CTAs at
+// 90 registers (with the lane constants opaque the loop needs fewer live
+// values); deferring the warp reduction by one entry to overlap it with the
+// next entry measured +9%
+#define SSS_BWD_MINB 11
 #endif
 constexpr int kFwdMinBlocks = SSS_FWD_MINB;
 constexpr int kBwdMinBlocks = SSS_BWD_MINB;
