@@ -351,6 +351,11 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
       const int T = __shfl_sync(full, incl, 31);
       const int excl = incl - n_i;
       if (act) S.rec[lane].excl = excl;
+      // window bit of this rank's first instance: shl.b32 clamps shift
+      // counts >= 32 to a zero result, so one shift covers "outside the
+      // window" (below it the unsigned difference wraps); inactive ranks
+      // start far beyond any window
+      const uint32_t start_t = act ? (uint32_t)excl : 0x40000000u;
       // covering ranks per bin column / row, over the step's union rect
       const int ux0 = (int)__reduce_min_sync(full, act ? (unsigned)cbx0 : 0xffffu);
       const int ux1 = (int)__reduce_max_sync(full, act ? (unsigned)cbx1 : 0u);
@@ -367,7 +372,8 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
       __syncwarp();
       int base = 0;  // ranks starting before the window
       for (int t0 = 0; t0 < T; t0 += 32) {
-        const unsigned bit = (act && excl >= t0 && excl < t0 + 32) ? 1u << (excl - t0) : 0u;
+        unsigned bit;
+        asm("shl.b32 %0, 1, %1;" : "=r"(bit) : "r"(start_t - (uint32_t)t0));
         const unsigned B = __reduce_or_sync(full, bit);
         const int own = base + __popc(B & ((2u << lane) - 1u)) - 1;
         base += __popc(B);
