@@ -68,11 +68,40 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, cons
   }
 }
 
+// The cameras as the fp64 geometry uses them: converted to double once on the
+// host (exact), so the per-view loop does no float->double conversions
+// (F2F.F64.F32 runs on the XU pipe with the fp64 divisions and square roots).
+struct DevCameraD {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy, z_near;
+  float center[3];  // fp32 (the SH view direction is fp32)
+  float pad;
+};
+struct CamPackD {
+  int n, width, height, tiles_x, tiles_y;
+  DevCameraD cam[kMaxViewsPerLaunch];
+};
+static_assert(sizeof(CamPackD) < 32000, "kernel parameter space");
+
+void fill_campack_d(const CamPack& f, int nv, CamPackD& d) {
+  d.n = nv; d.width = f.width; d.height = f.height; d.tiles_x = f.tiles_x; d.tiles_y = f.tiles_y;
+  for (int k = 0; k < nv; ++k) {
+    const DevCamera& c = f.cam[k];
+    DevCameraD& o = d.cam[k];
+    for (int i = 0; i < 9; ++i) o.R[i] = (double)c.R[i];
+    for (int i = 0; i < 3; ++i) o.t[i] = (double)c.t[i];
+    o.fx = c.fx; o.fy = c.fy; o.cx = c.cx; o.cy = c.cy; o.z_near = c.z_near;
+    for (int i = 0; i < 3; ++i) o.center[i] = c.center[i];
+    o.pad = 0.f;
+  }
+}
+
 template <int DEG>
 #ifndef SSS_PROJ_MINB
 #define SSS_PROJ_MINB 4  // 128 registers, 16 warps/SM (measured -20% vs 160 registers)
 #endif
-__global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params P, const __grid_constant__ CamPack cp,
+__global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params P, const __grid_constant__ CamPackD cp,
                                                        int nv, int v0, float4* __restrict__ rec,
                                                        float* __restrict__ depth,
                                                        short4* __restrict__ rect) {
@@ -131,16 +160,16 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
   const bool lowpass = P.variant & SSS_VARIANT_LOWPASS;
 
   for (int vv = 0; vv < nv; ++vv) {
-    const DevCamera& cam = cp.cam[vv];
+    const DevCameraD& cam = cp.cam[vv];
     const int64_t o_idx = (int64_t)(v0 + vv) * n + i;
     double p[3];
     for (int a = 0; a < 3; ++a)
-      p[a] = (((double)cam.R[a * 3 + 0] * mu[0] + (double)cam.R[a * 3 + 1] * mu[1]) +
-              (double)cam.R[a * 3 + 2] * mu[2]) + (double)cam.t[a];
+      p[a] = ((cam.R[a * 3 + 0] * mu[0] + cam.R[a * 3 + 1] * mu[1]) +
+              cam.R[a * 3 + 2] * mu[2]) + cam.t[a];
     depth[o_idx] = (float)p[2];
     short4 rr = make_short4(1, 1, 0, 0);  // culled
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
-    bool vis = opaque_enough && (p[2] > (double)cam.z_near);
+    bool vis = opaque_enough && (p[2] > cam.z_near);
     if (vis) {
       const double px = p[0], py = p[1], pz = p[2];
       const double fx = cam.fx, fy = cam.fy;
@@ -150,12 +179,12 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
       double T1[9], Sc[9];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
-          T1[a * 3 + b] = ((double)cam.R[a * 3 + 0] * vi.Sig[0 * 3 + b] + (double)cam.R[a * 3 + 1] * vi.Sig[1 * 3 + b]) +
-                          (double)cam.R[a * 3 + 2] * vi.Sig[2 * 3 + b];
+          T1[a * 3 + b] = (cam.R[a * 3 + 0] * vi.Sig[0 * 3 + b] + cam.R[a * 3 + 1] * vi.Sig[1 * 3 + b]) +
+                          cam.R[a * 3 + 2] * vi.Sig[2 * 3 + b];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
-          Sc[a * 3 + b] = (T1[a * 3 + 0] * (double)cam.R[b * 3 + 0] + T1[a * 3 + 1] * (double)cam.R[b * 3 + 1]) +
-                          T1[a * 3 + 2] * (double)cam.R[b * 3 + 2];
+          Sc[a * 3 + b] = (T1[a * 3 + 0] * cam.R[b * 3 + 0] + T1[a * 3 + 1] * cam.R[b * 3 + 1]) +
+                          T1[a * 3 + 2] * cam.R[b * 3 + 2];
       double K2[6];
       for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 3; ++b)
@@ -169,8 +198,8 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
       }
       const double det = cxx * cyy - cxy * cxy;
       const double A = cyy / det, B = -cxy / det, C = cxx / det;
-      const double mx = (fx * px) / pz + (double)cam.cx;
-      const double my = (fy * py) / pz + (double)cam.cy;
+      const double mx = (fx * px) / pz + cam.cx;
+      const double my = (fy * py) / pz + cam.cy;
       const float mx_f = (float)mx, my_f = (float)my;
       const float A_f = (float)A, B2_f = (float)(2.0 * B), C_f = (float)C;
       vis = ((float)det > 0.0f) && isfinite(mx_f) && isfinite(my_f) && isfinite(A_f) &&
@@ -229,8 +258,10 @@ extern "C" sss_status sss_project(const sss_params* p, const sss_camera* cams, i
   // launch), so the call allocates nothing and is CUDA-graph capturable.
   for (int v0 = 0; v0 < n_views; v0 += kMaxViewsPerLaunch) {
     const int nv = n_views - v0 < kMaxViewsPerLaunch ? n_views - v0 : kMaxViewsPerLaunch;
-    CamPack cp;
-    fill_campack(cams, v0, nv, cp);
+    CamPack cpf;
+    fill_campack(cams, v0, nv, cpf);
+    static thread_local CamPackD cp;  // ~19 KB: kept off the stack
+    fill_campack_d(cpf, nv, cp);
     float4* rec = (float4*)out->rec;
     short4* rect = (short4*)out->rect;
     switch (p->sh_degree) {
