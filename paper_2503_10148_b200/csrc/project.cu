@@ -61,9 +61,11 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, cons
     Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
     K = 16;
   }
+  // colour is not discrete-feeding: fused multiply-adds (explicit, this file
+  // is compiled with -fmad=false for the fp64 geometry)
   for (int c = 0; c < 3; ++c) {
     float acc = 0.f;
-    for (int m = 0; m < K; ++m) acc += sh[m * 3 + c] * Y[m];
+    for (int m = 0; m < K; ++m) acc = __fmaf_rn(sh[m * 3 + c], Y[m], acc);
     out[c] = fmaxf(acc + 0.5f, 0.f);
   }
 }
