@@ -424,7 +424,7 @@ __device__ __forceinline__ void sh_dir_grad(int deg, float x, float y, float z, 
 
 template <int DEG>
 #ifndef SSS_PROJB_MINB
-#define SSS_PROJB_MINB 4  // 128 registers (measured -12% vs 189)
+#define SSS_PROJB_MINB 3  // 168 registers (80 B spilled at degree 3, 432 B at 4 CTAs/SM): -0.7 ms per 64 views
 #endif
 __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_params P, const __grid_constant__ CamPack cp,
                                                            int nv, int v0, float2* __restrict__ g2d,
