@@ -122,6 +122,43 @@ __global__ void keys_init_kernel(const float* __restrict__ depth, const short4* 
   }
 }
 
+// The same with four consecutive components per thread and 16-byte accesses
+// (n % 4 == 0: every view's segment starts 16-byte aligned).
+__global__ void keys_init4_kernel(const float4* __restrict__ depth, const int4* __restrict__ rect,
+                                  int64_t n, uint4* __restrict__ keys, int4* __restrict__ vals,
+                                  int32_t* __restrict__ n_vis) {
+  const int v = blockIdx.y;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // quad index in the view
+  const int64_t nq = n >> 2;
+  int cnt = 0;
+  if (q < nq) {
+    const int64_t o = (int64_t)v * nq + q;
+    const int4 r01 = rect[2 * o], r23 = rect[2 * o + 1];  // two short4 per int4
+    const float4 d = depth[o];
+    // short4 {x0, y0, x1, y1}: visible iff x0 <= x1 (low halves of words 0 and 1)
+    const bool v0 = (short)(r01.x & 0xffff) <= (short)(r01.y & 0xffff);
+    const bool v1 = (short)(r01.z & 0xffff) <= (short)(r01.w & 0xffff);
+    const bool v2 = (short)(r23.x & 0xffff) <= (short)(r23.y & 0xffff);
+    const bool v3 = (short)(r23.z & 0xffff) <= (short)(r23.w & 0xffff);
+    keys[o] = make_uint4(v0 ? __float_as_uint(d.x) : 0xFFFFFFFFu, v1 ? __float_as_uint(d.y) : 0xFFFFFFFFu,
+                         v2 ? __float_as_uint(d.z) : 0xFFFFFFFFu, v3 ? __float_as_uint(d.w) : 0xFFFFFFFFu);
+    const int32_t i0 = (int32_t)(4 * q);
+    vals[o] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+    cnt = (int)v0 + (int)v1 + (int)v2 + (int)v3;
+  }
+  __shared__ int32_t wsum[8];
+  int c = cnt;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if (lane_id() == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
+    if (s) atomicAdd(&n_vis[v], s);
+  }
+}
+
 // ------------------------------------------------------- bin histograms
 __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0, int& bx1, int& by1) {
   bx0 = r.x >> shift; by0 = r.y >> shift; bx1 = r.z >> shift; by1 = r.w >> shift;
@@ -568,8 +605,14 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   cudaMemsetAsync(out->overflow, 0, sizeof(int32_t), s);
   cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   if (n > 0) {
-    dim3 gi(div_up(n, 256), n_views);
-    keys_init_kernel<<<gi, 256, 0, s>>>(pr->depth, rect, n, keys_a, vals_a, n_vis);
+    if (n % 4 == 0) {
+      const dim3 gi(div_up(n / 4, 256), n_views);
+      keys_init4_kernel<<<gi, 256, 0, s>>>((const float4*)pr->depth, (const int4*)rect, n, (uint4*)keys_a,
+                                           (int4*)vals_a, n_vis);
+    } else {
+      const dim3 gi(div_up(n, 256), n_views);
+      keys_init_kernel<<<gi, 256, 0, s>>>(pr->depth, rect, n, keys_a, vals_a, n_vis);
+    }
     count_launch();
     const dim3 gr(L.tiles_per_view, n_views);
     radix_sort_pairs(keys_a, vals_a, keys_b, vals_b, n, n_views, L.tiles_per_view, rhist, s);

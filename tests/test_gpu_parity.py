@@ -121,6 +121,26 @@ def test_scatter_staged_and_direct_paths_agree(orc, sss, shift):
         assert np.array_equal(ref.ids[0, :M].cpu().numpy(), ids)
 
 
+@pytest.mark.parametrize("n", [1001, 1002, 1003, 1004])
+def test_bin_sort_any_component_count(orc, sss, n):
+    """Component counts with n % 4 != 0 take the scalar key initialisation
+    (n % 4 == 0: four components per thread, 16-byte accesses); both give
+    the oracle's lists bit for bit."""
+    from gpu_helpers import to_dev
+
+    sc = make_custom_scene(n, 1, 200, 133, seed=47)
+    params = to_dev(sc)
+    pr = sss.sss_project(params, sc.cameras)
+    bins = sss.sss_bin_sort(pr, sc.cameras, bin_shift=0)
+    assert not sss.sss_check_overflow(bins)
+    counts, ids, _ = orc.bin_sort(sc.params, sc.sh_degree, sc.cameras[0])
+    M = len(ids)
+    assert int(bins.totals[0].item()) == M
+    rg = bins.ranges[0].cpu().numpy()
+    assert np.array_equal(rg[:, 1] - rg[:, 0], counts)
+    assert np.array_equal(bins.ids[0, :M].cpu().numpy(), ids)
+
+
 def test_scatter_large_rects_bit_exact(orc, sss):
     """Components covering most of a 1297x840 view (rects of up to 82 x 53
     tiles): the flattened walk's rank/bin arithmetic (division of the
