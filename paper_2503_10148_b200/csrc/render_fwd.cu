@@ -129,9 +129,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
     if (__syncthreads_count(!all_done()) == 0) break;
     if (threadIdx.x == 0) SSS_COUNT(0, 1);
-    unsigned cm[kBatch / 32];  // REC: this warp's composited entries (warp-uniform bits)
-#pragma unroll
-    for (int q = 0; q < kBatch / 32; ++q) cm[q] = 0u;
+    static_assert(kBatch == 64, "one 64-bit composited mask per batch");
+    unsigned long long cm = 0ull;  // REC: this warp's composited entries (warp-uniform bits)
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? idv[pos] : 0;
@@ -196,10 +195,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       }
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
-        if (REC) {
-#pragma unroll
-          for (int q = 0; q < kBatch / 32; ++q) cm[q] |= (j >> 5) == q ? 1u << (j & 31) : 0u;
-        }
+        if (REC) cm |= 1ull << j;
         const float4 c = sc[j];  // {e, r, g, b}
         const int32_t pj1 = spos[j] + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
@@ -223,9 +219,10 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     if (REC) {  // spos is rewritten only after the next top barrier
 #pragma unroll
       for (int q = 0; q < kBatch / 32; ++q) {
-        const int slot = n_rec + __popc(cm[q] & lt);
-        if (((cm[q] >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
-        n_rec += __popc(cm[q]);
+        const unsigned cq = (unsigned)(cm >> (32 * q));
+        const int slot = n_rec + __popc(cq & lt);
+        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
+        n_rec += __popc(cq);
       }
     }
   }
