@@ -304,7 +304,7 @@ struct alignas(16) WalkRec {  // one of the step's (compacted) components
   int32_t excl;               // first instance index of the component in the step
   int32_t id;
   uint32_t packed;            // bx0 | by0 << 10 | (width - 1) << 20 (bins)
-  float inv_w;                // 1 / width, correctly rounded
+  uint32_t magic;             // ceil(2^31 / width): floor(k / w) = umulhi(2k, magic) for k, w < 2^15
 };
 struct alignas(16) WalkScratch {
   WalkRec rec[32];
@@ -322,8 +322,8 @@ struct alignas(16) WalkScratch {
 //   Instance t belongs to the rank whose first index excl is the last one
 //   <= t: a bit mask of the rank starts inside the 32-instance window
 //   (one OR-reduction) and a popcount give it.  Its bin comes from the
-//   rank's rect (division by the rect width through a correctly rounded
-//   reciprocal: exact for k < 2^20).
+//   rank's rect (division by the rect width as a multiply-high with
+//   ceil(2^31 / w): exact for k, w < 2^15; k < SSS_MAX_BINS).
 //   The slot of (rank r, bin b) is wbase[b] + the number of lower ranks
 //   covering b — a popcount of per-column and per-row rank ballots — so
 //   bins receive their entries in depth order without 64-bit keys or
@@ -375,7 +375,7 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
         WalkRec rr;
         rr.id = st.z;
         rr.packed = (uint32_t)cbx0 | ((uint32_t)cby0 << 10) | ((uint32_t)(wd - 1) << 20);
-        rr.inv_w = __frcp_rn((float)wd);
+        rr.magic = (uint32_t)((0x80000000ull + (uint64_t)wd - 1) / (uint64_t)wd);
         S.rec[lane] = rr;  // excl below
         if (kv) S.dbits[lane] = (uint32_t)st.w;
       }
@@ -420,7 +420,7 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
         if (t < T) {
           const WalkRec R = S.rec[own];
           const int k = t - R.excl;
-          const int q = (int)(((float)k + 0.5f) * R.inv_w);
+          const int q = (int)__umulhi(2u * (uint32_t)k, R.magic);
           const int wd = (int)(R.packed >> 20) + 1;
           const int bx = (int)(R.packed & 1023u) + (k - q * wd);
           const int by = (int)((R.packed >> 10) & 1023u) + q;
