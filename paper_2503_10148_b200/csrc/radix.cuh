@@ -148,24 +148,40 @@ __global__ void __launch_bounds__(kRadixThreads, SSS_RADIX_MINB) radix_onesweep_
   const int32_t* vin = vals_in + (int64_t)v * n;
   uint32_t key[kRadixItems];
   uint32_t loc[kRadixItems];
-#pragma unroll
-  for (int c = 0; c < kRadixItems; ++c) {
-    const int64_t i = base + c * 32 + lane;
-    key[c] = i < n ? kin[i] : 0xFFFFFFFFu;
-  }
   const unsigned lt = (1u << lane) - 1u;
+  const bool full = tbase + kRadixTile <= n;  // every tile but a segment's last: no bounds checks
+  if (full) {
 #pragma unroll
-  for (int c = 0; c < kRadixItems; ++c) {
-    const int64_t i = base + c * 32 + lane;
-    const bool ok = i < n;
-    const unsigned d = (key[c] >> shift) & 255u;
-    const unsigned valid = __ballot_sync(0xffffffffu, ok);
-    const unsigned pm = peers_of(d) & valid;
-    const uint32_t before = ok ? run[w][d] : 0u;
-    loc[c] = before + __popc(pm & lt);
-    __syncwarp();
-    if (ok && (pm & lt) == 0) run[w][d] = before + __popc(pm);
-    __syncwarp();
+    for (int c = 0; c < kRadixItems; ++c) key[c] = kin[base + c * 32 + lane];
+#pragma unroll
+    for (int c = 0; c < kRadixItems; ++c) {
+      const unsigned d = (key[c] >> shift) & 255u;
+      const unsigned pm = peers_of(d);
+      const uint32_t before = run[w][d];
+      loc[c] = before + __popc(pm & lt);
+      __syncwarp();
+      if ((pm & lt) == 0) run[w][d] = before + __popc(pm);
+      __syncwarp();
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < kRadixItems; ++c) {
+      const int64_t i = base + c * 32 + lane;
+      key[c] = i < n ? kin[i] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int c = 0; c < kRadixItems; ++c) {
+      const int64_t i = base + c * 32 + lane;
+      const bool ok = i < n;
+      const unsigned d = (key[c] >> shift) & 255u;
+      const unsigned valid = __ballot_sync(0xffffffffu, ok);
+      const unsigned pm = peers_of(d) & valid;
+      const uint32_t before = ok ? run[w][d] : 0u;
+      loc[c] = before + __popc(pm & lt);
+      __syncwarp();
+      if (ok && (pm & lt) == 0) run[w][d] = before + __popc(pm);
+      __syncwarp();
+    }
   }
   __syncthreads();
   // per digit d (thread d): prefix over warps, tile count, tile-local start,
@@ -204,7 +220,7 @@ __global__ void __launch_bounds__(kRadixThreads, SSS_RADIX_MINB) radix_onesweep_
 #pragma unroll
   for (int c = 0; c < kRadixItems; ++c) {
     const int64_t i = base + c * 32 + lane;
-    if (i < n) {
+    if (full || i < n) {
       const unsigned d = (key[c] >> shift) & 255u;
       const uint32_t lp = run[w][d] + loc[c];
       skey[lp] = key[c];
