@@ -537,27 +537,29 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
     const float GS[4] = {GS00, GS01, GS01, GS11};
     // dL/dSc = J^T GS J ; dL/dJ = 2 GS J Sc
     float GSc[9];
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) {
-        float acc = 0.f;
-        for (int k = 0; k < 2; ++k)
-          for (int l = 0; l < 2; ++l) acc += J[k * 3 + a] * GS[k * 2 + l] * J[l * 3 + b];
-        GSc[a * 3 + b] = acc;
-      }
+    {
+      float U[6];  // GS J (2x3), then GSc = J^T (GS J)
+      for (int k = 0; k < 2; ++k)
+        for (int b = 0; b < 3; ++b) U[k * 3 + b] = GS[k * 2 + 0] * J[0 * 3 + b] + GS[k * 2 + 1] * J[1 * 3 + b];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) GSc[a * 3 + b] = J[0 * 3 + a] * U[0 * 3 + b] + J[1 * 3 + a] * U[1 * 3 + b];
+    }
     float JS[6];
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 3; ++b) JS[a * 3 + b] = J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b] + J[a * 3 + 2] * Sc[2 * 3 + b];
     float GJ[6];
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 3; ++b) GJ[a * 3 + b] = 2.f * (GS[a * 2 + 0] * JS[0 * 3 + b] + GS[a * 2 + 1] * JS[1 * 3 + b]);
-    // dL/dSigma += Rc^T GSc Rc
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) {
-        float acc = 0.f;
-        for (int k = 0; k < 3; ++k)
-          for (int l = 0; l < 3; ++l) acc += cam.R[k * 3 + a] * GSc[k * 3 + l] * cam.R[l * 3 + b];
-        gSig[a * 3 + b] += acc;
-      }
+    // dL/dSigma += Rc^T (GSc Rc): two 3x3 products (54 FMAs instead of 81 triple terms)
+    {
+      float T2[9];
+      for (int k = 0; k < 3; ++k)
+        for (int b = 0; b < 3; ++b)
+          T2[k * 3 + b] = GSc[k * 3 + 0] * cam.R[0 * 3 + b] + GSc[k * 3 + 1] * cam.R[1 * 3 + b] + GSc[k * 3 + 2] * cam.R[2 * 3 + b];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          gSig[a * 3 + b] += cam.R[0 * 3 + a] * T2[0 * 3 + b] + cam.R[1 * 3 + a] * T2[1 * 3 + b] + cam.R[2 * 3 + a] * T2[2 * 3 + b];
+    }
     // camera-space mean through mean2d and J(p)
     const float dmx = -2.f * (QA * G0.x + QB * G0.y), dmy = -2.f * (QB * G0.x + QC * G0.y);
     const float iz2 = iz * iz, iz3 = iz2 * iz;
