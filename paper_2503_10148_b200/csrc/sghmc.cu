@@ -144,27 +144,65 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   } else {
     for (int a = 0; a < 3; ++a) noise[a] = eta * xi[a];
   }
+  // every load of the three mean planes before the first store (see adam_planes)
+  const bool need_mv = hp.g_adam || hp.mu_mode == 2;
+  float pm[3], gm[3], mo[3], vo[3], rm[3];
+  bool onm[3];
+#pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (!mine(a)) continue;
+    onm[a] = mine(a);
+    if (!onm[a]) continue;
     const int64_t idx = a * n + i;
-    const float graw = Gr.mean[idx] * hp.grad_scale;
+    pm[a] = P.mean[idx];
+    gm[a] = Gr.mean[idx];
+    if (need_mv) {
+      mo[a] = Mo.mean[idx];
+      vo[a] = Vo.mean[idx];
+    }
+    if (hp.mu_mode != 2) rm[a] = r[idx];
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (!onm[a]) continue;
+    const int64_t idx = a * n + i;
+    const float graw = gm[a] * hp.grad_scale;
+    float dir = 0.f;
+    if (need_mv) {  // Adam direction, as adam_dir
+      const float mm = hp.beta1 * mo[a] + (1.f - hp.beta1) * graw;
+      const float vv = hp.beta2 * vo[a] + (1.f - hp.beta2) * graw * graw;
+      Mo.mean[idx] = mm;
+      Vo.mean[idx] = vv;
+      dir = (mm * hp.inv_b1t) / (sqrtf(vv * hp.inv_b2t) + hp.adam_eps);
+    }
     if (hp.mu_mode == 2) {  // setting 1: Adam on the means, no sampler state
-      P.mean[idx] -= eps * adam_dir(graw, Mo.mean, Vo.mean, idx, hp);
+      P.mean[idx] = pm[a] - eps * dir;
       continue;
     }
-    const float g = hp.g_adam ? adam_dir(graw, Mo.mean, Vo.mean, idx, hp) : graw;
-    const float ra = r[idx];
+    const float g = hp.g_adam ? dir : graw;
+    const float ra = rm[a];
     const float F = (hp.burn_in || hp.mu_mode == 1) ? 0.f : eps * (1.f - eps * Cf) * ra;
-    P.mean[idx] = P.mean[idx] - eps * eps * g + gate * (F + noise[a]);
+    P.mean[idx] = pm[a] - eps * eps * g + gate * (F + noise[a]);
     r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
   }
   // ---- Adam on the other groups
   adam_planes<3, true>(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, i, n, 0, 3, 3, hp.lr_group[0], hp);
   adam_planes<4>(P.rot, Gr.rot, Mo.rot, Vo.rot, i, n, 0, 4, 6, hp.lr_group[1], hp);
-  if (mine(10)) adam_plane(P.raw_nu, Gr.raw_nu, Mo.raw_nu, Vo.raw_nu, i, hp.lr_group[2], hp);
-  if (mine(11)) {
+  {  // raw nu and raw opacity: both planes' loads before the stores
+    const bool on_nu = mine(10), on_o = mine(11);
+    float t2[2] = {0.f, 0.f}, g2[2] = {0.f, 0.f}, m2[2] = {0.f, 0.f}, v2[2] = {0.f, 0.f};
+    if (on_nu) { t2[0] = P.raw_nu[i]; g2[0] = Gr.raw_nu[i]; m2[0] = Mo.raw_nu[i]; v2[0] = Vo.raw_nu[i]; }
+    if (on_o) { t2[1] = P.raw_opacity[i]; g2[1] = Gr.raw_opacity[i]; m2[1] = Mo.raw_opacity[i]; v2[1] = Vo.raw_opacity[i]; }
     const float reg_o = hp.eps_o * (o > 0.f ? 1.f : (o < 0.f ? -1.f : 0.f)) * (positive ? o * (1.f - o) : 1.f - o * o);
-    adam_plane(P.raw_opacity, Gr.raw_opacity, Mo.raw_opacity, Vo.raw_opacity, i, hp.lr_group[3], hp, reg_o);
+    auto step = [&](int k, float reg, float lr, float* theta, float* m, float* v) {  // as adam_plane
+      const float g = fmaf(g2[k], hp.grad_scale, reg);
+      const float mm = hp.beta1 * m2[k] + (1.f - hp.beta1) * g;
+      const float vv = hp.beta2 * v2[k] + (1.f - hp.beta2) * g * g;
+      m[i] = mm;
+      v[i] = vv;
+      theta[i] = t2[k] - lr * ((mm * hp.inv_b1t) / (sqrtf(vv * hp.inv_b2t) + hp.adam_eps));
+    };
+    if (on_nu) step(0, 0.f, hp.lr_group[2], P.raw_nu, Mo.raw_nu, Vo.raw_nu);
+    if (on_o) step(1, reg_o, hp.lr_group[3], P.raw_opacity, Mo.raw_opacity, Vo.raw_opacity);
   }
   for (int k = 0; k < 3 * K; k += kShBatch)
     adam_planes<kShBatch>(P.sh, Gr.sh, Mo.sh, Vo.sh, i, n, k, min(k + kShBatch, 3 * K), 12, hp.lr_group[4], hp);
