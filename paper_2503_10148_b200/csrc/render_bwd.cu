@@ -423,6 +423,9 @@ __device__ __forceinline__ void sh_dir_grad(int deg, float x, float y, float z, 
 }
 
 template <int DEG>
+#ifndef SSS_PROJB_L2_AHEAD
+#define SSS_PROJB_L2_AHEAD 1  // L2 prefetch of the record two views on (-3.5% project_bwd)
+#endif
 #ifndef SSS_PROJB_MINB
 #define SSS_PROJB_MINB 3  // 168 registers (80 B spilled at degree 3, 432 B at 4 CTAs/SM): -0.7 ms per 64 views
 #endif
@@ -489,6 +492,10 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
       const float2* gq = gp + (int64_t)n * 5;
 #pragma unroll
       for (int k = 0; k < 5; ++k) N[k] = __ldcs(gq + k);
+#if SSS_PROJB_L2_AHEAD
+      if (vv + 1 + SSS_PROJB_L2_AHEAD < nv)  // the record SSS_PROJB_L2_AHEAD views further on, into L2
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(gq + (int64_t)n * 5 * SSS_PROJB_L2_AHEAD));
+#endif
     }
     const bool nz = (G0.x != 0.f) | (G0.y != 0.f) | (G0.z != 0.f) | (G0.w != 0.f) | (G1.x != 0.f) |
                     (G1.y != 0.f) | (G1.z != 0.f) | (G1.w != 0.f) | (G2.x != 0.f) | (G2.y != 0.f);
