@@ -407,7 +407,10 @@ void build_view(const orc_params* P, const orc_cam& cam, View& v, bool bin) {
   }
   v.order.clear();
   for (int64_t i = 0; i < n; ++i)
-    if (v.pr[i].cull == 0 && v.pr[i].n_tiles > 0) v.order.push_back((int)i);
+    // every component the inclusion test may accept: visible ones (cull 0)
+    // and those whose tile AABB misses the image (cull 4, no tiles) -- the
+    // brute force tests them too, so a non-conservative rect would show
+    if (v.pr[i].cull == 0 || v.pr[i].cull == 4) v.order.push_back((int)i);
   // R8: global per-view order by fp32 camera depth, ties by component index
   std::stable_sort(v.order.begin(), v.order.end(), [&](int a, int b) {
     if (v.pr[a].depth_f != v.pr[b].depth_f) return v.pr[a].depth_f < v.pr[b].depth_f;
@@ -428,8 +431,18 @@ struct Entry {
   bool clamped;
 };
 
-// The included sequence of one pixel (Eq. 7 with R9-R11).  mode 0: brute
-// force over all visible components; 1: the pixel's tile list; 2: frozen list.
+// The included sequence of one pixel (Eq. 7 with R9-R11).
+//   mode 0 (brute force): every visible component in (depth, index) order
+//     (R8), included iff its fp32 h at the pixel centre is <= hmax (R9) --
+//     no tile rect, no tile list: the plain per-pixel definition;
+//   mode 1 (tiled): the pixel's tile list (components whose tile rect covers
+//     the tile, same order), the same h test -- the acceleration the GPU
+//     mirrors; mode 0 == mode 1 bit for bit is the pin that the rect is
+//     conservative (tests/test_oracle_pins.py);
+//   mode 2: a frozen list (every listed component included, no stop test).
+// Stop rule (R11): the component that drives W below 1e-4
+// is composited, then the pixel stops; nothing after it is considered, even
+// a negative component that would re-grow W.
 void pixel_list(const View& v, int x, int y, int mode, const int32_t* frozen, int cap,
                 std::vector<Entry>& out, double* tie) {
   out.clear();
@@ -438,10 +451,10 @@ void pixel_list(const View& v, int x, int y, int mode, const int32_t* frozen, in
   const int tx = x / kTile, ty = y / kTile;
   double W = 1.0;
   double tmin = std::numeric_limits<double>::infinity();
-  auto consider = [&](int i, bool gated) -> bool {  // returns true to stop
+  auto consider = [&](int i, int gate) -> bool {  // gate: 0 none, 1 h test, 2 rect + h test; true = stop
     const Proj& r = v.pr[i];
-    if (gated) {
-      if (!(tx >= r.rect[0] && tx <= r.rect[2] && ty >= r.rect[1] && ty <= r.rect[3])) return false;
+    if (gate == 2 && !(tx >= r.rect[0] && tx <= r.rect[2] && ty >= r.rect[1] && ty <= r.rect[3])) return false;
+    if (gate >= 1) {
       const float h32 = h_f32(pxf, pyf, r);
       if (!(h32 <= r.hmax_f)) return false;
     }
@@ -458,17 +471,17 @@ void pixel_list(const View& v, int x, int y, int mode, const int32_t* frozen, in
     out.push_back(e);
     W = W * (1.0 - e.alpha);
     tmin = std::min(tmin, std::fabs(W - kWStop) / kWStop);
-    return gated && W < kWStop;
+    return gate >= 1 && W < kWStop;
   };
   if (mode == 2) {
     const int32_t* L = frozen + ((size_t)y * v.W + x) * cap;
-    for (int k = 0; k < cap && L[k] >= 0; ++k) consider(L[k], false);
+    for (int k = 0; k < cap && L[k] >= 0; ++k) consider(L[k], 0);
   } else if (mode == 1) {
     for (int i : v.tiles[(size_t)ty * v.tw + tx])
-      if (consider(i, true)) break;
+      if (consider(i, 2)) break;
   } else {
     for (int i : v.order)
-      if (consider(i, true)) break;
+      if (consider(i, 1)) break;
   }
   if (tie) *tie = tmin;
 }

@@ -12,6 +12,8 @@ from .scenes import (  # noqa: F401
     CONFIG_NAMES,
     make_scene,
     make_custom_scene,
+    make_stress_scene,
+    make_stop_rule_scene,
     make_optimizer_state,
     sghmc_params_for,
     make_targets,

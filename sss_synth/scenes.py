@@ -282,6 +282,81 @@ def make_custom_scene(n: int, sh_degree: int, width: int, height: int, n_views: 
                  name=f"custom_n{n}_d{sh_degree}_{width}x{height}_v{n_views}")
 
 
+def make_stress_scene(n: int = 600, sh_degree: int = 1, width: int = 157, height: int = 119,
+                      seed: int = 5, n_views: int = 1) -> Scene:
+    """Edge-case components for the binning / inclusion parity cases: a mix of
+    huge (log-scale U[-1.2, -0.4]), strongly elongated (one axis up to e^3.8
+    ~ 45x the others), off-image (means outside the view frustum, so only a
+    fat tail reaches the frame), near-plane (camera depth 0.25-0.8) and
+    ordinary components, with nu from {1.001, U[1, 16], 200, 5000}, |o| in
+    U(0.002, 0.999) (below the 1/255 visibility level and up to the alpha
+    clamp) and 30 % negative.  Ragged frame (157 x 119: partial tiles).
+    Inputs only; nothing of the method is evaluated here."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    params = make_params(rng, n, sh_degree, "uniform", 8.0, 0.3).astype(np.float64)
+    cams = make_cameras("single" if n_views == 1 else "ring", n_views, width, height)
+    cam = cams[0]
+    R = cam.R.astype(np.float64)
+    cpos = -(R.T @ cam.t.astype(np.float64))
+    kind = rng.integers(0, 5, n)
+    for i in range(n):
+        k = kind[i]
+        if k == 0:    # huge
+            params[3:6, i] = rng.uniform(-1.2, -0.4, 3)
+        elif k == 1:  # elongated: one long axis, two short
+            ax = rng.integers(0, 3)
+            ls = rng.uniform(-4.6, -3.8, 3)
+            ls[ax] = rng.uniform(-1.4, -0.8)
+            params[3:6, i] = ls
+        elif k == 2:  # off-image: a point in camera space beyond the frame edges
+            z = rng.uniform(2.5, 5.5)
+            xs = rng.choice([-1.0, 1.0]) * rng.uniform(0.55, 0.95) * z * cam.width / (2 * cam.fx)
+            ys = rng.uniform(-0.9, 0.9) * z * cam.height / (2 * cam.fy)
+            if rng.uniform() < 0.5:
+                xs, ys = rng.uniform(-0.9, 0.9) * z * cam.width / (2 * cam.fx), \
+                    rng.choice([-1.0, 1.0]) * rng.uniform(0.55, 0.95) * z * cam.height / (2 * cam.fy)
+            f = rng.uniform(1.1, 2.2)  # past the edge (some AABBs miss the frame)
+            pc = np.array([xs * f, ys * f, z])
+            params[0:3, i] = R.T @ pc + cpos
+            params[3:6, i] = rng.uniform(-2.5, -1.2, 3)
+        elif k == 3:  # near plane (a few behind it)
+            pc = np.array([rng.uniform(-0.1, 0.1), rng.uniform(-0.08, 0.08), rng.uniform(0.15, 0.8)])
+            params[0:3, i] = R.T @ pc + cpos
+            params[3:6, i] = rng.uniform(-4.5, -3.0, 3)
+        c = rng.integers(0, 4)
+        nu = [1.001, rng.uniform(1.0, 16.0), 200.0, 5000.0][c]
+        params[10, i] = _raw_from_nu(nu) if nu - 1.0 <= 30.0 else nu - 1.0
+        mag = rng.uniform(0.002, 0.999)
+        params[11, i] = np.arctanh(mag if rng.uniform() >= 0.3 else -mag)
+    return Scene(config=0, params=params.astype(np.float32), sh_degree=sh_degree, cameras=cams,
+                 seed=seed, name=f"stress_n{n}_d{sh_degree}_{width}x{height}")
+
+
+def make_stop_rule_scene(bg=(0.0, 0.0, 0.0)) -> Scene:
+    """Five co-located components on the optical axis of a 64 x 64 camera
+    whose principal point is a pixel centre (h = 0 there, so alpha = o):
+    opacities 0.98, 0.97, 0.9, -0.9, 0.5 front to back (depths 4.6 .. 5.0),
+    each with one pure colour channel pattern so a composited component shows
+    in the image.  Used for the R11 stop-rule pin."""
+    from math import atanh
+    n, deg = 5, 0
+    P = param_plane_count(deg)
+    params = np.zeros((P, n), np.float64)
+    ops = [0.98, 0.97, 0.9, -0.9, 0.5]
+    cols = [(1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0), (1.0, 1.0, 0.0), (1.0, 1.0, 1.0)]
+    for i in range(n):
+        params[0:3, i] = (0.0, 0.0, -0.4 + 0.1 * i)  # camera at z = -5: depth 4.6 + 0.1 i
+        params[3:6, i] = -1.0
+        params[6, i] = 1.0
+        params[10, i] = _raw_from_nu(4.0)
+        params[11, i] = atanh(ops[i])
+        params[12:15, i] = (np.asarray(cols[i]) - 0.5) * 2.0 * math.sqrt(math.pi)
+    cam = Camera(R=np.eye(3, dtype=np.float32), t=np.array([0.0, 0.0, 5.0], np.float32), fx=100.0,
+                 fy=100.0, cx=32.5, cy=32.5, width=64, height=64)
+    return Scene(config=0, params=params.astype(np.float32), sh_degree=deg, cameras=[cam],
+                 bg=np.asarray(bg, np.float32), seed=0, name="stop_rule")
+
+
 def make_targets(scene: Scene, views=None, seed_offset: int = 0) -> np.ndarray:
     """U[0,1] target images [len(views)][3][H][W] float32, seeded per view."""
     views = range(scene.n_views) if views is None else views

@@ -300,9 +300,19 @@ def _scenes_small():
 
 
 def test_tiled_equals_brute_force(orc):
-    """Tile lists are an acceleration of Eq. 7, not a change of it:
-    bit-identical fp64 images, transmittance and counts."""
-    for sc in _scenes_small():
+    """Tile lists are an acceleration of Eq. 7, not a change of it (SPEC.md:232,
+    659): bit-identical fp64 images, transmittance and counts.  The brute force
+    tests every component not culled (including those whose tile AABB misses
+    the frame) with the fp32 h <= hmax rule alone -- no tile rect -- so any
+    pair a non-conservative rect dropped would show here.  The stress scenes
+    carry huge, 45:1 elongated, off-image, near-plane, nu = 1 and nu = 5000
+    components on a ragged 157 x 119 frame."""
+    from sss_synth import make_stress_scene
+    stress = [make_stress_scene(seed=s, sh_degree=s % 4) for s in (5, 6, 7)]
+    for sc in stress:
+        pr = orc.project(sc.params, sc.sh_degree, sc.cameras[0])
+        assert np.sum(pr.cull == 4) > 10 and np.sum(pr.cull == 1) > 3  # AABB off-frame / behind
+    for sc in _scenes_small() + stress:
         for cam in sc.cameras:
             a = orc.render(sc.params, sc.sh_degree, cam, bg=(0.1, 0.2, 0.3), mode="brute")
             b = orc.render(sc.params, sc.sh_degree, cam, bg=(0.1, 0.2, 0.3), mode="tiled")
@@ -313,11 +323,99 @@ def test_tiled_equals_brute_force(orc):
 
 
 @pytest.mark.slow
-def test_tiled_equals_brute_force_config2_reduced(orc):
-    sc = make_scene(2, n=20000)
+def test_tiled_equals_brute_force_config2_full(orc):
+    """Config 2 at its stated size (100,000 components, 256 x 256, SH 3):
+    rect-free brute force == tiled, bit for bit (~11 s on 8 cores)."""
+    sc = make_scene(2)
+    assert sc.n == 100_000
     a = orc.render(sc.params, 3, sc.cameras[0], mode="brute")
     b = orc.render(sc.params, 3, sc.cameras[0], mode="tiled")
     assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.n_contrib, b.n_contrib)
+    assert np.array_equal(a.final_T, b.final_T)
+    assert a.n_contrib.mean() > 50
+
+
+def test_extreme_elongation_rect_stays_conservative(orc):
+    """Axis ratios up to e^11 (elongated splats seen from the side): the +1 px
+    AABB margin still covers every pixel the fp32 h test accepts."""
+    from sss_synth import make_stress_scene
+    sc = make_stress_scene(seed=3)
+    for ratio_log in (5, 9, 11):
+        p = sc.params.astype(np.float64)
+        p[3:6] = -4.0
+        p[3] = -4.0 + 0.5 * ratio_log
+        p[4] = -4.0 - 0.5 * ratio_log
+        p = p.astype(np.float32)
+        a = orc.render(p, sc.sh_degree, sc.cameras[0], mode="brute")
+        b = orc.render(p, sc.sh_degree, sc.cameras[0], mode="tiled")
+        assert a.n_contrib.max() > 0
+        assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.n_contrib, b.n_contrib)
+
+
+def test_stop_rule_pin(orc):
+    """R11 on a hand-derived pixel: five co-located
+    components with alpha = o (h = 0 at the principal point, T = 1):
+    0.98, 0.97, 0.9, -0.9, 0.5 front to back.  W = 1 -> 0.02 -> 6e-4 -> 6e-5:
+    the third component drives W below 1e-4, IS composited, and the pixel
+    stops; the negative fourth (which would re-grow W to 1.14e-4 > 1e-4 and
+    let the fifth in) is ignored.  Stopping before the crossing component
+    (n = 2, W = 6e-4) or not stopping (n = 5) both fail."""
+    from sss_synth import make_stop_rule_scene
+    sc = make_stop_rule_scene()
+    cam = sc.cameras[0]
+    o = np.tanh(sc.params[11].astype(np.float64))  # the fp32-stored opacities
+    a1, a2, a3 = o[0], o[1], o[2]
+    for bg in ((0.0, 0.0, 0.0), (0.25, 0.5, 0.75)):
+        for mode in ("brute", "tiled"):
+            fr = orc.render(sc.params, 0, cam, bg=bg, mode=mode)
+            assert fr.n_contrib[32, 32] == 3
+            W = (1 - a1) * (1 - a2) * (1 - a3)
+            assert fr.final_T[32, 32] == pytest.approx(W, rel=1e-12)
+            assert 5e-5 < W < 1e-4 < W * (1 - o[3])
+            # colours (1,0,0), (0,1,0), (0,0,1): one channel per composited component
+            col = np.clip(sc.params[12:15, :3].astype(np.float64) * Y00 + 0.5, 0, None)  # fp32-stored DC
+            al = np.array([a1, a2 * (1 - a1), a3 * (1 - a1) * (1 - a2)])
+            exp = col @ al + np.asarray(bg) * W
+            assert np.allclose(col, np.eye(3), atol=1e-7)
+            np.testing.assert_allclose(fr.rgb[:, 32, 32], exp, rtol=1e-12, atol=1e-15)
+    # backward: the post-stop components get exactly zero gradient from this pixel
+    d = np.zeros((3, 64, 64))
+    d[:, 32, 32] = (1.0, -0.5, 0.25)
+    _, g2d = orc.backward(sc.params, 0, cam, d, mode="brute", want_g2d=True)
+    assert np.all(g2d[3:] == 0.0) and np.all(g2d[:3, 8] != 0.0)
+    # closed-form dC/do of the third (last composited) component: dL/da3 * T,
+    # T = 1: W3 sum_k g_k (c3_k - S3_k) with S3 = bg = 0
+    W3 = (1 - a1) * (1 - a2)
+    c3 = np.clip(sc.params[12:15, 2].astype(np.float64) * Y00 + 0.5, 0, None)
+    assert g2d[2, 8] == pytest.approx(W3 * float(np.dot((1.0, -0.5, 0.25), c3)), rel=1e-12)
+
+
+def test_alpha_clamp_pin(orc):
+    """R10: alpha = clamp(o T, -0.99, 0.99) with zero gradient through an
+    active clamp.  One component with o = 0.999 seen at h = 0: alpha = 0.99
+    (not 0.999), W = 0.01, C = 0.99 c; with the image gradient on that pixel
+    only, dL/do and every geometry / nu gradient are exactly 0 while dL/dc =
+    alpha W_before g = 0.99 g.  With o = 0.98 (no clamp) dL/do = T c g."""
+    from sss_synth import make_stop_rule_scene
+    sc = make_stop_rule_scene()
+    cam = sc.cameras[0]
+    for o, clamped in ((0.999, True), (-0.999, True), (0.98, False)):
+        p = sc.params[:, :1].astype(np.float64).copy()
+        p[11, 0] = math.atanh(o)
+        p[12:15, 0] = (np.array([0.8, 0.8, 0.8]) - 0.5) / Y00
+        fr = orc.render(p, 0, cam, mode="brute")
+        a = float(np.clip(np.tanh(p[11, 0]), -0.99, 0.99))
+        assert fr.rgb[0, 32, 32] == pytest.approx(0.8 * a, rel=1e-12)
+        assert fr.final_T[32, 32] == pytest.approx(1 - a, rel=1e-12)
+        d = np.zeros((3, 64, 64))
+        d[0, 32, 32] = 1.0
+        _, g2d = orc.backward(p, 0, cam, d, mode="brute", want_g2d=True)
+        assert g2d[0, 5] == pytest.approx(a, rel=1e-12)  # dL/dc_R = alpha W g
+        if clamped:
+            assert abs(a) == 0.99
+            assert np.all(g2d[0, [0, 1, 2, 3, 4, 8, 9]] == 0.0)
+        else:
+            assert g2d[0, 8] == pytest.approx(0.8, rel=1e-6)  # T = 1 (h = 0), c = 0.8
 
 
 def test_binning_is_the_sorted_rect_instances(orc):
@@ -367,25 +465,29 @@ def test_tile_rect_is_conservative(orc):
 
 
 # ---------------------------------------------------------------- backward
-def _fd_scene(sh_degree, seed, n=6, w=24, h=20):
+def _fd_scene(sh_degree, seed, n=6, w=24, h=20, o_range=(0.15, 0.85), ls_mean=-0.9):
     rng = np.random.default_rng(seed)
     comps = []
     K = (sh_degree + 1) ** 2
     for _ in range(n):
-        comps.append(dict(mu=rng.uniform(-0.35, 0.35, 3), log_scale=rng.normal(-0.9, 0.25, 3),
+        comps.append(dict(mu=rng.uniform(-0.35, 0.35, 3), log_scale=rng.normal(ls_mean, 0.25, 3),
                           q=rng.normal(size=4) * rng.uniform(0.5, 2.0), nu=rng.uniform(1.2, 12),
-                          o=rng.choice([-1, 1], p=[0.3, 0.7]) * rng.uniform(0.15, 0.85),
+                          o=rng.choice([-1, 1], p=[0.3, 0.7]) * rng.uniform(*o_range),
                           rgb=rng.uniform(0.25, 0.75, 3),
                           sh_rest=rng.normal(0, 0.05, 3 * (K - 1))))
     cam = _cam_from((0.8, -3.7, 1.1), w=w, h=h, f=18.0)
     return planes_from(comps, sh_degree), cam
 
 
-@pytest.mark.parametrize("sh_degree,seed", [(0, 1), (3, 2), (1, 3), (2, 4)])
-def test_backward_matches_finite_differences(orc, sh_degree, seed):
+@pytest.mark.parametrize("sh_degree,seed,o_range", [(0, 1, (0.15, 0.85)), (3, 2, (0.15, 0.85)),
+                                                     (1, 3, (0.15, 0.85)), (2, 4, (0.15, 0.85)),
+                                                     (0, 5, (0.993, 0.999)), (3, 6, (0.993, 0.999))])
+def test_backward_matches_finite_differences(orc, sh_degree, seed, o_range):
     """SM backward with the full dT/dnu (R13): central
-    differences of L = <d_rgb, C> in fp64 with frozen gating."""
-    pl, cam = _fd_scene(sh_degree, seed)
+    differences of L = <d_rgb, C> in fp64 with frozen gating.
+    The high-opacity cases (|o| up to 0.999) put pixels on the active
+    +-0.99 alpha clamp (R10), whose zero gradient the differences confirm."""
+    pl, cam = _fd_scene(sh_degree, seed, o_range=o_range, ls_mean=-0.9 if o_range[1] < 0.99 else 0.6)
     H, W = cam.height, cam.width
     d = np.random.default_rng(seed + 100).normal(size=(3, H, W))
     base = orc.render(pl, sh_degree, cam, mode="brute", record_lists=16)
@@ -410,6 +512,14 @@ def test_backward_matches_finite_differences(orc, sh_degree, seed):
     for name, sl in group_slices(sh_degree).items():
         assert np.linalg.norm(fd[sl]) > 0, name
         assert rel_l2(grad[sl], fd[sl]) < 1e-5, (name, rel_l2(grad[sl], fd[sl]))
+    if o_range[1] > 0.99:  # the clamp is active somewhere in the frozen lists
+        o = np.tanh(pl[11])
+        clamped = 0
+        for i in range(pl.shape[1]):
+            if abs(o[i]) > 0.99:
+                T = orc.render(pl[:, i:i + 1], sh_degree, cam, mode="brute")
+                clamped += int(np.sum(np.abs(1 - T.final_T) >= 0.99 - 1e-12))
+        assert clamped > 0
 
 
 def test_printed_dT_dnu_fails_finite_differences(orc):
