@@ -114,7 +114,10 @@ typedef struct {
  *  ranges   [V][n_bins][2] start, end (absolute offsets within the view)
  *  totals   [V] instance count of the view (written even on overflow)
  *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
- *           scattered and every range is empty; grow and retry). */
+ *           scattered for that view and its ranges are empty; grow and
+ *           retry).  Sticky: sss_bin_sort only ever sets it; the caller
+ *           zeroes it (so one check after many calls sees every overflow;
+ *           sss_sghmc_step can be told to skip its update when it is set). */
 typedef struct {
   int32_t bin_shift;
   int32_t n_views;
@@ -179,6 +182,11 @@ typedef struct {
    * the full update bit for bit. */
   int32_t plane_begin, plane_end;
   int32_t reserved;
+  /* Device int32 flag (nullable): if *skip_if != 0 when the kernel runs, the
+   * step writes nothing (pass sss_bins.overflow so an iteration whose
+   * binning overflowed -- its views rendered as background -- never moves
+   * the parameters, moments or momentum; the caller grows and replays). */
+  const int32_t* skip_if;
 } sss_sghmc_hparams;
 
 /* flags for sss_render_bwd */

@@ -178,7 +178,8 @@ def hparams_c(hp) -> L.sss_sghmc_hparams:
                                hp.grad_scale, int(hp.step), int(hp.seed),
                                float(getattr(hp, "eps_o", 0.0)), float(getattr(hp, "eps_sigma", 0.0)),
                                int(getattr(hp, "mu_mode", 0)), int(getattr(hp, "plane_begin", 0)),
-                               int(getattr(hp, "plane_end", 0)), 0)
+                               int(getattr(hp, "plane_end", 0)), 0,
+                               _ptr(getattr(hp, "skip_if", None)))
 
 
 # ------------------------------------------------------------- entry points

@@ -602,7 +602,8 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     cudaFuncSetAttribute(chunk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  cudaMemsetAsync(out->overflow, 0, sizeof(int32_t), s);
+  // out->overflow is sticky: set here on overflow, never cleared (the caller
+  // resets it after checking), so a check after many calls sees every one
   cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   if (n > 0) {
     if (n % 4 == 0) {

@@ -100,7 +100,10 @@ template <bool NU_PAPER, bool GENERAL, bool FIRST>
 __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4 b, float4 c, float einu,
                                            EntrySums2& e, bool inc0, bool inc1) {
   const float2 t = mul2(h, bc2(b.w));
-  const float2 opt = add2(t, bc2(1.f));
+  // 1 + h/nu, kept finite: an excluded pixel far from a very thin splat can
+  // have h = inf, and T = Topt (1 + h/nu) must give 0 there, not 0 * inf
+  const float2 opt1 = add2(t, bc2(1.f));  // the forward's rounding (never contracted)
+  const float2 opt = make_float2(fminf(opt1.x, 3.0e38f), fminf(opt1.y, 3.0e38f));
   float2 lg, exm;
   if (GENERAL && b.w == 0.f) {  // Gaussian variant: T = exp(-h/2), t = 0, lg = 0
     lg = bc2(0.f);

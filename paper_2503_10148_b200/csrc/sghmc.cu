@@ -44,6 +44,7 @@ struct HP {
   float inv_b1t, inv_b2t;  // 1 / (1 - beta^t)
   uint32_t ctr2, ctr3;     // step (lo, hi)
   uint32_t key0, key1;     // seed (lo, hi)
+  const int32_t* skip_if;  // device flag: nonzero = write nothing
 };
 
 __device__ __forceinline__ float adam_dir(float g, float* m, float* v, int64_t idx, const HP& hp) {
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   const int64_t n = P.n;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (hp.skip_if && *hp.skip_if) return;  // e.g. the iteration's binning overflowed
   const int K = (P.sh_degree + 1) * (P.sh_degree + 1);
   // gate and (burn-in) covariance from the pre-update state
   const bool positive = P.variant & SSS_VARIANT_POSITIVE;
@@ -237,6 +239,7 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
   hp.beta1 = h->beta1; hp.beta2 = h->beta2; hp.adam_eps = h->adam_eps; hp.grad_scale = h->grad_scale;
   hp.eps_o = h->eps_o; hp.eps_sigma = h->eps_sigma;
   hp.mu_mode = h->mu_mode;
+  hp.skip_if = h->skip_if;
   const int Pn = 12 + 3 * (p->sh_degree + 1) * (p->sh_degree + 1);
   hp.p0 = h->plane_begin;
   hp.p1 = (h->plane_begin == 0 && h->plane_end == 0) ? Pn : h->plane_end;

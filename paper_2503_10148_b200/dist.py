@@ -55,6 +55,13 @@ def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
+def allreduce_max_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place max over ranks (device tensor; no host sync)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
 def plane_shard(P: int, rank: int, world: int):
     """(planes per rank Pr, [begin, end) owned by `rank`) of a [R * Pr][n]
     padded plane buffer."""

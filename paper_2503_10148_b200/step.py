@@ -5,10 +5,21 @@ sss_render_fwd -> sss_render_bwd (fused L1, gradients accumulated over
 views); then the NCCL all-reduce of the flat gradient buffer (R > 1) and
 sss_sghmc_step with grad_scale = 1/V (R26).  All calls are asynchronous on
 one stream; the only host synchronisation is the loss / overflow read-back
-the caller asks for.  Buffers are allocated once and reused (the bin
-capacity is sized from a measured instance count with headroom; an
-overflow is detected from the device flag and the iteration replayed with a
-larger buffer).
+the caller asks for.  Buffers are allocated once and reused; the bin
+capacity is sized from a measured instance count with headroom.
+
+Bin overflow (an iteration needs more instances than the capacity): the
+overflow flag is sticky on the device and the sampler step is told to skip
+its update when it is set (sss_sghmc_hparams.skip_if; all-reduced over
+ranks first, so replicas never diverge), so an overflowed iteration never
+moves parameters, moments or momentum.  step(check=True) reads the flag
+(one host sync), grows the capacity and replays the iteration;
+step(check=False) leaves the check to the caller (overflowed() after a run
+sees every overflow since the last reset_overflow()).
+
+Loss: step() returns this rank's device float[1] sum over its views of the
+per-view mean L1 (sss_render_bwd's loss_out); the objective of R26 is that
+sum over all ranks divided by total_views (see mean_loss()).
 """
 from __future__ import annotations
 
@@ -170,9 +181,18 @@ class TrainStep:
                 A.sss_render_bwd(self.params, pv, bv, cams, fv, half="projection", **kw)
                 self._mark("render_bwd_projection")
 
-    def step(self, targets: torch.Tensor) -> torch.Tensor:
-        """One full iteration; returns the (device) loss of this rank."""
+    def step(self, targets: torch.Tensor, check: bool = False) -> torch.Tensor:
+        """One full iteration; returns this rank's device loss sum (see the
+        module docstring).  check=True: synchronise on the overflow flag and
+        replay the iteration with grown bins until it fits."""
         self.forward_backward(targets)
+        while check and self.overflowed():
+            self.grow()
+            self.forward_backward(targets)
+        flag = self.bins[0].overflow
+        if self.world > 1:  # any rank's overflow skips every rank's update
+            D.allreduce_max_(flag, self.group)
+        self.hp.skip_if = flag
         self.hp.step = self.t
         self.hp.grad_scale = 1.0 / self.total_views
         if self.shard:
@@ -208,8 +228,19 @@ class TrainStep:
         return out
 
     def overflowed(self) -> bool:
-        """Synchronising check of the bin overflow flag."""
+        """Synchronising check of the (sticky) bin overflow flag."""
         return bool(self.bins[0].overflow.item())
 
+    def reset_overflow(self):
+        self.bins[0].overflow.zero_()
+
     def grow(self):
+        """Re-measure the instance counts and re-size the bins (x1.5 headroom
+        on top of the usual); the new buffers start with a clear flag."""
         self._size_bins(factor=1.5)
+
+    def mean_loss(self, loss: torch.Tensor = None) -> float:
+        """The R26 objective (1/V) sum_v L1_v over all ranks (host sync)."""
+        t = (self.loss if loss is None else loss).clone()
+        D.allreduce_sum_(t, self.group)
+        return float(t.item()) / self.total_views

@@ -2,13 +2,18 @@
 
 * config 3 (500k components, 1297x840): every projection record, every tile
   count, sampled per-tile key lists, the whole image and the whole gradient.
-* configs 4 and 5 (2M / 3M components): two views each, with the bench's
-  16-view launch shape (bin_shift 2) — projection, tile counts and sampled
-  tile lists bit-exact, sampled pixels vs the oracle evaluated pixel by
-  pixel, and gradients of a loss restricted to sampled pixels (the oracle's
-  backward over those pixels is cheap; the GPU runs its full kernels with
-  an image gradient that is zero elsewhere).  Config 5 also checks the
-  SGHMC/Adam step over all 3M components.
+* configs 4 and 5 (2M / 3M components): two views each launched together
+  at bin_shift 2 — projection, tile counts and sampled tile lists
+  bit-exact, sampled pixels vs the oracle evaluated pixel by pixel, and
+  gradients of a loss restricted to sampled pixels (the oracle's backward
+  over those pixels is cheap; the GPU runs its full kernels with an image
+  gradient that is zero elsewhere).
+* config 5 in bench.py's exact launch: all 64 views in one launch of every
+  kernel at bin_shift 2, the forward recording its per-strip lists, the
+  fused-L1 backward (render_bwd_kernel<FILTER, L1>); views 0, 31 and 63 are
+  checked (projection, coarse-bin lists of sampled bins, >= 600 sampled
+  pixels, sampled-pixel gradients).
+* config 5's SGHMC/Adam step over all 3M components.
 """
 import numpy as np
 import pytest
@@ -216,3 +221,76 @@ def test_sharded_step_nccl_single_rank(orc, sss):
         np.testing.assert_allclose(out[1], out[0], rtol=1e-6, atol=1e-7)
     finally:
         dist.destroy_process_group()
+
+
+def test_config5_bench_launch(orc, sss):
+    """Config 5 exactly as bench.py launches it: 64 views per launch,
+    bin_shift 2, per-strip composited lists on, fused L1 backward.  Targets
+    equal the GPU image except at sampled pixels of views 0/31/63, where they
+    sit 0.01-0.3 away, so sign(C - target) (R20) is decided identically on
+    both sides and is zero elsewhere: the gradient of that loss is the
+    oracle backward of those pixels (rect-free brute force, pinned == tiled)."""
+    import torch
+
+    from gpu_helpers import bin_lists, to_dev
+    from sss_synth import make_scene
+    from test_gpu_parity import _check_projection
+
+    sc = make_scene(5)
+    cams = sc.cameras
+    V, H, W = len(cams), cams[0].height, cams[0].width
+    assert V == 64
+    params = to_dev(sc)
+    pr = sss.sss_project(params, cams)
+    bins = sss.sss_bin_sort(pr, cams, bin_shift=2)  # probe-sized capacity (x1.25), as TrainStep
+    assert not sss.sss_check_overflow(bins)
+    fr = sss.Frame.empty(V, H, W)  # per-strip lists on (bench), n_contrib counted here
+    sss.sss_render_fwd(pr, bins, cams, out=fr)
+    torch.cuda.synchronize()
+    check = [0, 31, 63]
+    rng = np.random.default_rng(55)
+    tgt = fr.rgb.clone()
+    refs = []
+    tx, ty = (W + 15) // 16, (H + 15) // 16
+    bxn, byn = (tx + 3) // 4, (ty + 3) // 4
+    for v in check:
+        o = _check_projection(orc, sc, pr, v)
+        # coarse-bin lists of sampled bins: the oracle's (depth, index) order
+        # over visible components whose tile rect meets the bin
+        order = np.lexsort((np.arange(sc.n), o.depth.view(np.uint32)))
+        vis = o.n_tiles > 0
+        r = o.rect >> 2
+        lists = bin_lists(bins, v, bxn * byn)
+        for b in rng.choice(bxn * byn, 10, replace=False):
+            bx, by = b % bxn, b // bxn
+            hit = vis & (r[:, 0] <= bx) & (r[:, 2] >= bx) & (r[:, 1] <= by) & (r[:, 3] >= by)
+            assert np.array_equal(lists[b], order[hit[order]]), (v, b)
+        px = rng.choice(H * W, 640, replace=False).astype(np.int32)
+        ref = orc.render(sc.params, 3, cams[v], mode="brute", pixels=px)
+        rgb = fr.rgb[v].reshape(3, -1)[:, px].cpu().numpy()
+        nc = fr.n_contrib[v].reshape(-1)[px].cpu().numpy()
+        mism = nc != ref.n_contrib
+        assert np.all(ref.tie[mism] < 1e-3) and mism.mean() < 0.01
+        assert np.abs(rgb - ref.rgb)[:, ~mism].max() <= 1e-4
+        sgn = rng.choice([-1.0, 1.0], size=(3, len(px)))
+        off = rng.uniform(0.01, 0.3, size=(3, len(px)))
+        tv = tgt[v].reshape(3, -1)
+        tv[:, torch.from_numpy(px).long().cuda()] = torch.from_numpy((rgb - sgn * off).astype(np.float32)).cuda()
+        refs.append((v, px, sgn))
+    ws = torch.zeros(max(sss.render_bwd_workspace_bytes(sc.n, V), 4), dtype=torch.uint8, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    g = sss.sss_render_bwd(params, pr, bins, cams, fr, target=tgt.contiguous(), loss=loss, ws=ws)
+    torch.cuda.synchronize()
+    gref = 0
+    for v, px, sgn in refs:
+        gref = gref + orc.backward(sc.params, 3, cams[v], sgn / (3.0 * H * W), mode="brute",
+                                   pixels=px)[0]
+    gg = g.planes.cpu().numpy()
+    for grp, sl in group_slices(3).items():
+        assert rel_l2(gg[sl], gref[sl]) <= 1e-3, grp
+    exp_loss = sum(float(np.abs(fr.rgb[v].reshape(3, -1)[:, torch.from_numpy(px).long().cuda()].cpu().numpy()
+                                 - tgt[v].reshape(3, -1)[:, torch.from_numpy(px).long().cuda()].cpu().numpy()).sum())
+                   for v, px, _ in refs) / (3.0 * H * W)
+    assert abs(loss.item() - exp_loss) <= 1e-4 * exp_loss
+    # the workspace is left zero (consumed and cleared by the projection backward)
+    assert int(torch.count_nonzero(ws).item()) == 0

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from helpers import group_slices, rel_l2
-from sss_synth import make_custom_scene, make_optimizer_state, make_scene
+from sss_synth import make_custom_scene, make_optimizer_state, make_scene, make_stress_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -21,7 +21,8 @@ TIE_BAND = 1e-3  # relative distance of the oracle W from 1e-4 (R11)
 def _scenes():
     return {
         "cfg1": make_scene(1),
-        "cfg2_20k": make_scene(2, n=20000),
+        "cfg2": make_scene(2),  # 100,000 components, the stated size
+        "stress_d1": make_stress_scene(seed=5, sh_degree=1),  # huge/elongated/off-image/near-plane
         "ragged_d1": make_custom_scene(3000, 1, 200, 133, seed=3, p_negative=0.3),
         "blobs_d2_3v": make_custom_scene(6000, 2, 160, 96, n_views=3, seed=5, layout="blobs",
                                          nu_hi=16.0),
@@ -332,9 +333,72 @@ def test_sghmc_parity(orc, sss, variant):
     ulp = np.spacing(np.abs(p_ref).astype(np.float32)).astype(np.float64)
     bound = ulp + 1e-5 * np.abs(dref)
     assert np.all(np.abs(got - p_ref) <= bound + 1e-30), float((np.abs(got - p_ref) / bound).max())
+    # and most elements are the correctly rounded fp64 result: a systematic
+    # error inside the update would move far more than this fraction off it
+    frac = float(np.mean(got.astype(np.float32) != p_ref.astype(np.float32)))
+    assert frac < 0.05, frac
     assert rel_l2(rr.cpu().numpy() - r, r_ref - r) <= 1e-5
     assert rel_l2(mm.planes.cpu().numpy(), m_ref) <= 1e-5
     assert rel_l2(vv.planes.cpu().numpy(), v_ref) <= 1e-5
+
+
+def test_stop_rule_pixel(orc, sss):
+    """R11 on the hand-derived pixel of the oracle pin
+    (test_oracle_pins.py::test_stop_rule_pin): the GPU composites exactly the
+    first three of five co-located components (the negative fourth would
+    re-grow W), bins 0 and 2, with and without background; its gradient
+    gives the post-stop components nothing."""
+    import torch
+
+    from gpu_helpers import gpu_forward
+    from sss_synth import make_stop_rule_scene
+
+    sc = make_stop_rule_scene()
+    for shift in (0, 2):
+        for bg in ((0.0, 0.0, 0.0), (0.25, 0.5, 0.75)):
+            params, pr, bins, fr = gpu_forward(sc, bin_shift=shift, bg=bg)
+            ref = orc.render(sc.params, 0, sc.cameras[0], bg=bg, mode="brute")
+            assert int(fr.n_contrib[0, 32, 32].item()) == 3 == ref.n_contrib[32, 32]
+            assert abs(float(fr.final_T[0, 32, 32].item()) - ref.final_T[32, 32]) <= 1e-9
+            np.testing.assert_allclose(fr.rgb[0, :, 32, 32].cpu().numpy(), ref.rgb[:, 32, 32], atol=2e-7)
+            _check_frame("stop_rule", fr.rgb[0].cpu().numpy(), fr.final_T[0].cpu().numpy(),
+                         fr.n_contrib[0].cpu().numpy(), ref)
+        d = torch.zeros((1, 3, 64, 64), device="cuda")
+        d[0, :, 32, 32] = torch.tensor([1.0, -0.5, 0.25])
+        ws = torch.zeros(sss.render_bwd_workspace_bytes(sc.n, 1), dtype=torch.uint8, device="cuda")
+        g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws)
+        torch.cuda.synchronize()
+        gg = g.planes.cpu().numpy()
+        assert np.all(gg[:, 3:] == 0.0) and np.all(gg[11, :3] != 0.0)
+        gref, _ = orc.backward(sc.params, 0, sc.cameras[0], d[0].cpu().numpy().astype(np.float64), mode="brute")
+        assert rel_l2(gg, gref) <= 1e-5
+
+
+def test_alpha_clamp_zero_gradient(orc, sss):
+    """R10: one component with |o| = 0.999 seen at h = 0 (the oracle pin's
+    pixel): alpha = +-0.99 on the GPU too, and with the image gradient on that
+    pixel only, d raw_o and every geometry / nu gradient are exactly zero."""
+    import torch
+
+    from gpu_helpers import gpu_forward
+    from sss_synth import make_stop_rule_scene
+    from sss_synth.scenes import Scene
+
+    base = make_stop_rule_scene()
+    for o in (0.999, -0.999):
+        pl = base.params[:, :1].copy()
+        pl[11, 0] = np.float32(np.arctanh(o))
+        sc = Scene(config=0, params=pl, sh_degree=0, cameras=base.cameras)
+        params, pr, bins, fr = gpu_forward(sc)
+        assert abs(abs(1.0 - float(fr.final_T[0, 32, 32].item())) - 0.99) <= 1e-7
+        d = torch.zeros((1, 3, 64, 64), device="cuda")
+        d[0, 0, 32, 32] = 1.0
+        ws = torch.zeros(sss.render_bwd_workspace_bytes(1, 1), dtype=torch.uint8, device="cuda")
+        g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws)
+        torch.cuda.synchronize()
+        gg = g.planes.cpu().numpy()[:, 0]
+        assert np.all(gg[:12] == 0.0), gg[:12]  # mean, scale, rot, nu, opacity
+        assert gg[12] != 0.0  # the colour still receives alpha W g
 
 
 def test_philox_normals_match_oracle(orc, sss):
