@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--bin-shift", type=int, default=2)
     ap.add_argument("--views-per-batch", type=int, default=64)
+    ap.add_argument("--max-per-bin", type=int, default=0,
+                    help="truncated bin lists (sss.h sss_bins.max_per_bin); 0 = complete lists")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row timings")
@@ -292,7 +294,7 @@ def arm_config(a, sc, world):
     cam = sc.cameras[0]
     return {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": sc.n_views,
             "width": cam.width, "height": cam.height, "sh_degree": sc.sh_degree,
-            "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch,
+            "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch, "max_per_bin": a.max_per_bin,
             "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
                      if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
             "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
@@ -350,7 +352,7 @@ def main():
     planes = torch.from_numpy(sc.params).cuda()
     hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
     ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
-                   views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim)
+                   views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim, max_per_bin=a.max_per_bin)
     for _ in range(a.warmup):
         ts.step(targets)
         if ts.overflowed():

@@ -113,6 +113,20 @@ typedef struct {
  *  keys     nullable [V][capacity]: bin << 32 | float bits of depth
  *  ranges   [V][n_bins][2] start, end (absolute offsets within the view)
  *  totals   [V] instance count of the view (written even on overflow)
+ *  max_per_bin  0: every list is complete.  > 0: truncated lists -- bin b
+ *           holds only the first min(len_b, max_per_bin) entries of its list
+ *           (a pixel stops after W < 1e-4, R11, so the raster reads only a
+ *           front part of each list: ~2 % of the entries at config 5).  The
+ *           raster then continues a truncated list, for a tile that still has
+ *           a live pixel at its end, with sorted[v][resume[v][b] ...
+ *           n_vis[v]) filtered by the tile rect, which is exactly the rest of
+ *           the tile's list; images and gradients are unchanged.
+ *  sorted   [V][n] (nullable if max_per_bin == 0): the view's visible
+ *           components in (depth, index) order (first n_vis[v] entries)
+ *  n_vis    [V] (nullable if max_per_bin == 0): visible components per view
+ *  resume   [V][n_bins] (nullable if max_per_bin == 0): position in sorted
+ *           one past the bin's last materialised entry; n_vis[v] if the
+ *           list is complete
  *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
  *           scattered for that view and its ranges are empty; grow and
  *           retry).  Sticky: sss_bin_sort only ever sets it; the caller
@@ -127,6 +141,11 @@ typedef struct {
   int32_t* ranges;
   int64_t* totals;
   int32_t* overflow;
+  int32_t max_per_bin;
+  int32_t reserved;
+  int32_t* sorted;
+  int32_t* n_vis;
+  int32_t* resume;
 } sss_bins;
 
 /* Rendered frames (output of sss_render_fwd; all views share one size).
@@ -212,7 +231,9 @@ SSS_API size_t sss_bin_sort_workspace(int64_t n, int32_t n_views, const sss_came
  * stable LSD radix sort of the depth keys followed by a stable counting
  * scatter by bin.  ws: device scratch of at least sss_bin_sort_workspace()
  * bytes.  out->bin_shift, capacity, ids, ranges, totals, overflow must be set
- * (keys optional).  Overflow is device-side (see sss_bins).  SSS_ERR_SHAPE if
+ * (keys optional; sorted, n_vis, resume required when max_per_bin > 0).
+ * totals and the capacity count materialised entries.  Overflow is
+ * device-side (see sss_bins).  SSS_ERR_SHAPE if
  * the view has more than SSS_MAX_BINS bins or more than 1024 bins along an
  * axis (raise bin_shift).  The capacity also sizes the scatter's shared-
  * memory stage (capacity / chunks of 1024 components); chunks above it take

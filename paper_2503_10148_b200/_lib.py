@@ -49,7 +49,9 @@ class sss_projected(C.Structure):
 class sss_bins(C.Structure):
     _fields_ = [("bin_shift", C.c_int32), ("n_views", C.c_int32), ("capacity", C.c_int64),
                 ("ids", C.c_void_p), ("keys", C.c_void_p), ("ranges", C.c_void_p),
-                ("totals", C.c_void_p), ("overflow", C.c_void_p)]
+                ("totals", C.c_void_p), ("overflow", C.c_void_p), ("max_per_bin", C.c_int32),
+                ("reserved", C.c_int32), ("sorted", C.c_void_p), ("n_vis", C.c_void_p),
+                ("resume", C.c_void_p)]
 
 
 class sss_frame(C.Structure):

@@ -122,23 +122,43 @@ class Bins:
     keys: Optional[torch.Tensor]    # [V][capacity] i64 (bit pattern of u64) or None
     ranges: torch.Tensor            # [V][n_bins][2] i32
     totals: torch.Tensor            # [V] i64
-    overflow: torch.Tensor          # [1] i32
+    overflow: torch.Tensor          # [1] i32 (sticky: zeroed by the caller)
+    max_per_bin: int = 0            # 0: complete lists; > 0: truncated (sss.h)
+    sorted: Optional[torch.Tensor] = None  # [V][n] i32 depth-sorted visible ids
+    n_vis: Optional[torch.Tensor] = None   # [V] i32
+    resume: Optional[torch.Tensor] = None  # [V][n_bins] i32
 
     @classmethod
     def empty(cls, V: int, n_bins: int, capacity: int, bin_shift: int, keys: bool,
-              device="cuda") -> "Bins":
+              device="cuda", max_per_bin: int = 0, n: int = 0) -> "Bins":
+        """n: components (needed for the sorted array when max_per_bin > 0)."""
         cap = max(int(capacity), 1)
+        trunc = int(max_per_bin) > 0
         return cls(bin_shift, int(capacity),
                    torch.empty((V, cap), dtype=torch.int32, device=device),
                    torch.empty((V, cap), dtype=torch.int64, device=device) if keys else None,
                    torch.empty((V, n_bins, 2), dtype=torch.int32, device=device),
                    torch.zeros((V,), dtype=torch.int64, device=device),
-                   torch.zeros((1,), dtype=torch.int32, device=device))
+                   torch.zeros((1,), dtype=torch.int32, device=device),
+                   int(max_per_bin),
+                   torch.empty((V, max(int(n), 1)), dtype=torch.int32, device=device) if trunc else None,
+                   torch.zeros((V,), dtype=torch.int32, device=device) if trunc else None,
+                   torch.empty((V, n_bins), dtype=torch.int32, device=device) if trunc else None)
 
     def c(self) -> L.sss_bins:
         return L.sss_bins(self.bin_shift, int(self.totals.shape[0]), self.capacity, _ptr(self.ids),
                           _ptr(self.keys), _ptr(self.ranges), _ptr(self.totals),
-                          _ptr(self.overflow))
+                          _ptr(self.overflow), int(self.max_per_bin), 0, _ptr(self.sorted),
+                          _ptr(self.n_vis), _ptr(self.resume))
+
+    def view(self, nv: int) -> "Bins":
+        """The first nv views (shared storage)."""
+        return Bins(self.bin_shift, self.capacity, self.ids[:nv],
+                    self.keys[:nv] if self.keys is not None else None, self.ranges[:nv],
+                    self.totals[:nv], self.overflow, self.max_per_bin,
+                    self.sorted[:nv] if self.sorted is not None else None,
+                    self.n_vis[:nv] if self.n_vis is not None else None,
+                    self.resume[:nv] if self.resume is not None else None)
 
 
 TILE_CAP = 1536  # composited entries per 16x8 strip the forward records for the backward
@@ -203,9 +223,10 @@ def bin_sort_workspace_bytes(n: int, cams: Sequence, bin_shift: int, cams_c=None
 def sss_bin_sort(proj: Projected, cams: Sequence, bin_shift: int = 0,
                  capacity: Optional[int] = None, keys: bool = False,
                  ws: Optional[torch.Tensor] = None, out: Optional[Bins] = None, stream=None,
-                 cams_c=None, headroom: float = 1.25) -> Bins:
+                 cams_c=None, headroom: float = 1.25, max_per_bin: int = 0) -> Bins:
     """Bin and depth-sort.  With capacity=None the instance count is measured
-    first (one host sync) and the output sized with `headroom`."""
+    first (one host sync) and the output sized with `headroom`.
+    max_per_bin > 0: truncated lists (sss.h sss_bins)."""
     lib = L.load()
     V = len(cams)
     cc = cams_c if cams_c is not None else cameras_c(cams)
@@ -217,12 +238,12 @@ def sss_bin_sort(proj: Projected, cams: Sequence, bin_shift: int = 0,
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
     if out is None:
         if capacity is None:
-            probe = Bins.empty(V, nb, 0, bin_shift, False, dev)
+            probe = Bins.empty(V, nb, 0, bin_shift, False, dev, max_per_bin, proj.n)
             pc, prc = probe.c(), proj.c()
             L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(pc),
                                      _stream_ptr(stream)), "sss_bin_sort(probe)")
             capacity = int(int(probe.totals.max().item()) * headroom) + 1024
-        out = Bins.empty(V, nb, capacity, bin_shift, keys, dev)
+        out = Bins.empty(V, nb, capacity, bin_shift, keys, dev, max_per_bin, proj.n)
     bc, prc = out.c(), proj.c()
     L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(bc),
                              _stream_ptr(stream)), "sss_bin_sort")

@@ -7,10 +7,11 @@
 //
 // B200 design — two stages instead of one 64-bit key sort over all M
 // instances:
-//   1. a stable LSD radix sort (4 x 8-bit digits) of the N per-view depth keys
-//      (keys of culled components are 0xFFFFFFFF and sort last); each pass
-//      reorders its 4096-key tile by digit in shared memory so the global
-//      stores leave as per-digit runs;
+//   1. a stable LSD radix sort (8-bit digits) of the per-view depth keys
+//      read straight from the projection: culled components are dropped (the
+//      first pass compacts), passes whose digit is constant over the view are
+//      skipped (radix.cuh depth mode); each pass reorders its 4096-key tile
+//      by digit in shared memory so the global stores leave as per-digit runs;
 //   2. a stable counting scatter of the instances by bin, generated on the fly
 //      from the depth-sorted components: per-chunk bin histograms (shared
 //      memory), a column scan over chunks, a scan over bins, then a scatter in
@@ -24,6 +25,15 @@
 // Every instance is written exactly once (4 B id, +8 B key if requested); the
 // radix passes touch only N keys per view.  All views are processed by the
 // same launches (grid.y = view).
+//
+// Truncated lists (max_per_bin > 0, see sss.h): a bin keeps only its first
+// max_per_bin entries.  The chunk histograms give every (chunk, bin) its
+// index range in the bin's full list, so a chunk's instance is kept iff its
+// index is below the cap; a chunk with nothing to keep returns at once, and a
+// component whose rect meets only bins already full before the chunk skips
+// the walk (its instances could only land in full bins, so the slots of the
+// open bins are unchanged).  The instance at index cap - 1 of a truncated
+// bin records resume[b] = its sorted position + 1 for the raster.
 #include <algorithm>
 
 #include "radix.cuh"
@@ -69,7 +79,8 @@ constexpr size_t kScatterSmemMax = 225 * 1024;  // dynamic shared memory of a sc
 constexpr int64_t kScatterStageMax = SSS_SCATTER_STAGE_MAX;  // staged ids per chunk (64 KB)
 
 struct WsLayout {
-  size_t keys_a, keys_b, vals_a, vals_b, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start, total;
+  size_t keys_a, keys_b, vals_a, vals_b, sorted, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start,
+      total;
   int tiles_per_view, n_chunks, chunk;
 };
 
@@ -87,76 +98,15 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.keys_b = take(nv * 4);
   L.vals_a = take(nv * 4);
   L.vals_b = take(nv * 4);
+  L.sorted = take(nv * 4);  // used when the caller passes no sorted array
   L.n_vis = take((size_t)V * 4);
-  L.radix_hist = take(radix_ws_words(L.tiles_per_view, V) * 4);
+  L.radix_hist = take(depth_sort_ws_words(L.tiles_per_view, V) * 4);
   L.chunk_hist = take((size_t)V * L.n_chunks * (size_t)g.n_bins * 4);
   L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
   L.bin_total = take((size_t)V * g.n_bins * 4);
   L.bin_start = take((size_t)V * g.n_bins * 4);
   L.total = off;
   return L;
-}
-
-// ------------------------------------------------------------- depth keys
-__global__ void keys_init_kernel(const float* __restrict__ depth, const short4* __restrict__ rect,
-                                 int64_t n, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
-                                 int32_t* __restrict__ n_vis) {
-  const int v = blockIdx.y;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool vis = false;
-  if (i < n) {
-    const short4 r = rect[(int64_t)v * n + i];
-    vis = r.x <= r.z;
-    keys[(int64_t)v * n + i] = vis ? __float_as_uint(depth[(int64_t)v * n + i]) : 0xFFFFFFFFu;
-    vals[(int64_t)v * n + i] = (int32_t)i;
-  }
-  // one atomic per block (per-warp atomics on one address serialise)
-  __shared__ int32_t wsum[8];
-  const unsigned b = __ballot_sync(0xffffffffu, vis);
-  if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(b);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t s = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
-    if (s) atomicAdd(&n_vis[v], s);
-  }
-}
-
-// The same with four consecutive components per thread and 16-byte accesses
-// (n % 4 == 0: every view's segment starts 16-byte aligned).
-__global__ void keys_init4_kernel(const float4* __restrict__ depth, const int4* __restrict__ rect,
-                                  int64_t n, uint4* __restrict__ keys, int4* __restrict__ vals,
-                                  int32_t* __restrict__ n_vis) {
-  const int v = blockIdx.y;
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // quad index in the view
-  const int64_t nq = n >> 2;
-  int cnt = 0;
-  if (q < nq) {
-    const int64_t o = (int64_t)v * nq + q;
-    const int4 r01 = rect[2 * o], r23 = rect[2 * o + 1];  // two short4 per int4
-    const float4 d = depth[o];
-    // short4 {x0, y0, x1, y1}: visible iff x0 <= x1 (low halves of words 0 and 1)
-    const bool v0 = (short)(r01.x & 0xffff) <= (short)(r01.y & 0xffff);
-    const bool v1 = (short)(r01.z & 0xffff) <= (short)(r01.w & 0xffff);
-    const bool v2 = (short)(r23.x & 0xffff) <= (short)(r23.y & 0xffff);
-    const bool v3 = (short)(r23.z & 0xffff) <= (short)(r23.w & 0xffff);
-    keys[o] = make_uint4(v0 ? __float_as_uint(d.x) : 0xFFFFFFFFu, v1 ? __float_as_uint(d.y) : 0xFFFFFFFFu,
-                         v2 ? __float_as_uint(d.z) : 0xFFFFFFFFu, v3 ? __float_as_uint(d.w) : 0xFFFFFFFFu);
-    const int32_t i0 = (int32_t)(4 * q);
-    vals[o] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
-    cnt = (int)v0 + (int)v1 + (int)v2 + (int)v3;
-  }
-  __shared__ int32_t wsum[8];
-  int c = cnt;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-  if (lane_id() == 0) wsum[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t s = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
-    if (s) atomicAdd(&n_vis[v], s);
-  }
 }
 
 // ------------------------------------------------------- bin histograms
@@ -260,12 +210,17 @@ __global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* _
   if (w == 0) bin_total[(size_t)v * n_bins + b] = tot;
 }
 
-// per view: exclusive scan over bins -> bin_start, ranges, totals, overflow
+// per view: exclusive scan over bins of the materialised counts
+// min(total_b, cap) -> bin_start, ranges, totals, overflow; resume = n_vis
+// for complete lists (the scatter writes it for truncated ones)
 __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restrict__ bin_total, int n_bins,
-                                                        int64_t capacity, uint32_t* __restrict__ bin_start,
+                                                        int64_t capacity, uint32_t cap,
+                                                        uint32_t* __restrict__ bin_start,
                                                         int32_t* __restrict__ ranges,
                                                         int64_t* __restrict__ totals,
-                                                        int32_t* __restrict__ overflow) {
+                                                        int32_t* __restrict__ overflow,
+                                                        const int32_t* __restrict__ n_vis,
+                                                        int32_t* __restrict__ resume) {
   __shared__ unsigned long long part[1024];
   __shared__ int over;
   const int v = blockIdx.x, t = threadIdx.x;
@@ -273,7 +228,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   const int per = (n_bins + 1023) / 1024;
   const int lo = t * per, hi = min(lo + per, n_bins);
   unsigned long long s = 0;
-  for (int k = lo; k < hi; ++k) s += bt[k];
+  for (int k = lo; k < hi; ++k) s += min(bt[k], cap);
   part[t] = s;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
@@ -291,7 +246,9 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   __syncthreads();
   unsigned long long run = part[t] - s;
   for (int k = lo; k < hi; ++k) {
-    const uint32_t x = bt[k];
+    const uint32_t full = bt[k];
+    const uint32_t x = min(full, cap);
+    if (resume && full <= cap) resume[(size_t)v * n_bins + k] = n_vis[v];
     bin_start[(size_t)v * n_bins + k] = (uint32_t)run;
     ranges[((size_t)v * n_bins + k) * 2 + 0] = over ? 0 : (int32_t)run;
     ranges[((size_t)v * n_bins + k) * 2 + 1] = over ? 0 : (int32_t)(run + x);
@@ -310,7 +267,31 @@ struct alignas(16) WalkScratch {
   WalkRec rec[32];
   int4 stage[32];     // {bx0 | by0 << 16, bx1 | by1 << 16, id, depth bits}
   uint32_t dbits[32];
+  int32_t spos[32];   // position of the rank's component in the depth-sorted order
 };
+
+// Truncation state of one scatter CTA (chunk): see the file header.
+struct TruncCtx {
+  uint32_t cap;                       // max_per_bin, or UINT32_MAX
+  const uint32_t* openm;              // smem bit per bin: something of the bin is kept in this chunk
+  const uint32_t* ch;                 // the chunk's index of each bin in its full list (global)
+  const uint32_t* bs;                 // materialised start of each bin (global)
+  const uint32_t* btot;               // full list length of each bin (global)
+  int32_t* resume;                    // [n_bins] of this view, or nullptr
+};
+
+// any bin of the rect still open in this chunk (rects of more than 16 bins
+// are assumed open: the per-instance test drops what is full)
+__device__ __forceinline__ bool rect_open(const TruncCtx& tc, const BinGeom& g, int bx0, int by0, int bx1,
+                                          int by1) {
+  if ((bx1 - bx0 + 1) * (by1 - by0 + 1) > 16) return true;
+  for (int by = by0; by <= by1; ++by)
+    for (int bx = bx0; bx <= bx1; ++bx) {
+      const int b = by * g.bins_x + bx;
+      if ((tc.openm[b >> 5] >> (b & 31)) & 1u) return true;
+    }
+  return false;
+}
 
 // Walks the warp's depth-sorted components [wlo, whi), 32 at a time.  The
 // step's components with a non-empty bin rect are compacted to ranks
@@ -333,12 +314,13 @@ struct alignas(16) WalkScratch {
 //   where the CTA writes every bin's run of the chunk with coalesced stores;
 //   otherwise (keys requested, or a chunk larger than the stage) the id goes
 //   straight to its global slot.
-template <bool STAGED>
+template <bool STAGED, bool TRUNC>
 __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
                                           const float* __restrict__ dv, int64_t wlo, int64_t whi,
                                           const BinGeom& g, uint32_t* wbase, uint32_t* colmask,
                                           uint32_t* rowmask, WalkScratch& S, int32_t* __restrict__ dst,
-                                          uint64_t* __restrict__ kv) {
+                                          uint64_t* __restrict__ kv, const uint32_t* soff,
+                                          const TruncCtx& tc) {
   const int lane = lane_id();
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
@@ -359,11 +341,14 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
     {
       const int bx0 = r0.x >> g.shift, by0 = r0.y >> g.shift;
       const int bx1 = r0.z >> g.shift, by1 = r0.w >> g.shift;
-      const bool ne = valid && bx0 <= bx1 && by0 <= by1;
+      bool ne = valid && bx0 <= bx1 && by0 <= by1;
+      if (TRUNC && ne) ne = rect_open(tc, g, bx0, by0, bx1, by1);
       const unsigned NE = __ballot_sync(full, ne);
-      if (ne)
+      if (ne) {
         S.stage[__popc(NE & lt)] = make_int4(bx0 | (by0 << 16), bx1 | (by1 << 16), id0,
                                              kv ? (int)__float_as_uint(dv[id0]) : 0);
+        if (TRUNC) S.spos[__popc(NE & lt)] = (int32_t)(j0 + lane);
+      }
       __syncwarp();
       const bool act = lane < __popc(NE);
       int cbx0 = 1, cby0 = 1, cbx1 = 0, cby1 = 0, n_i = 0;
@@ -428,8 +413,23 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
           const unsigned m = colmask[bx] & rowmask[by];
           const uint32_t w0 = wbase[b];
           const uint32_t pos = w0 + __popc(m & ((1u << own) - 1u));
-          dst[pos] = R.id;
-          if (!STAGED && kv) kv[pos] = ((uint64_t)b << 32) | S.dbits[own];
+          if (!TRUNC) {
+            dst[pos] = R.id;
+            if (!STAGED && kv) kv[pos] = ((uint64_t)b << 32) | S.dbits[own];
+          } else {
+            // kept iff the instance's index in the bin's full list is < cap:
+            // staged, the bin's kept run ends at soff[b + 1]; direct, soff[b]
+            // holds the bin's global limit bs[b] + cap
+            const uint32_t lim = STAGED ? soff[b + 1] : soff[b];
+            if (pos < lim) {
+              dst[pos] = R.id;
+              if (!STAGED && kv) kv[pos] = ((uint64_t)b << 32) | S.dbits[own];
+              if (pos + 1 == lim && tc.resume) {  // last kept of this chunk: is it the cap-th entry?
+                const uint32_t idx = STAGED ? tc.ch[b] + (pos - soff[b]) : pos - tc.bs[b];
+                if (idx + 1 == tc.cap && tc.btot[b] > tc.cap) tc.resume[b] = S.spos[own] + 1;
+              }
+            }
+          }
           if (((m >> own) >> 1) == 0u) {  // highest covering rank: advance the bin
             upd_b = b;
             upd_v = w0 + __popc(m);
@@ -456,8 +456,9 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
     const uint32_t* __restrict__ chunk_hist, const uint8_t* __restrict__ warp_hist,
-    const uint32_t* __restrict__ bin_start, const int64_t* __restrict__ totals, int64_t capacity,
-    int stage_cap, int32_t* __restrict__ ids, uint64_t* __restrict__ keys) {
+    const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ bin_total,
+    const int64_t* __restrict__ totals, int64_t capacity, uint32_t cap, int stage_cap,
+    int32_t* __restrict__ ids, uint64_t* __restrict__ keys, int32_t* __restrict__ resume) {
   extern __shared__ uint4 sm4[];
   __shared__ uint32_t red[kScatterWarps];
   const int v = blockIdx.y, c = blockIdx.x;
@@ -465,18 +466,22 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const int64_t lo = (int64_t)c * kChunk;
   const int64_t nvis = n_vis[v];
   if (lo >= nvis) return;
+  const bool trunc = cap != 0xFFFFFFFFu;
   const int nb = g.n_bins;
   WalkScratch* scratch = reinterpret_cast<WalkScratch*>(sm4);             // [8]
   uint32_t* wbase = reinterpret_cast<uint32_t*>(scratch + kScatterWarps);  // [8][n_bins] next slot per bin
   uint32_t* masks = wbase + (size_t)kScatterWarps * nb;                    // [8][bins_x + bins_y] rank masks
-  uint32_t* soff = masks + kScatterWarps * (g.bins_x + g.bins_y);          // [n_bins + 1] run starts (stage)
+  uint32_t* soff = masks + kScatterWarps * (g.bins_x + g.bins_y);          // [n_bins + 1] run starts (stage) / limits
   uint32_t* gst = soff + nb + 1;                                           // [n_bins] run starts (global)
-  int32_t* sids = reinterpret_cast<int32_t*>(gst + nb);                   // [stage_cap] staged ids
+  uint32_t* openm = gst + nb;                                              // [ceil(n_bins / 32)] open bins
+  int32_t* sids = reinterpret_cast<int32_t*>(openm + ((nb + 31) >> 5));   // [stage_cap] staged ids
   const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
   const uint8_t* wh = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
   const uint32_t* bs = bin_start + (size_t)v * nb;
   const int w = threadIdx.x >> 5, lane = lane_id();
-  // the chunk's bin counts, scanned over bins: thread t owns bins [b0, b1)
+  for (int k = threadIdx.x; k < ((nb + 31) >> 5); k += kScatterThreads) openm[k] = 0u;
+  // the chunk's kept bin counts (all of them without a cap), scanned over
+  // bins: thread t owns bins [b0, b1)
   const int per = (nb + kScatterThreads - 1) / kScatterThreads;
   const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
   uint32_t mine = 0;
@@ -484,7 +489,8 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     uint32_t cb = 0;
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
-    mine += cb;
+    const uint32_t cs = ch[b];
+    mine += cs >= cap ? 0u : min(cb, cap - cs);
   }
   uint32_t incl = mine;
 #pragma unroll
@@ -500,19 +506,28 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     wpre += ww < w ? red[ww] : 0u;
     total += red[ww];
   }
+  if (total == 0) return;  // every instance of the chunk lands in a full bin (CTA-uniform)
   const bool staged = keys == nullptr && total <= (uint32_t)stage_cap;  // CTA-uniform
   uint32_t run = wpre + incl - mine;
   for (int b = b0; b < b1; ++b) {
-    const uint32_t gb = bs[b] + ch[b];
-    soff[b] = run;
+    uint32_t cb = 0;
+#pragma unroll
+    for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
+    const uint32_t cs = ch[b];
+    const uint32_t kept = cs >= cap ? 0u : min(cb, cap - cs);
+    const uint32_t gb = bs[b] + cs;
     gst[b] = gb;
+    // staged: the stage offset of the bin's kept run; direct: the bin's
+    // global limit (its materialised start + cap)
+    soff[b] = staged ? run : (trunc ? bs[b] + cap : 0xFFFFFFFFu);
     uint32_t acc = staged ? run : gb;  // + exclusive prefix of the per-warp counts
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
       wbase[(size_t)ww * nb + b] = acc;
       acc += wh[(size_t)ww * nb + b];
     }
-    run += acc - (staged ? run : gb);
+    if (kept) atomicOr(&openm[b >> 5], 1u << (b & 31));
+    run += kept;
   }
   if (threadIdx.x == 0) soff[nb] = total;
   __syncthreads();
@@ -526,11 +541,15 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
+  const TruncCtx tc{cap, openm, ch, bs, bin_total + (size_t)v * nb, resume ? resume + (size_t)v * nb : nullptr};
+  uint32_t* wb = wbase + (size_t)w * nb;
   if (!staged) {
-    warp_walk<false>(sid, rv, dv, wlo, whi, g, wbase + (size_t)w * nb, colmask, rowmask, scratch[w], idv, kv);
+    if (trunc) warp_walk<false, true>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], idv, kv, soff, tc);
+    else warp_walk<false, false>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], idv, kv, soff, tc);
     return;
   }
-  warp_walk<true>(sid, rv, dv, wlo, whi, g, wbase + (size_t)w * nb, colmask, rowmask, scratch[w], sids, nullptr);
+  if (trunc) warp_walk<true, true>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], sids, nullptr, soff, tc);
+  else warp_walk<true, false>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], sids, nullptr, soff, tc);
   __syncthreads();
   // copy-out: each group of kRunLanes lanes stores one bin's run (runs
   // average ~30 ids at bin_shift 2) with consecutive lanes on consecutive slots
@@ -577,6 +596,14 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     set_error("sss_bin_sort: null output buffer");
     return SSS_ERR_ARG;
   }
+  if (out->max_per_bin < 0 || (out->max_per_bin > 0 && (!out->sorted || !out->n_vis || !out->resume))) {
+    set_error("sss_bin_sort: max_per_bin > 0 needs sorted, n_vis and resume (and max_per_bin >= 0)");
+    return SSS_ERR_ARG;
+  }
+  if (n > 0x7fffffffLL - out->capacity) {  // virtual list positions (start + n) must fit int32
+    set_error("sss_bin_sort: n + capacity must be < 2^31");
+    return SSS_ERR_SHAPE;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const WsLayout L = ws_layout(n > 0 ? n : 1, n_views, g);
   if (!ws || ws_bytes < L.total) {
@@ -588,13 +615,16 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   uint32_t* keys_b = (uint32_t*)(w + L.keys_b);
   int32_t* vals_a = (int32_t*)(w + L.vals_a);
   int32_t* vals_b = (int32_t*)(w + L.vals_b);
-  int32_t* n_vis = (int32_t*)(w + L.n_vis);
+  int32_t* sorted = out->sorted ? out->sorted : (int32_t*)(w + L.sorted);
+  int32_t* n_vis = out->n_vis ? out->n_vis : (int32_t*)(w + L.n_vis);
   uint32_t* rhist = (uint32_t*)(w + L.radix_hist);
   uint32_t* chist = (uint32_t*)(w + L.chunk_hist);
   uint8_t* whist = (uint8_t*)(w + L.warp_hist);
   uint32_t* btot = (uint32_t*)(w + L.bin_total);
   uint32_t* bstart = (uint32_t*)(w + L.bin_start);
   const short4* rect = (const short4*)pr->rect;
+  const uint32_t cap = out->max_per_bin > 0 ? (uint32_t)out->max_per_bin : 0xFFFFFFFFu;
+  int32_t* resume = out->max_per_bin > 0 ? out->resume : nullptr;
 
   static thread_local bool attr_set = false;
   if (!attr_set) {  // large dynamic shared memory for the per-warp bin counters
@@ -604,31 +634,20 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   }
   // out->overflow is sticky: set here on overflow, never cleared (the caller
   // resets it after checking), so a check after many calls sees every one
-  cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   if (n > 0) {
-    if (n % 4 == 0) {
-      const dim3 gi(div_up(n / 4, 256), n_views);
-      keys_init4_kernel<<<gi, 256, 0, s>>>((const float4*)pr->depth, (const int4*)rect, n, (uint4*)keys_a,
-                                           (int4*)vals_a, n_vis);
-    } else {
-      const dim3 gi(div_up(n, 256), n_views);
-      keys_init_kernel<<<gi, 256, 0, s>>>(pr->depth, rect, n, keys_a, vals_a, n_vis);
-    }
-    count_launch();
-    const dim3 gr(L.tiles_per_view, n_views);
-    radix_sort_pairs(keys_a, vals_a, keys_b, vals_b, n, n_views, L.tiles_per_view, rhist, s);
-    int32_t* vin = vals_a;
-    // after 4 passes the sorted ids are in vals_a
+    depth_sort(pr->depth, rect, n, n_views, L.tiles_per_view, keys_a, keys_b, vals_a, vals_b, sorted, n_vis,
+               rhist, s);
     const dim3 gc(L.n_chunks, n_views);
     const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
-    chunk_hist_kernel<<<gc, kScatterThreads, hsm, s>>>(vin, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
+    chunk_hist_kernel<<<gc, kScatterThreads, hsm, s>>>(sorted, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
     column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 32 * kColWarps, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
     count_launch(2);
   } else {
     cudaMemsetAsync(btot, 0, sizeof(uint32_t) * n_views * g.n_bins, s);
+    cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   }
-  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, bstart, out->ranges, out->totals,
-                                            out->overflow);
+  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, cap, bstart, out->ranges, out->totals,
+                                            out->overflow, n_vis, resume);
   count_launch();
   if (n > 0) {
     // stage: the chunk's mean share of the capacity (the caller sizes the
@@ -636,15 +655,15 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     // shared memory left; larger chunks take the direct path
     const size_t fixed = sizeof(WalkScratch) * kScatterWarps +
                          ((size_t)kScatterWarps * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y) +
-                          2 * (size_t)g.n_bins + 1) * 4;
+                          2 * (size_t)g.n_bins + 1 + (size_t)((g.n_bins + 31) >> 5)) * 4;
     int64_t want = (out->capacity + L.n_chunks - 1) / L.n_chunks;
     want = std::min<int64_t>(std::max<int64_t>(want, 256), kScatterStageMax);
     const int64_t room = ((int64_t)kScatterSmemMax - (int64_t)fixed) / 4;
     const int stage_cap = (int)std::max<int64_t>(0, std::min<int64_t>((want + 31) & ~31, room));
     const size_t ssm = fixed + (size_t)stage_cap * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
-        vals_a, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, out->totals, out->capacity,
-        stage_cap, out->ids, out->keys);
+        sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, btot, out->totals,
+        out->capacity, cap, stage_cap, out->ids, out->keys, resume);
     count_launch();
   }
   return check_launch("sss_bin_sort");

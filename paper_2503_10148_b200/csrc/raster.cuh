@@ -97,7 +97,43 @@ static __device__ unsigned long long g_cnt[16];  // one set per translation unit
 struct RasterGeom {
   int width, height, tiles_x, tiles_y, shift, bins_x, n_bins;
   int64_t n, capacity;
+  // truncated bin lists (sss_bins.max_per_bin > 0): the tile's list is the
+  // bin's materialised entries [start, mend) followed by the virtual tail
+  // sorted[resume .. n_vis) (positions mend, mend + 1, ...), rect-filtered;
+  // nullptr = complete lists
+  const int32_t* sorted;
+  const int32_t* n_vis;
+  const int32_t* resume;
 };
+
+// The list of the tile's bin as the raster walks it: positions [start, end)
+// with end = mend + tail length; position p maps to a component through
+// ids (p < mend) or the depth-sorted tail (p >= mend, always rect-filtered).
+struct BinList {
+  int32_t start, mend, end, tail0;  // tail0: sorted index of position mend
+  const int32_t* ids;               // the view's ids
+  const int32_t* tail;              // the view's sorted ids (or nullptr)
+  __device__ __forceinline__ int32_t id(int32_t p) const {
+    return p < mend ? __ldg(ids + p) : __ldg(tail + tail0 + (p - mend));
+  }
+};
+
+__device__ __forceinline__ BinList bin_list(const RasterGeom& G, const int32_t* __restrict__ ids,
+                                            const int32_t* __restrict__ ranges, int v, int bin) {
+  BinList L;
+  L.start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
+  L.mend = ranges[((int64_t)v * G.n_bins + bin) * 2 + 1];
+  L.end = L.mend;
+  L.ids = ids + (int64_t)v * G.capacity;
+  L.tail = nullptr;
+  L.tail0 = 0;
+  if (G.sorted) {
+    L.tail0 = G.resume[(int64_t)v * G.n_bins + bin];
+    L.end = L.mend + (G.n_vis[v] - L.tail0);
+    L.tail = G.sorted + (int64_t)v * G.n;
+  }
+  return L;
+}
 
 bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera* cams, int n_views,
                  RasterGeom& G);

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
-  const int32_t start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
+  const BinList BL = bin_list(G, ids, ranges, v, bin);
+  const int32_t start = BL.start;
   int lx, ly, sx, sy;
   pixels_of(threadIdx.x, lx, ly, sx, sy);
   const int x0 = tx * kTile + lx, y = ty * kTile + ly;
@@ -227,7 +228,6 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const int32_t wlast = m;
   if (lane == 0) SSS_COUNT(7, wlast - start);
 
-  const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
   float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
@@ -260,10 +260,12 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     if (h <= lbeg || li < lbeg) return INT32_MAX;
     return use_list ? __ldg(tl + li) : li;
   };
-  auto id_at = [&](int32_t p) -> int32_t { return p < wlast ? __ldg(idv + p) : -1; };
+  auto id_at = [&](int32_t p) -> int32_t { return p < wlast ? BL.id(p) : -1; };
   auto issue = [&](int buf, int32_t p, int32_t id) -> int {
     bool ok = id >= 0;
-    if (FILTER && !use_list && ok) {
+    // unlisted replay: filter by the tile rect with bins, and always in the
+    // truncated list's tail (the depth-sorted visible set)
+    if (!use_list && ok && (FILTER || p >= BL.mend)) {
       const short4 r = rcv[id];
       ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
     }

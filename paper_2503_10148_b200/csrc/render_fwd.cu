@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
-  const int32_t start = ranges[((int64_t)v * G.n_bins + bin) * 2 + 0];
-  const int32_t end = ranges[((int64_t)v * G.n_bins + bin) * 2 + 1];
+  const BinList BL = bin_list(G, ids, ranges, v, bin);
+  const int32_t start = BL.start, end = BL.end;
   int lx, ly, sx, sy;
   pixels_of(threadIdx.x, lx, ly, sx, sy);
   const int x0 = tx * kTile + lx, y = ty * kTile + ly;
@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
 
-  const int32_t* idv = ids + (int64_t)v * G.capacity;
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
 
@@ -133,10 +132,11 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     unsigned long long cm = 0ull;  // REC: this warp's composited entries (warp-uniform bits)
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
-    const int32_t id = ok ? idv[pos] : 0;
+    const int32_t id = ok ? BL.id(pos) : 0;
     int slot, nb;
-    if (FILTER) {
-      if (ok) {
+    // the truncated list's tail is the depth-sorted visible set: always filtered
+    if (FILTER || end > BL.mend) {
+      if (ok && (FILTER || pos >= BL.mend)) {
         const short4 r = rcv[id];
         ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
       }
@@ -257,6 +257,11 @@ bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera
   G.n_bins = G.bins_x * div_up(G.tiles_y, 1 << G.shift);
   G.n = pr->n;
   G.capacity = bins->capacity;
+  const bool trunc = bins->max_per_bin > 0;
+  G.sorted = trunc ? bins->sorted : nullptr;
+  G.n_vis = trunc ? bins->n_vis : nullptr;
+  G.resume = trunc ? bins->resume : nullptr;
+  if (trunc && (!bins->sorted || !bins->n_vis || !bins->resume)) return false;
   return G.n_bins <= SSS_MAX_BINS && pr->n_views == n_views && bins->n_views == n_views;
 }
 

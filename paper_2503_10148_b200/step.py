@@ -37,7 +37,8 @@ class TrainStep:
                  views_per_batch: int = 16, bg=(0.0, 0.0, 0.0), headroom: float = 1.25,
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
-                 eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None):
+                 eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None,
+                 max_per_bin: int = 0):
         dev = planes.device
         world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
         # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
@@ -71,6 +72,7 @@ class TrainStep:
         self.cams = list(cameras)
         self.total_views = int(total_views if total_views is not None else len(self.cams))
         self.bin_shift = int(bin_shift)
+        self.max_per_bin = int(max_per_bin)  # > 0: truncated bin lists (sss.h sss_bins)
         self.bg = tuple(float(x) for x in bg)
         self.headroom = headroom
         self.group = group
@@ -117,14 +119,15 @@ class TrainStep:
             cams = [self.cams[v] for v in b]
             pv = self._proj_view(len(b))
             A.sss_project(self.params, cams, out=pv, cams_c=self.cams_c[bi])
-            probe = A.Bins.empty(len(b), self.n_bins, 0, self.bin_shift, False, self.params.planes.device)
+            probe = A.Bins.empty(len(b), self.n_bins, 0, self.bin_shift, False, self.params.planes.device,
+                                 self.max_per_bin, self.params.n)
             A.sss_bin_sort(pv, cams, bin_shift=self.bin_shift, ws=self.ws_bin, out=probe,
                            cams_c=self.cams_c[bi])
             cap = max(cap, int(probe.totals.max().item()))
         cap = int(cap * self.headroom * factor) + 4096
         vb = len(self.batches[0])
         self.bins = [A.Bins.empty(vb, self.n_bins, cap, self.bin_shift, False,
-                                  self.params.planes.device)]
+                                  self.params.planes.device, self.max_per_bin, self.params.n)]
         self.capacity = cap
 
     def _proj_view(self, nv: int) -> A.Projected:
@@ -140,9 +143,7 @@ class TrainStep:
                        f.tile_count[:nv] if f.tile_count is not None else None)
 
     def _bins_view(self, nv: int) -> A.Bins:
-        b = self.bins[0]
-        return A.Bins(b.bin_shift, b.capacity, b.ids[:nv], None, b.ranges[:nv], b.totals[:nv],
-                      b.overflow)
+        return self.bins[0].view(nv)
 
     # -- the iteration -----------------------------------------------------
     def forward_backward(self, targets: torch.Tensor) -> None:

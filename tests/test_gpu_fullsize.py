@@ -277,7 +277,7 @@ def test_config5_bench_launch(orc, sss):
         tv = tgt[v].reshape(3, -1)
         tv[:, torch.from_numpy(px).long().cuda()] = torch.from_numpy((rgb - sgn * off).astype(np.float32)).cuda()
         refs.append((v, px, sgn))
-    ws = torch.zeros(max(sss.render_bwd_workspace_bytes(sc.n, V), 4), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(sss.api.render_bwd_workspace_bytes(sc.n, V), 4), dtype=torch.uint8, device="cuda")
     loss = torch.zeros(1, device="cuda")
     g = sss.sss_render_bwd(params, pr, bins, cams, fr, target=tgt.contiguous(), loss=loss, ws=ws)
     torch.cuda.synchronize()

@@ -365,7 +365,7 @@ def test_stop_rule_pixel(orc, sss):
                          fr.n_contrib[0].cpu().numpy(), ref)
         d = torch.zeros((1, 3, 64, 64), device="cuda")
         d[0, :, 32, 32] = torch.tensor([1.0, -0.5, 0.25])
-        ws = torch.zeros(sss.render_bwd_workspace_bytes(sc.n, 1), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(sss.api.render_bwd_workspace_bytes(sc.n, 1), dtype=torch.uint8, device="cuda")
         g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws)
         torch.cuda.synchronize()
         gg = g.planes.cpu().numpy()
@@ -393,7 +393,7 @@ def test_alpha_clamp_zero_gradient(orc, sss):
         assert abs(abs(1.0 - float(fr.final_T[0, 32, 32].item())) - 0.99) <= 1e-7
         d = torch.zeros((1, 3, 64, 64), device="cuda")
         d[0, 0, 32, 32] = 1.0
-        ws = torch.zeros(sss.render_bwd_workspace_bytes(1, 1), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(sss.api.render_bwd_workspace_bytes(1, 1), dtype=torch.uint8, device="cuda")
         g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws)
         torch.cuda.synchronize()
         gg = g.planes.cpu().numpy()[:, 0]
@@ -574,3 +574,64 @@ def test_sghmc_plane_ranges_compose(sss):
             out[3][a0:a1] = part[3][a0:a1]
         for k in range(4):
             np.testing.assert_array_equal(out[k], full[k])
+
+
+@pytest.mark.parametrize("shift", [0, 1, 2])
+def test_truncated_bin_lists(orc, sss, scenes, shift):
+    """max_per_bin > 0 (sss.h): each bin keeps the first min(len, cap) entries
+    of its complete list (an exact prefix), resume[b] points one past the
+    cap-th entry in the depth-sorted visible order (n_vis for complete
+    lists), sorted[:n_vis] is the oracle's (depth, index) order, and the
+    raster -- continuing a truncated list through the rect-filtered tail --
+    gives the complete-list image bit for bit and the same gradients."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    for name in ("blobs_d2_3v", "stress_d1", "cfg2"):
+        sc = scenes[name]
+        V = sc.n_views
+        cam = sc.cameras[0]
+        params = to_dev(sc)
+        pr = sss.sss_project(params, sc.cameras)
+        full = sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift)
+        rf = full.ranges.cpu().numpy()
+        lens = rf[..., 1] - rf[..., 0]
+        for cap in (7, int(np.percentile(lens[lens > 0], 60)) + 1):
+            tb = sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift, max_per_bin=cap)
+            assert not sss.sss_check_overflow(tb)
+            rt = tb.ranges.cpu().numpy()
+            sorted_ = tb.sorted.cpu().numpy()
+            nvis = tb.n_vis.cpu().numpy()
+            resume = tb.resume.cpu().numpy()
+            for v in range(V):
+                o = orc.project(sc.params, sc.sh_degree, sc.cameras[v])
+                vis = o.n_tiles > 0
+                order = np.lexsort((np.arange(sc.n), o.depth.view(np.uint32)))
+                order = order[vis[order]]
+                assert nvis[v] == len(order)
+                assert np.array_equal(sorted_[v, :nvis[v]], order)
+                rank = np.empty(sc.n, np.int64)
+                rank[order] = np.arange(len(order))
+                fid, tid = full.ids[v].cpu().numpy(), tb.ids[v].cpu().numpy()
+                for b in range(rf.shape[1]):
+                    L = lens[v, b]
+                    k = min(L, cap)
+                    assert rt[v, b, 1] - rt[v, b, 0] == k
+                    pre = fid[rf[v, b, 0]:rf[v, b, 0] + k]
+                    assert np.array_equal(tid[rt[v, b, 0]:rt[v, b, 1]], pre)
+                    assert resume[v, b] == (nvis[v] if L <= cap else rank[pre[-1]] + 1), (name, v, b)
+            for tile_cap in (1536, 3):
+                f_full = sss.Frame.empty(V, cam.height, cam.width, tile_cap=tile_cap)
+                f_tr = sss.Frame.empty(V, cam.height, cam.width, tile_cap=tile_cap)
+                sss.sss_render_fwd(pr, full, sc.cameras, bg=(0.1, 0.2, 0.3), out=f_full)
+                sss.sss_render_fwd(pr, tb, sc.cameras, bg=(0.1, 0.2, 0.3), out=f_tr)
+                torch.cuda.synchronize()
+                assert torch.equal(f_full.rgb, f_tr.rgb) and torch.equal(f_full.final_T, f_tr.final_T)
+                assert torch.equal(f_full.n_contrib, f_tr.n_contrib)
+                d = torch.from_numpy(np.random.default_rng(2).normal(
+                    size=(V, 3, cam.height, cam.width)).astype(np.float32)).cuda()
+                g1 = sss.sss_render_bwd(params, pr, full, sc.cameras, f_full, bg=(0.1, 0.2, 0.3), d_rgb=d)
+                g2 = sss.sss_render_bwd(params, pr, tb, sc.cameras, f_tr, bg=(0.1, 0.2, 0.3), d_rgb=d)
+                torch.cuda.synchronize()
+                assert rel_l2(g2.planes.cpu().numpy(), g1.planes.cpu().numpy()) <= 1e-5, (name, cap, tile_cap)

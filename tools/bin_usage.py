@@ -47,6 +47,31 @@ for v in range(views):
             c = (Lt[j, i] - s0) if St[j, i] else n
             cons.append(c); lens.append(n); sat.append(St[j, i])
 cons, lens, sat = np.array(cons), np.array(lens), np.array(sat)
+# per bin (view-major): full length, max consumption over its tiles, all saturated
+nbv = rng.shape[1]
+bl = rng[..., 1] - rng[..., 0]
+bcons = np.zeros((views, nbv), np.int64)
+bsat = np.ones((views, nbv), bool)
+k = 0
+for v in range(views):
+    for j in range(ty):
+        for i in range(tx):
+            b = (j >> shift) * bx + (i >> shift)
+            bcons[v, b] = max(bcons[v, b], cons[k])
+            bsat[v, b] &= sat[k]
+            k += 1
+pol = {}
+for K in (4096, 8192, 16384, 32768):
+    over = cons > K  # tiles that would read the tail (their bin is longer than K)
+    pol[f"static_{K}"] = {"materialised_per_view": float(np.minimum(bl, K).sum() / views),
+                          "tiles_in_tail": int(over.sum()),
+                          "unsat_tiles_in_tail": int((over & ~sat).sum())}
+adapt = np.where(bsat, np.minimum(bl, (1.5 * bcons).astype(np.int64) + 256), bl)
+out["policy_adaptive_1p5"] = {"materialised_per_view": float(adapt.sum() / views),
+                              "bins_complete_unsat": int((~bsat & (bl > 4096)).sum()),
+                              "their_len_per_view": float(bl[~bsat & (bl > 4096)].sum() / views)}
+out["policies"] = pol
+out["full_per_view"] = float(bl.sum() / views)
 # per bin: the furthest any of its tiles reads
 out.update({
     "tiles": int(len(cons)), "frac_tiles_saturated": float(sat.mean()),
