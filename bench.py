@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--views-per-batch", type=int, default=64)
     ap.add_argument("--max-per-bin", type=int, default=0,
                     help="truncated bin lists (sss.h sss_bins.max_per_bin); 0 = complete lists")
+    ap.add_argument("--bins", default="adaptive", choices=["adaptive", "complete"],
+                    help="adaptive: per-bin caps from the previous forward's consumption (sss.h sss_bins.used)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row timings")
@@ -138,10 +140,29 @@ def ncu_traffic(kernel, views_per_launch):
     return int(b * views_per_launch / d.get("views_per_launch", views_per_launch))
 
 
+def alu_peaks():
+    """Measured FP32-pipe and MUFU rates of this GPU (sss_alu_peaks
+    microbenchmark) next to the nominal SMs x 128 lanes x
+    max clock."""
+    import ctypes as C
+
+    from paper_2503_10148_b200 import _lib as L
+
+    out = (C.c_double * 7)()
+    if L.load().sss_alu_peaks(out) != 0:
+        return None
+    sms, clk_khz = int(out[5]), out[6]
+    return {"ffma_lane_ops_per_s": out[0], "ffma2_lane_ops_per_s": out[1],
+            "fp32_lane_ops_per_s": max(out[0], out[1]),
+            "mufu_ex2_per_s": out[2], "mufu_lg2_per_s": out[3], "mufu_rcp_per_s": out[4],
+            "sm_count": sms, "sm_clock_mhz_attr": clk_khz / 1e3,
+            "how": "independent FFMA / FFMA2 / MUFU chains, 8 per thread, 8 CTAs x 256 threads per SM, best of 5"}
+
+
 def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, kernel=None):
     """Roofline entry of the dominant kernel (largest share of the timed step),
     or of `kernel` if given."""
-    lane_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6  # FP32 lane-ops/s (DESIGN.md §5)
+    lane_peak = pk["lane_peak"]  # FP32 lane-ops/s: measured (alu_peaks) or nominal
     hbm_peak = pk["hbm_gbs"] * 1e9
     table = {}
     pairs = counts["pairs"]
@@ -167,7 +188,7 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, ker
                  "peak": round(peak / 1e9, 2), "unit": unit, "frac": round(achieved / peak, 4),
                  "traffic": ncu_traffic(dom, views_per_launch),
                  "traffic_unit": "dram bytes per launch (ncu --set full, profiles/traffic.json)",
-                 "peak_source": pk["source"] + (" (148 SMs x 128 FP32 lanes x sm_max_mhz)" if bound == "alu" else " hbm_gbs"),
+                 "peak_source": (pk["lane_peak_source"] if bound == "alu" else pk["source"] + " hbm_gbs"),
                  "share_of_step": round(phase_ms[dom] / sum(phase_ms.values()), 3)}
 
 
@@ -294,7 +315,7 @@ def arm_config(a, sc, world):
     cam = sc.cameras[0]
     return {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": sc.n_views,
             "width": cam.width, "height": cam.height, "sh_degree": sc.sh_degree,
-            "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch, "max_per_bin": a.max_per_bin,
+            "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch, "max_per_bin": a.max_per_bin, "bins": a.bins,
             "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
                      if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
             "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
@@ -343,6 +364,7 @@ def main():
     rank, world, local = D.init()
     torch.cuda.set_device(local)
     P.load()
+    ap_meas = alu_peaks()
     sc = make_scene(a.config)
     V = sc.n_views
     mine = D.shard_views(V, rank, world)
@@ -352,7 +374,8 @@ def main():
     planes = torch.from_numpy(sc.params).cuda()
     hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
     ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
-                   views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim, max_per_bin=a.max_per_bin)
+                   views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim, max_per_bin=a.max_per_bin,
+                   adaptive_bins=a.bins == "adaptive")
     for _ in range(a.warmup):
         ts.step(targets)
         if ts.overflowed():
@@ -363,6 +386,8 @@ def main():
     cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip().isdigit()]
     clk = ClockSampler(int(cvd[local]) if local < len(cvd) else local)
     clk.start()
+    snap = ts.params.planes.clone()  # the first timed state (pair counts below)
+    torch.cuda.synchronize()
     P.launch_count(reset=True)
     ts.prof = []
     torch.cuda.synchronize()
@@ -384,18 +409,40 @@ def main():
     it_s = a.steps / (ms_max / 1e3)
     H, W = sc.cameras[0].height, sc.cameras[0].width
     mpix = it_s * V * H * W / 1e6
-    # ---- counts for the roofline (one extra untimed forward, same state)
+    # ---- counts for the roofline: composited pairs and instances of the
+    # timed states, measured (untimed) at the first and the last timed state
+    # and averaged (the counts drift slowly along the training trajectory)
     dev = torch.device("cuda", local)
-    ts.stats = {"pairs": torch.zeros((), dtype=torch.int64, device=dev),
-                "instances": torch.zeros((), dtype=torch.int64, device=dev)}
-    ts.forward_backward(targets)
-    pairs, inst = float(ts.stats["pairs"].item()), float(ts.stats["instances"].item())
-    ts.stats = None
+
+    def count_state():
+        ts.stats = {"pairs": torch.zeros((), dtype=torch.int64, device=dev),
+                    "instances": torch.zeros((), dtype=torch.int64, device=dev)}
+        ts.forward_backward(targets)
+        r = float(ts.stats["pairs"].item()), float(ts.stats["instances"].item())
+        ts.stats = None
+        return r
+
+    final = ts.params.planes.clone()
+    p_last, i_last = count_state()
+    ts.params.planes.copy_(snap)
+    p_first, i_first = count_state()
+    ts.params.planes.copy_(final)
+    del snap, final
+    pairs, inst = 0.5 * (p_first + p_last), 0.5 * (i_first + i_last)
     counts = {"steps": a.steps, "sghmc_planes": (ts.p1 - ts.p0) if ts.shard else sc.params.shape[0],
               "pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
               "launches_per_step": len(ts.batches) * a.steps,
               "pixels": len(mine) * a.steps * sc.cameras[0].width * sc.cameras[0].height}
     pk = peaks()
+    sms = ap_meas["sm_count"] if ap_meas else torch.cuda.get_device_properties(local).multi_processor_count
+    nominal = sms * 128 * pk["sm_max_mhz"] * 1e6
+    if ap_meas:
+        pk["lane_peak"] = ap_meas["fp32_lane_ops_per_s"]
+        pk["lane_peak_source"] = (f"measured (sss_alu_peaks: max of FFMA / FFMA2 lane-op rates; nominal "
+                                  f"{sms} SMs x 128 lanes x {pk['sm_max_mhz']:.0f} MHz = {nominal / 1e12:.2f} T)")
+    else:
+        pk["lane_peak"] = nominal
+        pk["lane_peak_source"] = f"nominal ({sms} SMs x 128 FP32 lanes x sm_max_mhz)"
     dom, roof = roofline_for(phases, counts, sc.n, len(mine) * a.steps, pk, 1,
                              views_per_launch=len(ts.batches[0]))
     # every timed phase against its own bound (informational; `roofline` is
@@ -492,7 +539,10 @@ def main():
             "gpu_launches": int(launches),
             "next_rows": next_rows,
             "clocks": clocks,
+            "alu_peaks": ap_meas,
             "bin_overflow": bool(overflow),
+            "counts_per_step": {"pairs_first": p_first, "pairs_last": p_last, "instances_first": i_first,
+                                "instances_last": i_last},
         }
         print(json.dumps(line), flush=True)
     D.barrier()

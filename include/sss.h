@@ -127,6 +127,15 @@ typedef struct {
  *  resume   [V][n_bins] (nullable if max_per_bin == 0): position in sorted
  *           one past the bin's last materialised entry; n_vis[v] if the
  *           list is complete
+ *  used     [V][n_bins] nullable: adaptive truncation.  sss_render_fwd with
+ *           these bins writes each bin's consumption (the list length its
+ *           tiles needed: up to the last composited entry if every pixel of
+ *           the tile stopped, 2^30 if some pixel is still live at the end);
+ *           the next sss_bin_sort caps bin b at min(max_per_bin, 2 used + 1024)
+ *           (no cap for used < 0 or >= 2^30: initialise to -1) and resets
+ *           used to 0 for the forward that follows.  Truncation (either
+ *           kind) never changes the raster's results; a tile that needs
+ *           more than its bin kept reads the tail (slower).
  *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
  *           scattered for that view and its ranges are empty; grow and
  *           retry).  Sticky: sss_bin_sort only ever sets it; the caller
@@ -146,6 +155,7 @@ typedef struct {
   int32_t* sorted;
   int32_t* n_vis;
   int32_t* resume;
+  int32_t* used;
 } sss_bins;
 
 /* Rendered frames (output of sss_render_fwd; all views share one size).
@@ -325,6 +335,13 @@ SSS_API sss_status sss_relocate(sss_params* p, sss_params* adam_m, sss_params* a
 SSS_API sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_params* adam_m,
                           sss_params* adam_v, float* momentum, const sss_sghmc_hparams* hp,
                           void* stream);
+
+/* Measurement infrastructure (not on the hot path): microbenchmarks of the
+ * current device's FP32 pipe and MUFU throughput (the
+ * roofline denominators are measured, not assumed).  out (host double[7]):
+ * scalar FFMA lane-ops/s, FFMA2 lane-ops/s (2 per lane), MUFU ex2, lg2 and
+ * rcp ops/s, SM count, SM clock in kHz.  Synchronous; ~0.1 s.  0 = ok. */
+SSS_API int sss_alu_peaks(double* out);
 
 SSS_API const char* sss_status_string(sss_status s);
 SSS_API const char* sss_last_error(void);

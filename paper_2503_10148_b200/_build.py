@@ -19,7 +19,8 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsss.so")
 BUILD = os.path.join(PKG, "build")
 
-SOURCES = ["abi.cu", "project.cu", "binsort.cu", "render_fwd.cu", "render_bwd.cu", "sghmc.cu", "loss.cu", "relocate.cu"]
+SOURCES = ["abi.cu", "project.cu", "binsort.cu", "render_fwd.cu", "render_bwd.cu", "sghmc.cu", "loss.cu", "relocate.cu",
+           "peaks.cu"]
 PER_FILE = {"project.cu": ["-fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

@@ -26,7 +26,7 @@ SSS_BWD_PROJECTION_ONLY = 4
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",
            "sss_image_loss_workspace", "sss_image_loss", "sss_relocate_workspace", "sss_relocate",
-           "sss_status_string", "sss_last_error", "sss_launch_count"]
+           "sss_status_string", "sss_last_error", "sss_launch_count", "sss_alu_peaks"]
 
 
 class sss_camera(C.Structure):
@@ -51,7 +51,7 @@ class sss_bins(C.Structure):
                 ("ids", C.c_void_p), ("keys", C.c_void_p), ("ranges", C.c_void_p),
                 ("totals", C.c_void_p), ("overflow", C.c_void_p), ("max_per_bin", C.c_int32),
                 ("reserved", C.c_int32), ("sorted", C.c_void_p), ("n_vis", C.c_void_p),
-                ("resume", C.c_void_p)]
+                ("resume", C.c_void_p), ("used", C.c_void_p)]
 
 
 class sss_frame(C.Structure):
@@ -119,6 +119,7 @@ def load(path: str = LIB_PATH):
         "sss_status_string": (C.c_char_p, [C.c_int]),
         "sss_last_error": (C.c_char_p, []),
         "sss_launch_count": (C.c_int64, [C.c_int32]),
+        "sss_alu_peaks": (C.c_int, [C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -127,13 +127,16 @@ class Bins:
     sorted: Optional[torch.Tensor] = None  # [V][n] i32 depth-sorted visible ids
     n_vis: Optional[torch.Tensor] = None   # [V] i32
     resume: Optional[torch.Tensor] = None  # [V][n_bins] i32
+    used: Optional[torch.Tensor] = None    # [V][n_bins] i32: adaptive truncation (sss.h)
 
     @classmethod
     def empty(cls, V: int, n_bins: int, capacity: int, bin_shift: int, keys: bool,
-              device="cuda", max_per_bin: int = 0, n: int = 0) -> "Bins":
-        """n: components (needed for the sorted array when max_per_bin > 0)."""
+              device="cuda", max_per_bin: int = 0, n: int = 0, adaptive: bool = False) -> "Bins":
+        """n: components (needed for the sorted array when truncating).
+        adaptive: per-bin caps from the previous forward's consumption (the
+        first call, with used = -1, builds complete lists)."""
         cap = max(int(capacity), 1)
-        trunc = int(max_per_bin) > 0
+        trunc = int(max_per_bin) > 0 or adaptive
         return cls(bin_shift, int(capacity),
                    torch.empty((V, cap), dtype=torch.int32, device=device),
                    torch.empty((V, cap), dtype=torch.int64, device=device) if keys else None,
@@ -143,13 +146,14 @@ class Bins:
                    int(max_per_bin),
                    torch.empty((V, max(int(n), 1)), dtype=torch.int32, device=device) if trunc else None,
                    torch.zeros((V,), dtype=torch.int32, device=device) if trunc else None,
-                   torch.empty((V, n_bins), dtype=torch.int32, device=device) if trunc else None)
+                   torch.empty((V, n_bins), dtype=torch.int32, device=device) if trunc else None,
+                   torch.full((V, n_bins), -1, dtype=torch.int32, device=device) if adaptive else None)
 
     def c(self) -> L.sss_bins:
         return L.sss_bins(self.bin_shift, int(self.totals.shape[0]), self.capacity, _ptr(self.ids),
                           _ptr(self.keys), _ptr(self.ranges), _ptr(self.totals),
                           _ptr(self.overflow), int(self.max_per_bin), 0, _ptr(self.sorted),
-                          _ptr(self.n_vis), _ptr(self.resume))
+                          _ptr(self.n_vis), _ptr(self.resume), _ptr(self.used))
 
     def view(self, nv: int) -> "Bins":
         """The first nv views (shared storage)."""
@@ -158,7 +162,8 @@ class Bins:
                     self.totals[:nv], self.overflow, self.max_per_bin,
                     self.sorted[:nv] if self.sorted is not None else None,
                     self.n_vis[:nv] if self.n_vis is not None else None,
-                    self.resume[:nv] if self.resume is not None else None)
+                    self.resume[:nv] if self.resume is not None else None,
+                    self.used[:nv] if self.used is not None else None)
 
 
 TILE_CAP = 1536  # composited entries per 16x8 strip the forward records for the backward

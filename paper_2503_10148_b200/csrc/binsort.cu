@@ -80,7 +80,7 @@ constexpr int64_t kScatterStageMax = SSS_SCATTER_STAGE_MAX;  // staged ids per c
 
 struct WsLayout {
   size_t keys_a, keys_b, vals_a, vals_b, sorted, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start,
-      total;
+      bin_cap, total;
   int tiles_per_view, n_chunks, chunk;
 };
 
@@ -105,6 +105,7 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
   L.bin_total = take((size_t)V * g.n_bins * 4);
   L.bin_start = take((size_t)V * g.n_bins * 4);
+  L.bin_cap = take((size_t)V * g.n_bins * 4);
   L.total = off;
   return L;
 }
@@ -213,8 +214,22 @@ __global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* _
 // per view: exclusive scan over bins of the materialised counts
 // min(total_b, cap) -> bin_start, ranges, totals, overflow; resume = n_vis
 // for complete lists (the scatter writes it for truncated ones)
+// Per-bin cap: the static max_per_bin (0xFFFFFFFF = none), or, with `used`
+// (the previous sss_render_fwd's per-bin consumption), 2 used + 1024 capped
+// by it; used < 0 or >= 2^30 (unknown, or a tile with a pixel still live at
+// the end of its list) keeps the static cap.  `used` is reset to 0 for the
+// forward that follows.
+__device__ __forceinline__ uint32_t bin_cap_of(uint32_t static_cap, int32_t* used, size_t k) {
+  if (!used) return static_cap;
+  const int32_t u = used[k];
+  used[k] = 0;
+  if (u < 0 || u >= (1 << 30)) return static_cap;
+  return min(static_cap, 2u * (uint32_t)u + 1024u);
+}
+
 __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restrict__ bin_total, int n_bins,
-                                                        int64_t capacity, uint32_t cap,
+                                                        int64_t capacity, uint32_t static_cap,
+                                                        int32_t* __restrict__ used, uint32_t* __restrict__ bcap,
                                                         uint32_t* __restrict__ bin_start,
                                                         int32_t* __restrict__ ranges,
                                                         int64_t* __restrict__ totals,
@@ -228,7 +243,11 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   const int per = (n_bins + 1023) / 1024;
   const int lo = t * per, hi = min(lo + per, n_bins);
   unsigned long long s = 0;
-  for (int k = lo; k < hi; ++k) s += min(bt[k], cap);
+  for (int k = lo; k < hi; ++k) {
+    const uint32_t c = bin_cap_of(static_cap, used, (size_t)v * n_bins + k);
+    bcap[(size_t)v * n_bins + k] = c;
+    s += min(bt[k], c);
+  }
   part[t] = s;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
@@ -247,6 +266,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   unsigned long long run = part[t] - s;
   for (int k = lo; k < hi; ++k) {
     const uint32_t full = bt[k];
+    const uint32_t cap = bcap[(size_t)v * n_bins + k];
     const uint32_t x = min(full, cap);
     if (resume && full <= cap) resume[(size_t)v * n_bins + k] = n_vis[v];
     bin_start[(size_t)v * n_bins + k] = (uint32_t)run;
@@ -272,7 +292,7 @@ struct alignas(16) WalkScratch {
 
 // Truncation state of one scatter CTA (chunk): see the file header.
 struct TruncCtx {
-  uint32_t cap;                       // max_per_bin, or UINT32_MAX
+  const uint32_t* cap;                // [n_bins] per-bin caps (UINT32_MAX: none)
   const uint32_t* openm;              // smem bit per bin: something of the bin is kept in this chunk
   const uint32_t* ch;                 // the chunk's index of each bin in its full list (global)
   const uint32_t* bs;                 // materialised start of each bin (global)
@@ -426,7 +446,8 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
               if (!STAGED && kv) kv[pos] = ((uint64_t)b << 32) | S.dbits[own];
               if (pos + 1 == lim && tc.resume) {  // last kept of this chunk: is it the cap-th entry?
                 const uint32_t idx = STAGED ? tc.ch[b] + (pos - soff[b]) : pos - tc.bs[b];
-                if (idx + 1 == tc.cap && tc.btot[b] > tc.cap) tc.resume[b] = S.spos[own] + 1;
+                const uint32_t cb = tc.cap[b];
+                if (idx + 1 == cb && tc.btot[b] > cb) tc.resume[b] = S.spos[own] + 1;
               }
             }
           }
@@ -457,7 +478,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
     const uint32_t* __restrict__ chunk_hist, const uint8_t* __restrict__ warp_hist,
     const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ bin_total,
-    const int64_t* __restrict__ totals, int64_t capacity, uint32_t cap, int stage_cap,
+    const int64_t* __restrict__ totals, int64_t capacity, const uint32_t* __restrict__ bin_cap, int stage_cap,
     int32_t* __restrict__ ids, uint64_t* __restrict__ keys, int32_t* __restrict__ resume) {
   extern __shared__ uint4 sm4[];
   __shared__ uint32_t red[kScatterWarps];
@@ -466,7 +487,8 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const int64_t lo = (int64_t)c * kChunk;
   const int64_t nvis = n_vis[v];
   if (lo >= nvis) return;
-  const bool trunc = cap != 0xFFFFFFFFu;
+  const bool trunc = resume != nullptr;
+  const uint32_t* bcv = bin_cap + (size_t)v * g.n_bins;
   const int nb = g.n_bins;
   WalkScratch* scratch = reinterpret_cast<WalkScratch*>(sm4);             // [8]
   uint32_t* wbase = reinterpret_cast<uint32_t*>(scratch + kScatterWarps);  // [8][n_bins] next slot per bin
@@ -489,7 +511,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     uint32_t cb = 0;
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
-    const uint32_t cs = ch[b];
+    const uint32_t cs = ch[b], cap = bcv[b];
     mine += cs >= cap ? 0u : min(cb, cap - cs);
   }
   uint32_t incl = mine;
@@ -513,13 +535,13 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     uint32_t cb = 0;
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
-    const uint32_t cs = ch[b];
+    const uint32_t cs = ch[b], cap = bcv[b];
     const uint32_t kept = cs >= cap ? 0u : min(cb, cap - cs);
     const uint32_t gb = bs[b] + cs;
     gst[b] = gb;
     // staged: the stage offset of the bin's kept run; direct: the bin's
     // global limit (its materialised start + cap)
-    soff[b] = staged ? run : (trunc ? bs[b] + cap : 0xFFFFFFFFu);
+    soff[b] = staged ? run : (cap != 0xFFFFFFFFu ? bs[b] + cap : 0xFFFFFFFFu);
     uint32_t acc = staged ? run : gb;  // + exclusive prefix of the per-warp counts
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
@@ -541,7 +563,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  const TruncCtx tc{cap, openm, ch, bs, bin_total + (size_t)v * nb, resume ? resume + (size_t)v * nb : nullptr};
+  const TruncCtx tc{bcv, openm, ch, bs, bin_total + (size_t)v * nb, resume ? resume + (size_t)v * nb : nullptr};
   uint32_t* wb = wbase + (size_t)w * nb;
   if (!staged) {
     if (trunc) warp_walk<false, true>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], idv, kv, soff, tc);
@@ -596,8 +618,9 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     set_error("sss_bin_sort: null output buffer");
     return SSS_ERR_ARG;
   }
-  if (out->max_per_bin < 0 || (out->max_per_bin > 0 && (!out->sorted || !out->n_vis || !out->resume))) {
-    set_error("sss_bin_sort: max_per_bin > 0 needs sorted, n_vis and resume (and max_per_bin >= 0)");
+  if (out->max_per_bin < 0 ||
+      ((out->max_per_bin > 0 || out->used) && (!out->sorted || !out->n_vis || !out->resume))) {
+    set_error("sss_bin_sort: truncated lists (max_per_bin > 0 or used) need sorted, n_vis and resume");
     return SSS_ERR_ARG;
   }
   if (n > 0x7fffffffLL - out->capacity) {  // virtual list positions (start + n) must fit int32
@@ -623,8 +646,10 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   uint32_t* btot = (uint32_t*)(w + L.bin_total);
   uint32_t* bstart = (uint32_t*)(w + L.bin_start);
   const short4* rect = (const short4*)pr->rect;
-  const uint32_t cap = out->max_per_bin > 0 ? (uint32_t)out->max_per_bin : 0xFFFFFFFFu;
-  int32_t* resume = out->max_per_bin > 0 ? out->resume : nullptr;
+  const bool trunc = out->max_per_bin > 0 || out->used;
+  const uint32_t static_cap = out->max_per_bin > 0 ? (uint32_t)out->max_per_bin : 0xFFFFFFFFu;
+  int32_t* resume = trunc ? out->resume : nullptr;
+  uint32_t* bcap = (uint32_t*)(w + L.bin_cap);
 
   static thread_local bool attr_set = false;
   if (!attr_set) {  // large dynamic shared memory for the per-warp bin counters
@@ -646,8 +671,8 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     cudaMemsetAsync(btot, 0, sizeof(uint32_t) * n_views * g.n_bins, s);
     cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   }
-  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, cap, bstart, out->ranges, out->totals,
-                                            out->overflow, n_vis, resume);
+  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, static_cap, out->used, bcap, bstart,
+                                            out->ranges, out->totals, out->overflow, n_vis, resume);
   count_launch();
   if (n > 0) {
     // stage: the chunk's mean share of the capacity (the caller sizes the
@@ -663,7 +688,7 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     const size_t ssm = fixed + (size_t)stage_cap * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
         sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, btot, out->totals,
-        out->capacity, cap, stage_cap, out->ids, out->keys, resume);
+        out->capacity, bcap, stage_cap, out->ids, out->keys, resume);
     count_launch();
   }
   return check_launch("sss_bin_sort");

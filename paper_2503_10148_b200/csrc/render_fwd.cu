@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
   __shared__ int32_t spos[kBatch];
+  __shared__ uint8_t smask[kBatch];  // bit w: the entry's ellipse may meet warp w's strip
   __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
@@ -133,39 +134,47 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? BL.id(pos) : 0;
-    int slot, nb;
-    // the truncated list's tail is the depth-sorted visible set: always filtered
-    if (FILTER || end > BL.mend) {
-      if (ok && (FILTER || pos >= BL.mend)) {
-        const short4 r = rcv[id];
-        ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      if (lane == 0) wcnt[w] = __popc(bal);
-      __syncthreads();
-      int off = 0, tot = 0;
-#pragma unroll
-      for (int k = 0; k < kRasterWarps; ++k) {
-        const int c = wcnt[k];
-        off += k < w ? c : 0;
-        tot += c;
-      }
-      slot = off + __popc(bal & lt);
-      nb = tot;
-    } else {
-      slot = threadIdx.x;
-      nb = min(kBatch, end - b0);
+    // the truncated list's tail is the depth-sorted visible set: always rect-filtered
+    if (ok && (FILTER || pos >= BL.mend)) {
+      const short4 r = rcv[id];
+      ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
     }
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    int off = 0, nb = 0;
+#pragma unroll
+    for (int k = 0; k < kRasterWarps; ++k) {
+      const int c = wcnt[k];
+      off += k < w ? c : 0;
+      nb += c;
+    }
+    const int slot = off + __popc(bal & lt);
     if (ok) {
       spos[slot] = pos;
-      sa[slot] = rv[(int64_t)id * 3 + 0];
-      sb[slot] = rv[(int64_t)id * 3 + 1];
+      const float4 ra = rv[(int64_t)id * 3 + 0];
+      const float4 rb = rv[(int64_t)id * 3 + 1];
+      sa[slot] = ra;
+      sb[slot] = rb;
       sc[slot] = rv[(int64_t)id * 3 + 2];
+      // per strip (warp): can the entry's ellipse reach any pixel centre of it?
+      const float X0 = (float)(tx * kTile) + 0.5f, Y0 = (float)(ty * kTile) + 0.5f;
+      unsigned m = 0;
+#pragma unroll
+      for (int s = 0; s < kRasterWarps; ++s) {
+        const float sy0 = Y0 + (float)(s * kWarpH);
+        m |= ellipse_meets_box(ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, X0, X0 + (float)(kWarpW - 1), sy0,
+                               sy0 + (float)(kWarpH - 1))
+                 ? (1u << s)
+                 : 0u;
+      }
+      smask[slot] = (uint8_t)m;
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     const int nb_w = __all_sync(0xffffffffu, all_done()) ? 0 : nb;  // warp already finished
     for (int j = 0; j < nb_w; ++j) {
+      if (!((smask[j] >> w) & 1u)) continue;  // the ellipse misses this strip (warp-uniform)
       if (lane == 0) SSS_COUNT(1, 1);
       const float4 a = sa[j];
       const float4 b = sb[j];  // {C, hmax, o, inv_nu}
@@ -227,6 +236,15 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     }
   }
   if (REC && lane == 0) tile_count[lslot] = n_rec;
+  if (G.used) {  // adaptive truncation: how much of the bin list this tile needed
+    const bool done = __syncthreads_and(all_done());
+    int32_t mx = lastc[0];
+#pragma unroll
+    for (int k = 1; k < kPX; ++k) mx = max(mx, lastc[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(&G.used[(int64_t)v * G.n_bins + bin], done ? mx - start : (1 << 30));
+  }
   const int64_t HW = (int64_t)G.width * G.height;
 #pragma unroll
   for (int k = 0; k < kPX; ++k) {
@@ -257,10 +275,11 @@ bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera
   G.n_bins = G.bins_x * div_up(G.tiles_y, 1 << G.shift);
   G.n = pr->n;
   G.capacity = bins->capacity;
-  const bool trunc = bins->max_per_bin > 0;
+  const bool trunc = bins->max_per_bin > 0 || bins->used;
   G.sorted = trunc ? bins->sorted : nullptr;
   G.n_vis = trunc ? bins->n_vis : nullptr;
   G.resume = trunc ? bins->resume : nullptr;
+  G.used = bins->used;
   if (trunc && (!bins->sorted || !bins->n_vis || !bins->resume)) return false;
   return G.n_bins <= SSS_MAX_BINS && pr->n_views == n_views && bins->n_views == n_views;
 }

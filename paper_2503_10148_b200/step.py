@@ -38,7 +38,7 @@ class TrainStep:
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
                  eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None,
-                 max_per_bin: int = 0):
+                 max_per_bin: int = 0, adaptive_bins: bool = False):
         dev = planes.device
         world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
         # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
@@ -73,6 +73,9 @@ class TrainStep:
         self.total_views = int(total_views if total_views is not None else len(self.cams))
         self.bin_shift = int(bin_shift)
         self.max_per_bin = int(max_per_bin)  # > 0: truncated bin lists (sss.h sss_bins)
+        # adaptive truncation: each view batch keeps its bins' consumption from
+        # the previous iteration's forward (sss.h sss_bins.used; -1 = complete)
+        self.adaptive_bins = bool(adaptive_bins)
         self.bg = tuple(float(x) for x in bg)
         self.headroom = headroom
         self.group = group
@@ -101,6 +104,8 @@ class TrainStep:
             self.ws_loss = torch.empty(max(A.image_loss_workspace_bytes(vb, H, W), 4),
                                        dtype=torch.uint8, device=dev)
         self.bins: List[A.Bins] = []
+        self.used = ([torch.full((len(b), self.n_bins), -1, dtype=torch.int32, device=dev) for b in self.batches]
+                     if self.adaptive_bins else None)
         self.prof = None  # list of (phase, cuda event) when timing phases
         self.stats = None  # dict of device counters (pairs, instances) when counting
         self._size_bins()
@@ -127,7 +132,8 @@ class TrainStep:
         cap = int(cap * self.headroom * factor) + 4096
         vb = len(self.batches[0])
         self.bins = [A.Bins.empty(vb, self.n_bins, cap, self.bin_shift, False,
-                                  self.params.planes.device, self.max_per_bin, self.params.n)]
+                                  self.params.planes.device, self.max_per_bin, self.params.n,
+                                  adaptive=self.adaptive_bins)]
         self.capacity = cap
 
     def _proj_view(self, nv: int) -> A.Projected:
@@ -157,6 +163,8 @@ class TrainStep:
             cams = [self.cams[v] for v in b]
             cc = self.cams_c[bi]
             pv, fv, bv = self._proj_view(nv), self._frame_view(nv), self._bins_view(nv)
+            if self.used is not None:
+                bv.used = self.used[bi]
             tg = targets[b[0]:b[-1] + 1]
             A.sss_project(self.params, cams, out=pv, cams_c=cc)
             self._mark("project")

@@ -635,3 +635,51 @@ def test_truncated_bin_lists(orc, sss, scenes, shift):
                 g2 = sss.sss_render_bwd(params, pr, tb, sc.cameras, f_tr, bg=(0.1, 0.2, 0.3), d_rgb=d)
                 torch.cuda.synchronize()
                 assert rel_l2(g2.planes.cpu().numpy(), g1.planes.cpu().numpy()) <= 1e-5, (name, cap, tile_cap)
+
+
+def test_adaptive_bin_caps(orc, sss, scenes):
+    """sss_bins.used: the forward records each bin's consumption, the next
+    bin_sort caps the bin at 2 used + 1024.  Round 1 (used = -1) builds
+    complete lists; round 2 truncates from round 1's consumption; round 3
+    starts from used = 0 (caps of 1024 for every bin: many tiles read the
+    rect-filtered tail).  All three render the complete-list image bit for
+    bit and give its gradients."""
+    import torch
+
+    from gpu_helpers import to_dev
+    from paper_2503_10148_b200 import api as A
+
+    for name in ("blobs_d2_3v", "cfg2", "stress_d1"):
+        sc = scenes[name]
+        V, cam = sc.n_views, sc.cameras[0]
+        params = to_dev(sc)
+        pr = sss.sss_project(params, sc.cameras)
+        full = sss.sss_bin_sort(pr, sc.cameras, bin_shift=2)
+        f0 = sss.Frame.empty(V, cam.height, cam.width)
+        sss.sss_render_fwd(pr, full, sc.cameras, out=f0)
+        d = torch.from_numpy(np.random.default_rng(4).normal(size=(V, 3, cam.height, cam.width))
+                             .astype(np.float32)).cuda()
+        g0 = sss.sss_render_bwd(params, pr, full, sc.cameras, f0, d_rgb=d).planes.cpu().numpy()
+        nb = full.ranges.shape[1]
+        ab = A.Bins.empty(V, nb, full.capacity, 2, False, "cuda", 0, sc.n, adaptive=True)
+        lens0 = (full.ranges[..., 1] - full.ranges[..., 0]).cpu().numpy()
+        for rnd in range(3):
+            if rnd == 2:
+                ab.used.zero_()
+            sss.sss_bin_sort(pr, sc.cameras, bin_shift=2, out=ab)
+            f = sss.Frame.empty(V, cam.height, cam.width)
+            sss.sss_render_fwd(pr, ab, sc.cameras, out=f)
+            torch.cuda.synchronize()
+            lens = (ab.ranges[..., 1] - ab.ranges[..., 0]).cpu().numpy()
+            if rnd == 0:
+                assert np.array_equal(lens, lens0)
+            else:
+                assert np.all(lens <= lens0)
+            assert torch.equal(f.rgb, f0.rgb) and torch.equal(f.final_T, f0.final_T), (name, rnd)
+            assert torch.equal(f.n_contrib, f0.n_contrib), (name, rnd)
+            g = sss.sss_render_bwd(params, pr, ab, sc.cameras, f, d_rgb=d).planes.cpu().numpy()
+            assert rel_l2(g, g0) <= 1e-5, (name, rnd)
+            used = ab.used.cpu().numpy()
+            assert np.all(used >= 0)
+        if name == "cfg2":
+            assert (lens < lens0).any()  # round 3 truncated something
