@@ -7,11 +7,14 @@
 //
 // B200 design — two stages instead of one 64-bit key sort over all M
 // instances:
-//   1. a stable LSD radix sort (8-bit digits) of the per-view depth keys
-//      read straight from the projection: culled components are dropped (the
-//      first pass compacts), passes whose digit is constant over the view are
-//      skipped (radix.cuh depth mode); each pass reorders its 4096-key tile
-//      by digit in shared memory so the global stores leave as per-digit runs;
+//   1. a stable LSD radix sort (4 x 8-bit digits) of the N per-view depth keys
+//      (keys of culled components are 0xFFFFFFFF and sort last, so the first
+//      n_vis sorted entries are the visible components); each pass reorders
+//      its 4096-key tile by digit in shared memory so the global stores leave
+//      as per-digit runs (a depth mode reading the projection directly,
+//      dropping culled keys and skipping constant digits, measured slower at
+//      config 5: no digit is constant there and the extra operand logic cost
+//      occupancy);
 //   2. a stable counting scatter of the instances by bin, generated on the fly
 //      from the depth-sorted components: per-chunk bin histograms (shared
 //      memory), a column scan over chunks, a scan over bins, then a scatter in
@@ -80,7 +83,7 @@ constexpr int64_t kScatterStageMax = SSS_SCATTER_STAGE_MAX;  // staged ids per c
 
 struct WsLayout {
   size_t keys_a, keys_b, vals_a, vals_b, sorted, n_vis, radix_hist, chunk_hist, warp_hist, bin_total, bin_start,
-      bin_cap, total;
+      bin_cap, chunk_kept, total;
   int tiles_per_view, n_chunks, chunk;
 };
 
@@ -100,14 +103,77 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.vals_b = take(nv * 4);
   L.sorted = take(nv * 4);  // used when the caller passes no sorted array
   L.n_vis = take((size_t)V * 4);
-  L.radix_hist = take(depth_sort_ws_words(L.tiles_per_view, V) * 4);
+  L.radix_hist = take(radix_ws_words(L.tiles_per_view, V) * 4);
   L.chunk_hist = take((size_t)V * L.n_chunks * (size_t)g.n_bins * 4);
   L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
   L.bin_total = take((size_t)V * g.n_bins * 4);
   L.bin_start = take((size_t)V * g.n_bins * 4);
   L.bin_cap = take((size_t)V * g.n_bins * 4);
+  L.chunk_kept = take((size_t)V * L.n_chunks * ((g.n_bins + 31) / 32) * 4);
   L.total = off;
   return L;
+}
+
+// ------------------------------------------------------------- depth keys
+__global__ void keys_init_kernel(const float* __restrict__ depth, const short4* __restrict__ rect,
+                                 int64_t n, uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                 int32_t* __restrict__ n_vis) {
+  const int v = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool vis = false;
+  if (i < n) {
+    const short4 r = rect[(int64_t)v * n + i];
+    vis = r.x <= r.z;
+    keys[(int64_t)v * n + i] = vis ? __float_as_uint(depth[(int64_t)v * n + i]) : 0xFFFFFFFFu;
+    vals[(int64_t)v * n + i] = (int32_t)i;
+  }
+  // one atomic per block (per-warp atomics on one address serialise)
+  __shared__ int32_t wsum[8];
+  const unsigned b = __ballot_sync(0xffffffffu, vis);
+  if (lane_id() == 0) wsum[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
+    if (s) atomicAdd(&n_vis[v], s);
+  }
+}
+
+// The same with four consecutive components per thread and 16-byte accesses
+// (n % 4 == 0: every view's segment starts 16-byte aligned).
+__global__ void keys_init4_kernel(const float4* __restrict__ depth, const int4* __restrict__ rect,
+                                  int64_t n, uint4* __restrict__ keys, int4* __restrict__ vals,
+                                  int32_t* __restrict__ n_vis) {
+  const int v = blockIdx.y;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // quad index in the view
+  const int64_t nq = n >> 2;
+  int cnt = 0;
+  if (q < nq) {
+    const int64_t o = (int64_t)v * nq + q;
+    const int4 r01 = rect[2 * o], r23 = rect[2 * o + 1];  // two short4 per int4
+    const float4 d = depth[o];
+    // short4 {x0, y0, x1, y1}: visible iff x0 <= x1 (low halves of words 0 and 1)
+    const bool v0 = (short)(r01.x & 0xffff) <= (short)(r01.y & 0xffff);
+    const bool v1 = (short)(r01.z & 0xffff) <= (short)(r01.w & 0xffff);
+    const bool v2 = (short)(r23.x & 0xffff) <= (short)(r23.y & 0xffff);
+    const bool v3 = (short)(r23.z & 0xffff) <= (short)(r23.w & 0xffff);
+    keys[o] = make_uint4(v0 ? __float_as_uint(d.x) : 0xFFFFFFFFu, v1 ? __float_as_uint(d.y) : 0xFFFFFFFFu,
+                         v2 ? __float_as_uint(d.z) : 0xFFFFFFFFu, v3 ? __float_as_uint(d.w) : 0xFFFFFFFFu);
+    const int32_t i0 = (int32_t)(4 * q);
+    vals[o] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+    cnt = (int)v0 + (int)v1 + (int)v2 + (int)v3;
+  }
+  __shared__ int32_t wsum[8];
+  int c = cnt;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if (lane_id() == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += wsum[k];
+    if (s) atomicAdd(&n_vis[v], s);
+  }
 }
 
 // ------------------------------------------------------- bin histograms
@@ -118,8 +184,9 @@ __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0
 // Per (chunk, view): bin counts of the chunk's instances, per warp of the
 // scatter's partition (warp w owns kChunk/8 consecutive depth-sorted
 // components).  Writes the chunk totals (u32, for the scans) and the per-warp
-// counts (u8: a warp's 128 components hit a bin at most 128 times), so the
-// scatter needs no counting pass of its own.
+// counts (u8: a warp's 128 components hit a bin at most 128 times; the 8
+// warps' counts of a bin packed in one u64), so the scatter needs no counting
+// pass of its own.
 __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
                                                          const int32_t* __restrict__ n_vis,
                                                          const short4* __restrict__ rect, int64_t n,
@@ -145,15 +212,18 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
   }
   __syncthreads();
   uint32_t* out = chunk_hist + ((size_t)v * n_chunks + c) * nb;
-  uint8_t* wout = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
+  uint64_t* wout = reinterpret_cast<uint64_t*>(warp_hist) + ((size_t)v * n_chunks + c) * nb;
+  static_assert(kScatterWarps == 8, "8 per-warp byte counts per u64");
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     uint32_t t = 0;
+    uint64_t packed = 0;
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
       const uint32_t x = hs[(size_t)ww * nb + b];
-      wout[(size_t)ww * nb + b] = (uint8_t)x;
+      packed |= (uint64_t)x << (8 * ww);
       t += x;
     }
+    wout[b] = packed;
     out[b] = t;
   }
 }
@@ -167,8 +237,26 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
 #define SSS_COLSCAN_WARPS 32
 #endif
 constexpr int kColWarps = SSS_COLSCAN_WARPS;  // warps splitting the chunk range of 32 bins
+// Per-bin cap: the static max_per_bin (0xFFFFFFFF = none), or, with `used`
+// (the previous sss_render_fwd's per-bin consumption), 2 used + 1024 capped
+// by it; used < 0 or >= 2^30 (unknown, or a tile with a pixel still live at
+// the end of its list) keeps the static cap.
+__device__ __forceinline__ uint32_t bin_cap_of(uint32_t static_cap, const int32_t* used, size_t k) {
+  if (!used) return static_cap;
+  const int32_t u = used[k];
+  if (u < 0 || u >= (1 << 30)) return static_cap;
+  return min(static_cap, 2u * (uint32_t)u + 1024u);
+}
+
+// The column scan also applies the caps: each (chunk, bin) keeps
+// clamp(cap_b - start, 0, count) instances; the kept total of every chunk
+// (warp sums over its 32 bins, one atomic per warp and chunk) lets the
+// scatter skip chunks that keep nothing at once.  Writes bcap.
 __global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* __restrict__ chunk_hist, int n_chunks,
-                                                          int n_bins, uint32_t* __restrict__ bin_total) {
+                                                          int n_bins, uint32_t* __restrict__ bin_total,
+                                                          uint32_t static_cap, const int32_t* __restrict__ used,
+                                                          uint32_t* __restrict__ bcap,
+                                                          uint32_t* __restrict__ chunk_kept) {
   __shared__ uint32_t wsum[kColWarps][32];
   const int v = blockIdx.y;
   const int w = threadIdx.x >> 5, lane = lane_id();
@@ -177,6 +265,7 @@ __global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* _
   const int per = (n_chunks + kColWarps - 1) / kColWarps;
   const int c0 = min(w * per, n_chunks), c1 = min(c0 + per, n_chunks);
   uint32_t* col = chunk_hist + (size_t)v * n_chunks * n_bins + (ok ? b : 0);
+  const uint32_t cap = ok ? bin_cap_of(static_cap, used, (size_t)v * n_bins + b) : 0u;
   uint32_t s = 0;
   if (ok) {
     int c = c0;
@@ -193,43 +282,49 @@ __global__ void __launch_bounds__(32 * kColWarps) column_scan_kernel(uint32_t* _
     run += k < w ? wsum[k][lane] : 0u;
     tot += wsum[k][lane];
   }
-  if (!ok) return;
+  // per (chunk, group of 32 bins): the kept count, summed by the scatter
+  // (no atomics); nullptr when nothing is capped
+  const int n_grp = gridDim.x;
+  uint32_t* ck = chunk_kept ? chunk_kept + (size_t)v * n_chunks * n_grp + blockIdx.x : nullptr;
   int c = c0;
-  for (; c + 4 <= c1; c += 4) {
-    const uint32_t x0 = col[(size_t)(c + 0) * n_bins], x1 = col[(size_t)(c + 1) * n_bins];
-    const uint32_t x2 = col[(size_t)(c + 2) * n_bins], x3 = col[(size_t)(c + 3) * n_bins];
-    col[(size_t)(c + 0) * n_bins] = run; run += x0;
-    col[(size_t)(c + 1) * n_bins] = run; run += x1;
-    col[(size_t)(c + 2) * n_bins] = run; run += x2;
-    col[(size_t)(c + 3) * n_bins] = run; run += x3;
+  for (; c + 4 <= c1; c += 4) {  // warp-uniform range; four loads in flight
+    uint32_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = ok ? col[(size_t)(c + u) * n_bins] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (ok) col[(size_t)(c + u) * n_bins] = run;
+      const uint32_t kept = run >= cap ? 0u : min(x[u], cap - run);
+      run += x[u];
+      if (ck) {
+        const uint32_t ks = __reduce_add_sync(0xffffffffu, kept);
+        if (lane == 0) ck[(size_t)(c + u) * n_grp] = ks;
+      }
+    }
   }
   for (; c < c1; ++c) {
-    const uint32_t x = col[(size_t)c * n_bins];
-    col[(size_t)c * n_bins] = run;
+    const uint32_t x = ok ? col[(size_t)c * n_bins] : 0u;
+    if (ok) col[(size_t)c * n_bins] = run;
+    const uint32_t kept = run >= cap ? 0u : min(x, cap - run);
     run += x;
+    if (ck) {
+      const uint32_t ks = __reduce_add_sync(0xffffffffu, kept);
+      if (lane == 0) ck[(size_t)c * n_grp] = ks;
+    }
   }
-  if (w == 0) bin_total[(size_t)v * n_bins + b] = tot;
+  if (w == 0 && ok) {
+    bin_total[(size_t)v * n_bins + b] = tot;
+    bcap[(size_t)v * n_bins + b] = cap;
+  }
 }
 
 // per view: exclusive scan over bins of the materialised counts
 // min(total_b, cap) -> bin_start, ranges, totals, overflow; resume = n_vis
 // for complete lists (the scatter writes it for truncated ones)
-// Per-bin cap: the static max_per_bin (0xFFFFFFFF = none), or, with `used`
-// (the previous sss_render_fwd's per-bin consumption), 2 used + 1024 capped
-// by it; used < 0 or >= 2^30 (unknown, or a tile with a pixel still live at
-// the end of its list) keeps the static cap.  `used` is reset to 0 for the
-// forward that follows.
-__device__ __forceinline__ uint32_t bin_cap_of(uint32_t static_cap, int32_t* used, size_t k) {
-  if (!used) return static_cap;
-  const int32_t u = used[k];
-  used[k] = 0;
-  if (u < 0 || u >= (1 << 30)) return static_cap;
-  return min(static_cap, 2u * (uint32_t)u + 1024u);
-}
-
+// (bcap from the column scan; `used` is reset to 0 for the forward that follows)
 __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restrict__ bin_total, int n_bins,
-                                                        int64_t capacity, uint32_t static_cap,
-                                                        int32_t* __restrict__ used, uint32_t* __restrict__ bcap,
+                                                        int64_t capacity, int32_t* __restrict__ used,
+                                                        const uint32_t* __restrict__ bcap,
                                                         uint32_t* __restrict__ bin_start,
                                                         int32_t* __restrict__ ranges,
                                                         int64_t* __restrict__ totals,
@@ -244,9 +339,8 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const uint32_t* __restri
   const int lo = t * per, hi = min(lo + per, n_bins);
   unsigned long long s = 0;
   for (int k = lo; k < hi; ++k) {
-    const uint32_t c = bin_cap_of(static_cap, used, (size_t)v * n_bins + k);
-    bcap[(size_t)v * n_bins + k] = c;
-    s += min(bt[k], c);
+    s += min(bt[k], bcap[(size_t)v * n_bins + k]);
+    if (used) used[(size_t)v * n_bins + k] = 0;
   }
   part[t] = s;
   __syncthreads();
@@ -293,47 +387,40 @@ struct alignas(16) WalkScratch {
 // Truncation state of one scatter CTA (chunk): see the file header.
 struct TruncCtx {
   const uint32_t* cap;                // [n_bins] per-bin caps (UINT32_MAX: none)
-  const uint32_t* openm;              // smem bit per bin: something of the bin is kept in this chunk
+  const uint64_t* openrow;            // smem [bins_y]: bit bx of row by = bin (bx, by) keeps something here
   const uint32_t* ch;                 // the chunk's index of each bin in its full list (global)
   const uint32_t* bs;                 // materialised start of each bin (global)
   const uint32_t* btot;               // full list length of each bin (global)
   int32_t* resume;                    // [n_bins] of this view, or nullptr
 };
 
-// any bin of the rect still open in this chunk (rects of more than 16 bins
-// are assumed open: the per-instance test drops what is full)
-__device__ __forceinline__ bool rect_open(const TruncCtx& tc, const BinGeom& g, int bx0, int by0, int bx1,
-                                          int by1) {
-  if ((bx1 - bx0 + 1) * (by1 - by0 + 1) > 16) return true;
-  for (int by = by0; by <= by1; ++by)
-    for (int bx = bx0; bx <= bx1; ++bx) {
-      const int b = by * g.bins_x + bx;
-      if ((tc.openm[b >> 5] >> (b & 31)) & 1u) return true;
+// Clips a bin rect to the bounding box of its bins still open in this chunk
+// (per bin row, a 64-bit mask of the open bins); false if none is open.  An
+// open bin of the rect stays inside the clipped rect, so the slots of open
+// bins (counts of lower components covering them) are unchanged; instances
+// in full bins are dropped anyway.  Views more than 64 bins wide: no clip.
+__device__ __forceinline__ bool rect_clip_open(const TruncCtx& tc, const BinGeom& g, int& bx0, int& by0, int& bx1,
+                                               int& by1) {
+  if (g.bins_x > 64) return true;
+  const uint64_t xm = (~0ull >> (63 - (bx1 - bx0))) << bx0;
+  uint64_t hit = 0;
+  int y0 = 1 << 20, y1 = -1;
+  for (int by = by0; by <= by1; ++by) {
+    const uint64_t m = tc.openrow[by] & xm;
+    if (m) {
+      y0 = min(y0, by);
+      y1 = by;
+      hit |= m;
     }
-  return false;
+  }
+  if (!hit) return false;
+  by0 = y0;
+  by1 = y1;
+  bx0 = __ffsll((long long)hit) - 1;
+  bx1 = 63 - __clzll((long long)hit);
+  return true;
 }
 
-// Walks the warp's depth-sorted components [wlo, whi), 32 at a time.  The
-// step's components with a non-empty bin rect are compacted to ranks
-// 0..K-1 (order kept) and their K rects flattened into T instances (rank-
-// major, row-major in each rect); the lanes then take 32 consecutive
-// instances at a time, so every lane writes one id per iteration whatever
-// the rect sizes (a lane per component would idle while the warp's largest
-// rect finishes).
-//   Instance t belongs to the rank whose first index excl is the last one
-//   <= t: a bit mask of the rank starts inside the 32-instance window
-//   (one OR-reduction) and a popcount give it.  Its bin comes from the
-//   rank's rect (division by the rect width as a multiply-high with
-//   ceil(2^31 / w): exact for k, w < 2^15; k < SSS_MAX_BINS).
-//   The slot of (rank r, bin b) is wbase[b] + the number of lower ranks
-//   covering b — a popcount of per-column and per-row rank ballots — so
-//   bins receive their entries in depth order without 64-bit keys or
-//   serialised lanes; the highest covering rank then advances wbase[b]
-//   (every lower rank's instance of b lies earlier in the window order).
-//   STAGED: the slots are chunk-local and the ids land in shared memory, from
-//   where the CTA writes every bin's run of the chunk with coalesced stores;
-//   otherwise (keys requested, or a chunk larger than the stage) the id goes
-//   straight to its global slot.
 template <bool STAGED, bool TRUNC>
 __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const short4* __restrict__ rv,
                                           const float* __restrict__ dv, int64_t wlo, int64_t whi,
@@ -344,25 +431,31 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
   const int lane = lane_id();
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  int id_n = 0;
-  short4 r_n = make_short4(1, 1, 0, 0);
-  if (wlo + lane < whi) {
-    id_n = sid[wlo + lane];
-    r_n = rv[id_n];
+  // the warp's (at most kWalkSteps x 32) components: every id, then every
+  // rect, loaded up front (two dependent round trips per warp instead of two
+  // per step: the walk of a chunk that keeps little is latency-bound)
+  constexpr int kWalkSteps = kChunk / kScatterWarps / 32;
+  int idp[kWalkSteps];
+  short4 rp[kWalkSteps];
+#pragma unroll
+  for (int st = 0; st < kWalkSteps; ++st) {
+    const int64_t j = wlo + st * 32 + lane;
+    idp[st] = j < whi ? sid[j] : -1;
   }
-  for (int64_t j0 = wlo; j0 < whi; j0 += 32) {
-    const int id0 = id_n;
-    const short4 r0 = r_n;
+#pragma unroll
+  for (int st = 0; st < kWalkSteps; ++st) rp[st] = idp[st] >= 0 ? rv[idp[st]] : make_short4(1, 1, 0, 0);
+#pragma unroll
+  for (int st = 0; st < kWalkSteps; ++st) {
+    const int64_t j0 = wlo + st * 32;
+    if (j0 >= whi) break;
+    const int id0 = idp[st];
+    const short4 r0 = rp[st];
     const bool valid = j0 + lane < whi;
-    if (j0 + 32 + lane < whi) {  // prefetch the next 32 components
-      id_n = sid[j0 + 32 + lane];
-      r_n = rv[id_n];
-    }
     {
-      const int bx0 = r0.x >> g.shift, by0 = r0.y >> g.shift;
-      const int bx1 = r0.z >> g.shift, by1 = r0.w >> g.shift;
+      int bx0 = r0.x >> g.shift, by0 = r0.y >> g.shift;
+      int bx1 = r0.z >> g.shift, by1 = r0.w >> g.shift;
       bool ne = valid && bx0 <= bx1 && by0 <= by1;
-      if (TRUNC && ne) ne = rect_open(tc, g, bx0, by0, bx1, by1);
+      if (TRUNC && ne) ne = rect_clip_open(tc, g, bx0, by0, bx1, by1);
       const unsigned NE = __ballot_sync(full, ne);
       if (ne) {
         S.stage[__popc(NE & lt)] = make_int4(bx0 | (by0 << 16), bx1 | (by1 << 16), id0,
@@ -476,7 +569,8 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
-    const uint32_t* __restrict__ chunk_hist, const uint8_t* __restrict__ warp_hist,
+    const uint32_t* __restrict__ chunk_hist, const uint64_t* __restrict__ warp_hist,
+    const uint32_t* __restrict__ chunk_kept,
     const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ bin_total,
     const int64_t* __restrict__ totals, int64_t capacity, const uint32_t* __restrict__ bin_cap, int stage_cap,
     int32_t* __restrict__ ids, uint64_t* __restrict__ keys, int32_t* __restrict__ resume) {
@@ -487,6 +581,13 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const int64_t lo = (int64_t)c * kChunk;
   const int64_t nvis = n_vis[v];
   if (lo >= nvis) return;
+  if (chunk_kept) {  // nothing to keep (the column scan's per-group counts)
+    const int n_grp = (g.n_bins + 31) / 32;
+    const uint32_t* ck = chunk_kept + ((size_t)v * n_chunks + c) * n_grp;
+    uint32_t k = 0;
+    for (int q = lane_id(); q < n_grp; q += 32) k += ck[q];
+    if (__syncthreads_or(k != 0) == 0) return;
+  }
   const bool trunc = resume != nullptr;
   const uint32_t* bcv = bin_cap + (size_t)v * g.n_bins;
   const int nb = g.n_bins;
@@ -495,22 +596,21 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   uint32_t* masks = wbase + (size_t)kScatterWarps * nb;                    // [8][bins_x + bins_y] rank masks
   uint32_t* soff = masks + kScatterWarps * (g.bins_x + g.bins_y);          // [n_bins + 1] run starts (stage) / limits
   uint32_t* gst = soff + nb + 1;                                           // [n_bins] run starts (global)
-  uint32_t* openm = gst + nb;                                              // [ceil(n_bins / 32)] open bins
-  int32_t* sids = reinterpret_cast<int32_t*>(openm + ((nb + 31) >> 5));   // [stage_cap] staged ids
+  uint64_t* openrow = reinterpret_cast<uint64_t*>(gst + nb + 1);  // [bins_y] open-bin row masks (8-B aligned: 10 nb + 8 (bx + by) + 2 words in)
+  int32_t* sids = reinterpret_cast<int32_t*>(openrow + g.bins_y);          // [stage_cap] staged ids
   const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
-  const uint8_t* wh = warp_hist + ((size_t)v * n_chunks + c) * kScatterWarps * nb;
+  const uint64_t* wh = warp_hist + ((size_t)v * n_chunks + c) * nb;  // 8 per-warp byte counts per bin
   const uint32_t* bs = bin_start + (size_t)v * nb;
   const int w = threadIdx.x >> 5, lane = lane_id();
-  for (int k = threadIdx.x; k < ((nb + 31) >> 5); k += kScatterThreads) openm[k] = 0u;
+  for (int k = threadIdx.x; k < g.bins_y; k += kScatterThreads) openrow[k] = 0ull;
   // the chunk's kept bin counts (all of them without a cap), scanned over
   // bins: thread t owns bins [b0, b1)
   const int per = (nb + kScatterThreads - 1) / kScatterThreads;
   const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
   uint32_t mine = 0;
   for (int b = b0; b < b1; ++b) {
-    uint32_t cb = 0;
-#pragma unroll
-    for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
+    const uint64_t w8 = wh[b];
+    const uint32_t cb = __dp4a((uint32_t)w8, 0x01010101u, __dp4a((uint32_t)(w8 >> 32), 0x01010101u, 0u));
     const uint32_t cs = ch[b], cap = bcv[b];
     mine += cs >= cap ? 0u : min(cb, cap - cs);
   }
@@ -532,9 +632,8 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const bool staged = keys == nullptr && total <= (uint32_t)stage_cap;  // CTA-uniform
   uint32_t run = wpre + incl - mine;
   for (int b = b0; b < b1; ++b) {
-    uint32_t cb = 0;
-#pragma unroll
-    for (int ww = 0; ww < kScatterWarps; ++ww) cb += wh[(size_t)ww * nb + b];
+    const uint64_t w8 = wh[b];
+    const uint32_t cb = __dp4a((uint32_t)w8, 0x01010101u, __dp4a((uint32_t)(w8 >> 32), 0x01010101u, 0u));
     const uint32_t cs = ch[b], cap = bcv[b];
     const uint32_t kept = cs >= cap ? 0u : min(cb, cap - cs);
     const uint32_t gb = bs[b] + cs;
@@ -546,9 +645,12 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
       wbase[(size_t)ww * nb + b] = acc;
-      acc += wh[(size_t)ww * nb + b];
+      acc += (uint32_t)(w8 >> (8 * ww)) & 255u;
     }
-    if (kept) atomicOr(&openm[b >> 5], 1u << (b & 31));
+    if (kept && g.bins_x <= 64) {
+      const int by = b / g.bins_x;
+      atomicOr(reinterpret_cast<unsigned long long*>(&openrow[by]), 1ull << (b - by * g.bins_x));
+    }
     run += kept;
   }
   if (threadIdx.x == 0) soff[nb] = total;
@@ -563,7 +665,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const float* dv = depth + (int64_t)v * n;
   int32_t* idv = ids + (int64_t)v * capacity;
   uint64_t* kv = keys ? keys + (int64_t)v * capacity : nullptr;
-  const TruncCtx tc{bcv, openm, ch, bs, bin_total + (size_t)v * nb, resume ? resume + (size_t)v * nb : nullptr};
+  const TruncCtx tc{bcv, openrow, ch, bs, bin_total + (size_t)v * nb, resume ? resume + (size_t)v * nb : nullptr};
   uint32_t* wb = wbase + (size_t)w * nb;
   if (!staged) {
     if (trunc) warp_walk<false, true>(sid, rv, dv, wlo, whi, g, wb, colmask, rowmask, scratch[w], idv, kv, soff, tc);
@@ -643,6 +745,7 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   uint32_t* rhist = (uint32_t*)(w + L.radix_hist);
   uint32_t* chist = (uint32_t*)(w + L.chunk_hist);
   uint8_t* whist = (uint8_t*)(w + L.warp_hist);
+  uint32_t* ckept = (uint32_t*)(w + L.chunk_kept);
   uint32_t* btot = (uint32_t*)(w + L.bin_total);
   uint32_t* bstart = (uint32_t*)(w + L.bin_start);
   const short4* rect = (const short4*)pr->rect;
@@ -659,19 +762,34 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
   }
   // out->overflow is sticky: set here on overflow, never cleared (the caller
   // resets it after checking), so a check after many calls sees every one
+  cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
   if (n > 0) {
-    depth_sort(pr->depth, rect, n, n_views, L.tiles_per_view, keys_a, keys_b, vals_a, vals_b, sorted, n_vis,
-               rhist, s);
+    // 16-byte key initialisation when every view's segment is 16-byte aligned
+    const bool vec = n % 4 == 0 && ((reinterpret_cast<uintptr_t>(pr->depth) | reinterpret_cast<uintptr_t>(rect) |
+                                     reinterpret_cast<uintptr_t>(keys_a) | reinterpret_cast<uintptr_t>(vals_a)) &
+                                    15u) == 0;
+    if (vec) {
+      const dim3 gi(div_up(n / 4, 256), n_views);
+      keys_init4_kernel<<<gi, 256, 0, s>>>((const float4*)pr->depth, (const int4*)rect, n, (uint4*)keys_a,
+                                           (int4*)vals_a, n_vis);
+    } else {
+      const dim3 gi(div_up(n, 256), n_views);
+      keys_init_kernel<<<gi, 256, 0, s>>>(pr->depth, rect, n, keys_a, vals_a, n_vis);
+    }
+    count_launch();
+    // culled keys (0xFFFFFFFF) sort last: sorted[:n_vis] are the visible ones
+    radix_sort_pairs(keys_a, vals_a, keys_b, vals_b, n, n_views, L.tiles_per_view, rhist, s, sorted);
     const dim3 gc(L.n_chunks, n_views);
     const size_t hsm = (size_t)kScatterWarps * g.n_bins * 4;
     chunk_hist_kernel<<<gc, kScatterThreads, hsm, s>>>(sorted, n_vis, rect, n, L.chunk, L.n_chunks, g, chist, whist);
-    column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 32 * kColWarps, 0, s>>>(chist, L.n_chunks, g.n_bins, btot);
+    column_scan_kernel<<<dim3(div_up(g.n_bins, 32), n_views), 32 * kColWarps, 0, s>>>(
+        chist, L.n_chunks, g.n_bins, btot, static_cap, out->used, bcap, trunc ? ckept : nullptr);
     count_launch(2);
   } else {
     cudaMemsetAsync(btot, 0, sizeof(uint32_t) * n_views * g.n_bins, s);
-    cudaMemsetAsync(n_vis, 0, sizeof(int32_t) * n_views, s);
+    cudaMemsetAsync(bcap, 0xFF, sizeof(uint32_t) * n_views * g.n_bins, s);
   }
-  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, static_cap, out->used, bcap, bstart,
+  bin_scan_kernel<<<n_views, 1024, 0, s>>>(btot, g.n_bins, out->capacity, out->used, bcap, bstart,
                                             out->ranges, out->totals, out->overflow, n_vis, resume);
   count_launch();
   if (n > 0) {
@@ -680,14 +798,20 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     // shared memory left; larger chunks take the direct path
     const size_t fixed = sizeof(WalkScratch) * kScatterWarps +
                          ((size_t)kScatterWarps * g.n_bins + kScatterWarps * (g.bins_x + g.bins_y) +
-                          2 * (size_t)g.n_bins + 1 + (size_t)((g.n_bins + 31) >> 5)) * 4;
+                          2 * (size_t)g.n_bins + 2 + 2 * (size_t)g.bins_y) * 4;
     int64_t want = (out->capacity + L.n_chunks - 1) / L.n_chunks;
     want = std::min<int64_t>(std::max<int64_t>(want, 256), kScatterStageMax);
+    // truncated lists: most chunks keep little, and the walk is latency-bound,
+    // so a small stage (more CTAs per SM) wins; the few front chunks that keep
+    // more than it take the direct path
+    if (trunc) want = std::min<int64_t>(want, 2048);
     const int64_t room = ((int64_t)kScatterSmemMax - (int64_t)fixed) / 4;
     const int stage_cap = (int)std::max<int64_t>(0, std::min<int64_t>((want + 31) & ~31, room));
     const size_t ssm = fixed + (size_t)stage_cap * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
-        sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, whist, bstart, btot, out->totals,
+        sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, (const uint64_t*)whist, trunc ? ckept : nullptr,
+        bstart, btot,
+        out->totals,
         out->capacity, bcap, stage_cap, out->ids, out->keys, resume);
     count_launch();
   }

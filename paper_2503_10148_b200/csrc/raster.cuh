@@ -23,7 +23,7 @@ constexpr int kLanesPerRow = kWarpW / kPX;
 // resident CTAs per SM the register allocation must allow (occupancy hides
 // the fixed-latency FP32/MUFU dependency chains of the hot loops)
 #ifndef SSS_FWD_MINB
-#define SSS_FWD_MINB 20  // 48 registers: 40 warps per SM (measured: -7% vs 56 registers)
+#define SSS_FWD_MINB 16  // 64 registers, no spills (per-strip staging; 48 spilled inside the entry loop: +6%)
 #endif
 #ifndef SSS_BWD_MINB
 // bwd: <= 93 registers (80 + 8 B of stack): 11 CTAs/SM, -0.6% vs 10 CTAs at

@@ -22,6 +22,10 @@
 // barrier, +5%: each warp then gathers every record itself.)
 #include "raster.cuh"
 
+#ifndef SSS_FWD_STRIP_CULL
+#define SSS_FWD_STRIP_CULL 1
+#endif
+
 namespace sss {
 namespace {
 
@@ -77,10 +81,11 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
-  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
-  __shared__ int32_t spos[kBatch];
-  __shared__ uint8_t smask[kBatch];  // bit w: the entry's ellipse may meet warp w's strip
-  __shared__ int32_t wcnt[kRasterWarps];
+  // per strip (warp) staging: an entry is staged for each strip its ellipse
+  // may reach (conservative box test), so a warp walks only its own entries
+  __shared__ float4 sa[kRasterWarps][kBatch], sb[kRasterWarps][kBatch], sc[kRasterWarps][kBatch];
+  __shared__ int32_t spos[kRasterWarps][kBatch];
+  __shared__ int32_t wcnt[kRasterWarps][kRasterWarps];  // [strip][staging warp]
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
@@ -139,45 +144,63 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       const short4 r = rcv[id];
       ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, ok);
-    if (lane == 0) wcnt[w] = __popc(bal);
-    __syncthreads();
-    int off = 0, nb = 0;
-#pragma unroll
-    for (int k = 0; k < kRasterWarps; ++k) {
-      const int c = wcnt[k];
-      off += k < w ? c : 0;
-      nb += c;
-    }
-    const int slot = off + __popc(bal & lt);
+    // the record, and which strips (warps) its ellipse may reach
+    float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
+    unsigned m = 0;
     if (ok) {
-      spos[slot] = pos;
-      const float4 ra = rv[(int64_t)id * 3 + 0];
-      const float4 rb = rv[(int64_t)id * 3 + 1];
-      sa[slot] = ra;
-      sb[slot] = rb;
-      sc[slot] = rv[(int64_t)id * 3 + 2];
-      // per strip (warp): can the entry's ellipse reach any pixel centre of it?
-      const float X0 = (float)(tx * kTile) + 0.5f, Y0 = (float)(ty * kTile) + 0.5f;
-      unsigned m = 0;
+      ra = rv[(int64_t)id * 3 + 0];
+      rb = rv[(int64_t)id * 3 + 1];
+      rc = rv[(int64_t)id * 3 + 2];
+      if (SSS_FWD_STRIP_CULL) {
+        const float X0 = (float)(tx * kTile) + 0.5f, Y0 = (float)(ty * kTile) + 0.5f;
 #pragma unroll
-      for (int s = 0; s < kRasterWarps; ++s) {
-        const float sy0 = Y0 + (float)(s * kWarpH);
-        m |= ellipse_meets_box(ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, X0, X0 + (float)(kWarpW - 1), sy0,
-                               sy0 + (float)(kWarpH - 1))
-                 ? (1u << s)
-                 : 0u;
+        for (int s = 0; s < kRasterWarps; ++s) {
+          const float sy0 = Y0 + (float)(s * kWarpH);
+          m |= ellipse_meets_box(ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, X0, X0 + (float)(kWarpW - 1), sy0,
+                                 sy0 + (float)(kWarpH - 1))
+                   ? (1u << s)
+                   : 0u;
+        }
+      } else {
+        m = (1u << kRasterWarps) - 1u;
       }
-      smask[slot] = (uint8_t)m;
+    }
+    unsigned bal[kRasterWarps];
+#pragma unroll
+    for (int s = 0; s < kRasterWarps; ++s) {
+      bal[s] = __ballot_sync(0xffffffffu, (m >> s) & 1u);
+      if (lane == 0) wcnt[s][w] = __popc(bal[s]);
+    }
+    __syncthreads();
+    int nb = 0;  // entries of this warp's strip
+#pragma unroll
+    for (int s = 0; s < kRasterWarps; ++s) {
+      int off = 0;
+#pragma unroll
+      for (int k = 0; k < kRasterWarps; ++k) {
+        const int c = wcnt[s][k];
+        off += k < w ? c : 0;
+        if (s == w) nb += c;
+      }
+      if ((m >> s) & 1u) {
+        const int slot = off + __popc(bal[s] & lt);
+        spos[s][slot] = pos;
+        sa[s][slot] = ra;
+        sb[s][slot] = rb;
+        sc[s][slot] = rc;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     const int nb_w = __all_sync(0xffffffffu, all_done()) ? 0 : nb;  // warp already finished
+    const float4* saw = sa[w];
+    const float4* sbw = sb[w];
+    const float4* scw = sc[w];
+    const int32_t* sposw = spos[w];
     for (int j = 0; j < nb_w; ++j) {
-      if (!((smask[j] >> w) & 1u)) continue;  // the ellipse misses this strip (warp-uniform)
       if (lane == 0) SSS_COUNT(1, 1);
-      const float4 a = sa[j];
-      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
+      const float4 a = saw[j];
+      const float4 b = sbw[j];  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
@@ -205,8 +228,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
         if (REC) cm |= 1ull << j;
-        const float4 c = sc[j];  // {e, r, g, b}
-        const int32_t pj1 = spos[j] + 1;
+        const float4 c = scw[j];  // {e, r, g, b}
+        const int32_t pj1 = sposw[j] + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
           for (int k = 0; k < kPairs; ++k) composite2<true>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
@@ -230,7 +253,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       for (int q = 0; q < kBatch / 32; ++q) {
         const unsigned cq = (unsigned)(cm >> (32 * q));
         const int slot = n_rec + __popc(cq & lt);
-        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
+        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = sposw[q * 32 + lane];
         n_rec += __popc(cq);
       }
     }
