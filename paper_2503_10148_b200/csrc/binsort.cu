@@ -72,7 +72,7 @@ inline BinGeom bin_geom(const sss_camera& c, int shift) {
 }
 
 #ifndef SSS_CHUNK
-#define SSS_CHUNK 1024
+#define SSS_CHUNK 2048  // 256 components per warp (per-warp bin counts as u16); the per-bin fixed costs of a chunk CTA amortise over twice the components of 1024
 #endif
 constexpr int kChunk = SSS_CHUNK;  // depth-sorted components per histogram / scatter CTA
 constexpr size_t kScatterSmemMax = 225 * 1024;  // dynamic shared memory of a scatter CTA
@@ -105,7 +105,7 @@ WsLayout ws_layout(int64_t n, int V, const BinGeom& g) {
   L.n_vis = take((size_t)V * 4);
   L.radix_hist = take(radix_ws_words(L.tiles_per_view, V) * 4);
   L.chunk_hist = take((size_t)V * L.n_chunks * (size_t)g.n_bins * 4);
-  L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * (size_t)g.n_bins);
+  L.warp_hist = take((size_t)V * L.n_chunks * kScatterWarps * 2 * (size_t)g.n_bins);  // 8 x u16 per (chunk, bin)
   L.bin_total = take((size_t)V * g.n_bins * 4);
   L.bin_start = take((size_t)V * g.n_bins * 4);
   L.bin_cap = take((size_t)V * g.n_bins * 4);
@@ -184,9 +184,9 @@ __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0
 // Per (chunk, view): bin counts of the chunk's instances, per warp of the
 // scatter's partition (warp w owns kChunk/8 consecutive depth-sorted
 // components).  Writes the chunk totals (u32, for the scans) and the per-warp
-// counts (u8: a warp's 128 components hit a bin at most 128 times; the 8
-// warps' counts of a bin packed in one u64), so the scatter needs no counting
-// pass of its own.
+// counts (u16: a warp's 256 components hit a bin at most 256 times; the 8
+// warps' counts of a bin packed in one 16-byte word), so the scatter needs no
+// counting pass of its own.
 __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
                                                          const int32_t* __restrict__ n_vis,
                                                          const short4* __restrict__ rect, int64_t n,
@@ -212,18 +212,18 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
   }
   __syncthreads();
   uint32_t* out = chunk_hist + ((size_t)v * n_chunks + c) * nb;
-  uint64_t* wout = reinterpret_cast<uint64_t*>(warp_hist) + ((size_t)v * n_chunks + c) * nb;
-  static_assert(kScatterWarps == 8, "8 per-warp byte counts per u64");
+  uint4* wout = reinterpret_cast<uint4*>(warp_hist) + ((size_t)v * n_chunks + c) * nb;
+  static_assert(kScatterWarps == 8, "8 per-warp u16 counts per 16-byte word");
+  static_assert(kChunk / kScatterWarps <= 65535, "per-warp counts fit u16");
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    uint32_t t = 0;
-    uint64_t packed = 0;
+    uint32_t t = 0, pk[4];
 #pragma unroll
-    for (int ww = 0; ww < kScatterWarps; ++ww) {
-      const uint32_t x = hs[(size_t)ww * nb + b];
-      packed |= (uint64_t)x << (8 * ww);
-      t += x;
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = hs[(size_t)(2 * q) * nb + b], hi = hs[(size_t)(2 * q + 1) * nb + b];
+      pk[q] = lo | (hi << 16);
+      t += lo + hi;
     }
-    wout[b] = packed;
+    wout[b] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     out[b] = t;
   }
 }
@@ -431,22 +431,26 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
   const int lane = lane_id();
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  // the warp's (at most kWalkSteps x 32) components: every id, then every
-  // rect, loaded up front (two dependent round trips per warp instead of two
-  // per step: the walk of a chunk that keeps little is latency-bound)
+  // the warp's components in groups of 4 x 32: every id, then every rect,
+  // loaded up front (two dependent round trips per group instead of two per
+  // step: the walk of a chunk that keeps little is latency-bound)
   constexpr int kWalkSteps = kChunk / kScatterWarps / 32;
-  int idp[kWalkSteps];
-  short4 rp[kWalkSteps];
+  constexpr int kGroup = 4;
+  static_assert(kWalkSteps % kGroup == 0, "whole preload groups");
+  for (int g0 = 0; g0 < kWalkSteps; g0 += kGroup) {
+  if (wlo + g0 * 32 >= whi) break;
+  int idp[kGroup];
+  short4 rp[kGroup];
 #pragma unroll
-  for (int st = 0; st < kWalkSteps; ++st) {
-    const int64_t j = wlo + st * 32 + lane;
+  for (int st = 0; st < kGroup; ++st) {
+    const int64_t j = wlo + (g0 + st) * 32 + lane;
     idp[st] = j < whi ? sid[j] : -1;
   }
 #pragma unroll
-  for (int st = 0; st < kWalkSteps; ++st) rp[st] = idp[st] >= 0 ? rv[idp[st]] : make_short4(1, 1, 0, 0);
+  for (int st = 0; st < kGroup; ++st) rp[st] = idp[st] >= 0 ? rv[idp[st]] : make_short4(1, 1, 0, 0);
 #pragma unroll
-  for (int st = 0; st < kWalkSteps; ++st) {
-    const int64_t j0 = wlo + st * 32;
+  for (int st = 0; st < kGroup; ++st) {
+    const int64_t j0 = wlo + (g0 + st) * 32;
     if (j0 >= whi) break;
     const int id0 = idp[st];
     const short4 r0 = rp[st];
@@ -555,6 +559,7 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
       }
     }
   }
+  }
 }
 
 // stable scatter: CTA per (chunk of kChunk depth-sorted components, view);
@@ -569,7 +574,7 @@ __device__ __forceinline__ void warp_walk(const int32_t* __restrict__ sid, const
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     const int32_t* __restrict__ sorted_ids, const int32_t* __restrict__ n_vis,
     const short4* __restrict__ rect, const float* __restrict__ depth, int64_t n, int n_chunks, BinGeom g,
-    const uint32_t* __restrict__ chunk_hist, const uint64_t* __restrict__ warp_hist,
+    const uint32_t* __restrict__ chunk_hist, const uint4* __restrict__ warp_hist,
     const uint32_t* __restrict__ chunk_kept,
     const uint32_t* __restrict__ bin_start, const uint32_t* __restrict__ bin_total,
     const int64_t* __restrict__ totals, int64_t capacity, const uint32_t* __restrict__ bin_cap, int stage_cap,
@@ -599,7 +604,7 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   uint64_t* openrow = reinterpret_cast<uint64_t*>(gst + nb + 1);  // [bins_y] open-bin row masks (8-B aligned: 10 nb + 8 (bx + by) + 2 words in)
   int32_t* sids = reinterpret_cast<int32_t*>(openrow + g.bins_y);          // [stage_cap] staged ids
   const uint32_t* ch = chunk_hist + ((size_t)v * n_chunks + c) * nb;
-  const uint64_t* wh = warp_hist + ((size_t)v * n_chunks + c) * nb;  // 8 per-warp byte counts per bin
+  const uint4* wh = warp_hist + ((size_t)v * n_chunks + c) * nb;  // 8 per-warp u16 counts per bin
   const uint32_t* bs = bin_start + (size_t)v * nb;
   const int w = threadIdx.x >> 5, lane = lane_id();
   for (int k = threadIdx.x; k < g.bins_y; k += kScatterThreads) openrow[k] = 0ull;
@@ -609,8 +614,9 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
   uint32_t mine = 0;
   for (int b = b0; b < b1; ++b) {
-    const uint64_t w8 = wh[b];
-    const uint32_t cb = __dp4a((uint32_t)w8, 0x01010101u, __dp4a((uint32_t)(w8 >> 32), 0x01010101u, 0u));
+    const uint4 w8 = wh[b];
+    const uint32_t cb = __dp2a_lo(w8.x, 0x0101u, __dp2a_lo(w8.y, 0x0101u,
+                          __dp2a_lo(w8.z, 0x0101u, __dp2a_lo(w8.w, 0x0101u, 0u))));  // (u16 lo + u16 hi) per word
     const uint32_t cs = ch[b], cap = bcv[b];
     mine += cs >= cap ? 0u : min(cb, cap - cs);
   }
@@ -632,8 +638,9 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   const bool staged = keys == nullptr && total <= (uint32_t)stage_cap;  // CTA-uniform
   uint32_t run = wpre + incl - mine;
   for (int b = b0; b < b1; ++b) {
-    const uint64_t w8 = wh[b];
-    const uint32_t cb = __dp4a((uint32_t)w8, 0x01010101u, __dp4a((uint32_t)(w8 >> 32), 0x01010101u, 0u));
+    const uint4 w8 = wh[b];
+    const uint32_t cb = __dp2a_lo(w8.x, 0x0101u, __dp2a_lo(w8.y, 0x0101u,
+                          __dp2a_lo(w8.z, 0x0101u, __dp2a_lo(w8.w, 0x0101u, 0u))));  // (u16 lo + u16 hi) per word
     const uint32_t cs = ch[b], cap = bcv[b];
     const uint32_t kept = cs >= cap ? 0u : min(cb, cap - cs);
     const uint32_t gb = bs[b] + cs;
@@ -645,7 +652,8 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
 #pragma unroll
     for (int ww = 0; ww < kScatterWarps; ++ww) {
       wbase[(size_t)ww * nb + b] = acc;
-      acc += (uint32_t)(w8 >> (8 * ww)) & 255u;
+      const uint32_t word = ww < 2 ? w8.x : ww < 4 ? w8.y : ww < 6 ? w8.z : w8.w;
+      acc += (word >> (16 * (ww & 1))) & 0xffffu;
     }
     if (kept && g.bins_x <= 64) {
       const int by = b / g.bins_x;
@@ -804,12 +812,12 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     // truncated lists: most chunks keep little, and the walk is latency-bound,
     // so a small stage (more CTAs per SM) wins; the few front chunks that keep
     // more than it take the direct path
-    if (trunc) want = std::min<int64_t>(want, 2048);
+    if (trunc) want = std::min<int64_t>(want, 4096);
     const int64_t room = ((int64_t)kScatterSmemMax - (int64_t)fixed) / 4;
     const int stage_cap = (int)std::max<int64_t>(0, std::min<int64_t>((want + 31) & ~31, room));
     const size_t ssm = fixed + (size_t)stage_cap * 4;
     scatter_kernel<<<dim3(L.n_chunks, n_views), kScatterThreads, ssm, s>>>(
-        sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, (const uint64_t*)whist, trunc ? ckept : nullptr,
+        sorted, n_vis, rect, pr->depth, n, L.n_chunks, g, chist, (const uint4*)whist, trunc ? ckept : nullptr,
         bstart, btot,
         out->totals,
         out->capacity, bcap, stage_cap, out->ids, out->keys, resume);
