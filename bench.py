@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--views-per-batch", type=int, default=64)
     ap.add_argument("--max-per-bin", type=int, default=0,
                     help="truncated bin lists (sss.h sss_bins.max_per_bin); 0 = complete lists")
+    ap.add_argument("--overlap-blocks", type=int, default=4,
+                    help="N > 1: component blocks of the gradient exchange overlapped with the "
+                         "projection backward (0 = one reduce-scatter after it)")
     ap.add_argument("--bins", default="adaptive", choices=["adaptive", "complete"],
                     help="adaptive: per-bin caps from the previous forward's consumption (sss.h sss_bins.used)")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -361,6 +364,9 @@ def main():
     from paper_2503_10148_b200.step import TrainStep
     from sss_synth import CONFIG_NAMES, make_scene, make_targets, sghmc_params_for
 
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # communicator lines (comm_nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank, world, local = D.init()
     torch.cuda.set_device(local)
     P.load()
@@ -375,7 +381,7 @@ def main():
     hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
     ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
                    views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim, max_per_bin=a.max_per_bin,
-                   adaptive_bins=a.bins == "adaptive")
+                   adaptive_bins=a.bins == "adaptive", overlap_blocks=a.overlap_blocks if world > 1 else 0)
     for _ in range(a.warmup):
         ts.step(targets)
         if ts.overflowed():
@@ -401,6 +407,8 @@ def main():
     D.barrier()
     launches = P.launch_count(reset=True)
     clocks = clk.stop()
+    # bitwise checksum of the parameters over ranks after the timed steps
+    identical = D.replicas_identical(ts.params.planes)
     ms = e0.elapsed_time(e1)
     ms_max = D.allreduce_max(ms, device=torch.device("cuda", local))
     phases = ts.phase_ms()
@@ -541,6 +549,11 @@ def main():
             "clocks": clocks,
             "alu_peaks": ap_meas,
             "bin_overflow": bool(overflow),
+            "replicas_identical": bool(identical),
+            "exchange": {"scheme": ("zero1-blocked-overlap" if ts.shard and ts.blocks else
+                                    "zero1" if ts.shard else "replicated" if world > 1 else "none"),
+                         "blocks": ts.blocks, "world": world,
+                         "backend": (torch.distributed.get_backend() if world > 1 else None)},
             "counts_per_step": {"pairs_first": p_first, "pairs_last": p_last, "instances_first": i_first,
                                 "instances_last": i_last},
         }

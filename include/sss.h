@@ -77,6 +77,15 @@ typedef struct {
 #define SSS_VARIANT_POSITIVE 1 /* o = sigmoid(raw_opacity): "positive t-dis" (settings 1-2) */
 #define SSS_VARIANT_GAUSSIAN 2 /* 3DGS Gaussian kernel exp(-h/2) (nu unused; inv_nu = 0 in the record) */
 #define SSS_VARIANT_LOWPASS 4  /* +0.3 on the diagonal of Sigma2D (setting 1) */
+/* block > 0 (gradients only: sss_render_bwd's grad, sss_project_bwd_range's
+ * grad, sss_sghmc_step's grad): component-blocked layout for the overlapped
+ * multi-GPU exchange.  The set is then one flat buffer at `mean` of
+ * ceil(n / block) blocks of [block_planes][block] floats (block_planes >=
+ * 12 + 3K, the rest padding): plane p of component i is at
+ * mean[(i / block) * block_planes * block + p * block + i % block]; the other
+ * five pointers are ignored.  A block is contiguous, so its exchange can
+ * start as soon as the components of that block are done.  Everywhere else
+ * block must be 0. */
 typedef struct {
   int64_t n;
   int32_t sh_degree;
@@ -87,6 +96,9 @@ typedef struct {
   float* raw_nu;
   float* raw_opacity;
   float* sh;
+  int64_t block;
+  int32_t block_planes;
+  int32_t reserved;
 } sss_params;
 
 /* Per-(view, component) projection (output of sss_project).
@@ -281,6 +293,16 @@ SSS_API sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, 
                           const sss_frame* fwd, const float* d_rgb, const float* target,
                           float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
                           int32_t flags, void* stream);
+
+/* a5 alone, for the components [i0, i1): the projection backward (see
+ * sss_render_bwd) consuming and clearing their screen-space gradient records
+ * in ws (filled by sss_render_bwd with SSS_BWD_RASTER_ONLY) and adding their
+ * parameter gradients to grad (plain or component-blocked layout).  Calls for
+ * disjoint ranges may be issued one after the other so that each block's
+ * gradient exchange overlaps the next block's computation. */
+SSS_API sss_status sss_project_bwd_range(const sss_params* p, const sss_camera* cams, int32_t n_views,
+                                         void* ws, size_t ws_bytes, sss_params* grad, int64_t i0, int64_t i1,
+                                         void* stream);
 
 /* Bytes of device scratch sss_image_loss needs for n_views views of
  * height x width (the three SSIM partial-derivative maps over the valid

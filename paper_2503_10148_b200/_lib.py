@@ -26,7 +26,8 @@ SSS_BWD_PROJECTION_ONLY = 4
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",
            "sss_image_loss_workspace", "sss_image_loss", "sss_relocate_workspace", "sss_relocate",
-           "sss_status_string", "sss_last_error", "sss_launch_count", "sss_alu_peaks"]
+           "sss_status_string", "sss_last_error", "sss_launch_count", "sss_alu_peaks",
+           "sss_project_bwd_range"]
 
 
 class sss_camera(C.Structure):
@@ -38,7 +39,8 @@ class sss_camera(C.Structure):
 class sss_params(C.Structure):
     _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("variant", C.c_int32),
                 ("mean", C.c_void_p), ("log_scale", C.c_void_p), ("rot", C.c_void_p),
-                ("raw_nu", C.c_void_p), ("raw_opacity", C.c_void_p), ("sh", C.c_void_p)]
+                ("raw_nu", C.c_void_p), ("raw_opacity", C.c_void_p), ("sh", C.c_void_p),
+                ("block", C.c_int64), ("block_planes", C.c_int32), ("reserved", C.c_int32)]
 
 
 class sss_projected(C.Structure):
@@ -108,6 +110,8 @@ def load(path: str = LIB_PATH):
         "sss_render_bwd": (st, [P(sss_params), P(sss_projected), P(sss_bins), P(sss_camera),
                                 C.c_int32, P(C.c_float), P(sss_frame), vp, vp, vp,
                                 P(sss_params), vp, C.c_size_t, C.c_int32, vp]),
+        "sss_project_bwd_range": (st, [P(sss_params), P(sss_camera), C.c_int32, vp, C.c_size_t, P(sss_params),
+                                       C.c_int64, C.c_int64, vp]),
         "sss_sghmc_step": (st, [P(sss_params), P(sss_params), P(sss_params), P(sss_params), vp,
                                 P(sss_sghmc_hparams), vp]),
         "sss_image_loss_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
@@ -122,7 +126,12 @@ def load(path: str = LIB_PATH):
         "sss_alu_peaks": (C.c_int, [C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
-        f = getattr(lib, name)
+        try:
+            f = getattr(lib, name)
+        except AttributeError:
+            if "SSS_LIB" in os.environ:  # an older variant build (dev A/B runs) may lack newer entries
+                continue
+            raise
         f.restype = res
         f.argtypes = args
     _lib = lib

@@ -54,7 +54,47 @@ class Params:
         n = self.n
         off = lambda p: C.c_void_p(b + 4 * p * n)  # noqa: E731
         return L.sss_params(n, self.sh_degree, self.variant, off(0), off(3), off(6), off(10), off(11),
-                            off(12))
+                            off(12), 0, 0, 0)
+
+
+class BlockedParams:
+    """A component-blocked parameter-shaped set (gradients of the overlapped
+    multi-GPU exchange, sss.h sss_params.block): one flat [n_blocks][P_pad][B]
+    fp32 tensor; block k holds components [k B, (k + 1) B), plane p at row p.
+    A block is contiguous, so it can be exchanged while later blocks are
+    still being computed."""
+
+    def __init__(self, buf: torch.Tensor, n: int, sh_degree: int, variant: int = 0):
+        assert buf.dtype == torch.float32 and buf.is_contiguous() and buf.dim() == 3
+        assert buf.shape[1] >= n_planes(sh_degree) and buf.shape[0] * buf.shape[2] >= n
+        self.buf = buf
+        self.n = int(n)
+        self.sh_degree = int(sh_degree)
+        self.variant = int(variant)
+
+    @property
+    def block(self) -> int:
+        return int(self.buf.shape[2])
+
+    @classmethod
+    def zeros(cls, n: int, sh_degree: int, n_blocks: int, planes: int, device, variant: int = 0):
+        B = -(-n // n_blocks)
+        return cls(torch.zeros((n_blocks, planes, B), dtype=torch.float32, device=device), n, sh_degree,
+                   variant)
+
+    def block_range(self, k: int):
+        B = self.block
+        return k * B, min(self.n, (k + 1) * B)
+
+    def to_planes(self) -> torch.Tensor:
+        """The plain [P][n] layout (a copy; host-side inspection / tests)."""
+        P = n_planes(self.sh_degree)
+        return self.buf[:, :P, :].permute(1, 0, 2).reshape(P, -1)[:, :self.n].contiguous()
+
+    def c(self) -> L.sss_params:
+        z = C.c_void_p(0)
+        return L.sss_params(self.n, self.sh_degree, self.variant, C.c_void_p(self.buf.data_ptr()), z, z, z, z, z,
+                            self.block, int(self.buf.shape[1]), 0)
 
 
 def camera_c(cam) -> L.sss_camera:
@@ -314,6 +354,18 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
                                _ptr(d_rgb), _ptr(target), _ptr(loss), C.byref(gc), _ptr(ws),
                                ws.numel(), flags, _stream_ptr(stream)), "sss_render_bwd")
     return grad
+
+
+def sss_project_bwd_range(params: Params, cams: Sequence, ws: torch.Tensor, grad, i0: int, i1: int,
+                          stream=None, cams_c=None) -> None:
+    """The projection backward (a5) for components [i0, i1) only (sss.h):
+    consumes the screen-space records a raster-only sss_render_bwd left in
+    ws; grad is a Params or BlockedParams."""
+    lib = L.load()
+    cc = cams_c if cams_c is not None else cameras_c(cams)
+    pc, gc = params.c(), grad.c()
+    L.check(lib.sss_project_bwd_range(C.byref(pc), cc, len(cams), _ptr(ws), ws.numel(), C.byref(gc),
+                                      int(i0), int(i1), _stream_ptr(stream)), "sss_project_bwd_range")
 
 
 def image_loss_workspace_bytes(V: int, H: int, W: int) -> int:

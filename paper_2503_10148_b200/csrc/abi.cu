@@ -29,9 +29,18 @@ sss_status check_launch(const char* what) {
 
 void count_launch(int64_t k) { g_launches += k; }
 
-sss_status validate_params(const sss_params* p, const char* what) {
+sss_status validate_params(const sss_params* p, const char* what, bool allow_block) {
   if (!p) { set_error("%s: null params", what); return SSS_ERR_ARG; }
   if (p->n < 0) { set_error("%s: n < 0", what); return SSS_ERR_ARG; }
+  if (p->block != 0) {
+    if (!allow_block || p->block < 0 || p->block_planes < 12 + 3 * (p->sh_degree + 1) * (p->sh_degree + 1)) {
+      set_error("%s: component-blocked layout not accepted here (or block_planes too small)", what);
+      return SSS_ERR_ARG;
+    }
+    if (p->n > 0 && !p->mean) { set_error("%s: null buffer", what); return SSS_ERR_ARG; }
+    if (p->n > (int64_t)INT32_MAX) { set_error("%s: n too large", what); return SSS_ERR_ARG; }
+    return SSS_OK;
+  }
   if (p->sh_degree < 0 || p->sh_degree > 3) {
     set_error("%s: sh_degree %d outside [0,3]", what, p->sh_degree);
     return SSS_ERR_ARG;

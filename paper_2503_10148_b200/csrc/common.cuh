@@ -37,7 +37,28 @@ void set_error(const char* fmt, ...);
 sss_status check_launch(const char* what);
 void count_launch(int64_t k = 1);
 bool fill_campack(const sss_camera* cams, int first, int count, CamPack& cp);
-sss_status validate_params(const sss_params* p, const char* what);
+sss_status validate_params(const sss_params* p, const char* what, bool allow_block = false);
+
+// The plane pointers and plane stride of component i's storage: plain [P][n]
+// (stride n), or its block of a component-blocked set (sss.h sss_params.block;
+// pointers offset so that plane_ptr[k * stride + i] addresses component i).
+__device__ __forceinline__ sss_params block_view(const sss_params& G, int64_t i, int64_t& stride) {
+  if (G.block <= 0) {
+    stride = G.n;
+    return G;
+  }
+  const int64_t B = G.block, b = i / B;
+  stride = B;
+  float* base = G.mean + b * (int64_t)G.block_planes * B - b * B;
+  sss_params V = G;
+  V.mean = base;
+  V.log_scale = base + 3 * B;
+  V.rot = base + 6 * B;
+  V.raw_nu = base + 10 * B;
+  V.raw_opacity = base + 11 * B;
+  V.sh = base + 12 * B;
+  return V;
+}
 sss_status validate_cams(const sss_camera* cams, int n_views, const char* what);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }

@@ -436,11 +436,11 @@ template <int DEG>
 #endif
 __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_params P, const __grid_constant__ CamPack cp,
                                                            int nv, int v0, float2* __restrict__ g2d,
-                                                           sss_params Gd) {
+                                                           sss_params Gd, int64_t i0, int64_t i1) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int64_t n = P.n;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   float mu[3], s[3], q[4];
   for (int k = 0; k < 3; ++k) mu[k] = P.mean[k * n + i];
   for (int k = 0; k < 3; ++k) s[k] = P.log_scale[k * n + i];
@@ -638,22 +638,24 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
 #pragma unroll
   for (int a = 0; a < 4; ++a) grot[a] = (gq[a] - qh[a] * dotq) / qn;
   const float gnu = g_nu * dnu, gro = g_o * (positive ? o * (1.f - o) : 1.f - o * o);
+  int64_t gn;  // plane stride of the gradient (plain or component-blocked, sss.h)
+  Gd = block_view(Gd, i, gn);
   {
     float cur[12];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cur[a] = Gd.mean[a * n + i];
+    for (int a = 0; a < 3; ++a) cur[a] = Gd.mean[a * gn + i];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cur[3 + a] = Gd.log_scale[a * n + i];
+    for (int a = 0; a < 3; ++a) cur[3 + a] = Gd.log_scale[a * gn + i];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) cur[6 + a] = Gd.rot[a * n + i];
+    for (int a = 0; a < 4; ++a) cur[6 + a] = Gd.rot[a * gn + i];
     cur[10] = Gd.raw_nu[i];
     cur[11] = Gd.raw_opacity[i];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gd.mean[a * n + i] = cur[a] + gmu[a];
+    for (int a = 0; a < 3; ++a) Gd.mean[a * gn + i] = cur[a] + gmu[a];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Gd.log_scale[a * n + i] = cur[3 + a] + gls[a];
+    for (int a = 0; a < 3; ++a) Gd.log_scale[a * gn + i] = cur[3 + a] + gls[a];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) Gd.rot[a * n + i] = cur[6 + a] + grot[a];
+    for (int a = 0; a < 4; ++a) Gd.rot[a * gn + i] = cur[6 + a] + grot[a];
     Gd.raw_nu[i] = cur[10] + gnu;
     Gd.raw_opacity[i] = cur[11] + gro;
   }
@@ -662,10 +664,10 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
     float cur[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (k0 + u < 3 * K) cur[u] = Gd.sh[(k0 + u) * n + i];
+      if (k0 + u < 3 * K) cur[u] = Gd.sh[(k0 + u) * gn + i];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (k0 + u < 3 * K) Gd.sh[(k0 + u) * n + i] = cur[u] + gsh[k0 + u];
+      if (k0 + u < 3 * K) Gd.sh[(k0 + u) * gn + i] = cur[u] + gsh[k0 + u];
   }
 }
 
@@ -675,6 +677,51 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
 using namespace sss;
 
 SSS_COUNTER_ACCESSOR(sss_dev_counters_bwd)
+
+namespace sss {
+// the a5 kernel over components [i0, i1), views in launches of <= 128
+static sss_status project_bwd_launch(const sss_params& p, const sss_camera* cams, int n_views, float* g2d,
+                                     const sss_params& grad, int64_t i0, int64_t i1, cudaStream_t s) {
+  if (i1 <= i0) return SSS_OK;
+  const int threads = 128;
+  const int blocks = div_up(i1 - i0, threads);
+  sss_status st;
+  for (int v0 = 0; v0 < n_views; v0 += kMaxViewsPerLaunch) {
+    const int nv = n_views - v0 < kMaxViewsPerLaunch ? n_views - v0 : kMaxViewsPerLaunch;
+    CamPack cp;
+    fill_campack(cams, v0, nv, cp);
+    switch (p.sh_degree) {
+      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
+      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
+      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
+      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
+    }
+    count_launch();
+    if ((st = check_launch("sss_render_bwd(projection)")) != SSS_OK) return st;
+  }
+  return SSS_OK;
+}
+}  // namespace sss
+
+extern "C" sss_status sss_project_bwd_range(const sss_params* p, const sss_camera* cams, int32_t n_views,
+                                            void* ws, size_t ws_bytes, sss_params* grad, int64_t i0, int64_t i1,
+                                            void* stream) {
+  sss_status st;
+  if ((st = validate_params(p, "sss_project_bwd_range")) != SSS_OK) return st;
+  if ((st = validate_params(grad, "sss_project_bwd_range(grad)", true)) != SSS_OK) return st;
+  if ((st = validate_cams(cams, n_views, "sss_project_bwd_range")) != SSS_OK) return st;
+  if (grad->n != p->n || grad->sh_degree != p->sh_degree) {
+    set_error("sss_project_bwd_range: n / sh_degree mismatch");
+    return SSS_ERR_ARG;
+  }
+  if (i0 < 0 || i1 > p->n || i0 > i1) { set_error("sss_project_bwd_range: bad range"); return SSS_ERR_ARG; }
+  const size_t need = (size_t)p->n * n_views * SSS_G2D_FLOATS * sizeof(float);
+  if (ws_bytes < need || (need > 0 && !ws)) {
+    set_error("sss_project_bwd_range: workspace %zu < %zu bytes", ws_bytes, need);
+    return SSS_ERR_ARG;
+  }
+  return project_bwd_launch(*p, cams, n_views, (float*)ws, *grad, i0, i1, (cudaStream_t)stream);
+}
 
 extern "C" size_t sss_render_bwd_workspace(int64_t n, int32_t n_views) {
   if (n < 0 || n_views <= 0) return 0;
@@ -688,7 +735,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
                                      int32_t flags, void* stream) {
   sss_status st;
   if ((st = validate_params(p, "sss_render_bwd")) != SSS_OK) return st;
-  if ((st = validate_params(grad, "sss_render_bwd(grad)")) != SSS_OK) return st;
+  if ((st = validate_params(grad, "sss_render_bwd(grad)", true)) != SSS_OK) return st;
   if ((st = validate_cams(cams, n_views, "sss_render_bwd")) != SSS_OK) return st;
   if (!pr || !bins || !fwd || !bg) { set_error("sss_render_bwd: null argument"); return SSS_ERR_ARG; }
   if (grad->n != p->n || grad->sh_degree != p->sh_degree || pr->n != p->n) {
@@ -739,20 +786,6 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
 #undef SSS_BWD_LAUNCH_N
 #undef SSS_BWD_LAUNCH
   if (p->n == 0 || (flags & SSS_BWD_RASTER_ONLY)) return SSS_OK;
-  const int threads = 128;
-  const int blocks = div_up(p->n, threads);
-  for (int v0 = 0; v0 < n_views; v0 += kMaxViewsPerLaunch) {
-    const int nv = n_views - v0 < kMaxViewsPerLaunch ? n_views - v0 : kMaxViewsPerLaunch;
-    CamPack cp;
-    fill_campack(cams, v0, nv, cp);
-    switch (p->sh_degree) {
-      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
-      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
-      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
-      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, (float2*)g2d, *grad); break;
-    }
-    count_launch();
-    if ((st = check_launch("sss_render_bwd(projection)")) != SSS_OK) return st;
-  }
+  return project_bwd_launch(*p, cams, n_views, g2d, *grad, 0, p->n, s);
   return SSS_OK;
 }

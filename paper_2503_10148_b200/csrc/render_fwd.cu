@@ -19,12 +19,12 @@
 // rejected: per-warp bounding-box or exact ellipse-strip culling — the warps
 // of a tile then drift apart at the batch barrier — register prefetching of
 // the next batch, and per-warp batches staged by cp.async without the CTA
-// barrier, +5%: each warp then gathers every record itself.)
+// barrier, +5%: each warp then gathers every record itself; round 2: a
+// conservative ellipse-vs-strip box test at staging with per-strip staging
+// arrays, so each warp walks only entries that can reach its strip: +5% at
+// config 5 -- the duplicated staging and the 64 registers it needs cost more
+// than the culled entries save.)
 #include "raster.cuh"
-
-#ifndef SSS_FWD_STRIP_CULL
-#define SSS_FWD_STRIP_CULL 1
-#endif
 
 namespace sss {
 namespace {
@@ -81,11 +81,9 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
-  // per strip (warp) staging: an entry is staged for each strip its ellipse
-  // may reach (conservative box test), so a warp walks only its own entries
-  __shared__ float4 sa[kRasterWarps][kBatch], sb[kRasterWarps][kBatch], sc[kRasterWarps][kBatch];
-  __shared__ int32_t spos[kRasterWarps][kBatch];
-  __shared__ int32_t wcnt[kRasterWarps][kRasterWarps];  // [strip][staging warp]
+  __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
+  __shared__ int32_t spos[kBatch];
+  __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
@@ -139,68 +137,42 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
     const int32_t id = ok ? BL.id(pos) : 0;
-    // the truncated list's tail is the depth-sorted visible set: always rect-filtered
-    if (ok && (FILTER || pos >= BL.mend)) {
-      const short4 r = rcv[id];
-      ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
-    }
-    // the record, and which strips (warps) its ellipse may reach
-    float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
-    unsigned m = 0;
-    if (ok) {
-      ra = rv[(int64_t)id * 3 + 0];
-      rb = rv[(int64_t)id * 3 + 1];
-      rc = rv[(int64_t)id * 3 + 2];
-      if (SSS_FWD_STRIP_CULL) {
-        const float X0 = (float)(tx * kTile) + 0.5f, Y0 = (float)(ty * kTile) + 0.5f;
-#pragma unroll
-        for (int s = 0; s < kRasterWarps; ++s) {
-          const float sy0 = Y0 + (float)(s * kWarpH);
-          m |= ellipse_meets_box(ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, X0, X0 + (float)(kWarpW - 1), sy0,
-                                 sy0 + (float)(kWarpH - 1))
-                   ? (1u << s)
-                   : 0u;
-        }
-      } else {
-        m = (1u << kRasterWarps) - 1u;
+    int slot, nb;
+    // the truncated list's tail is the depth-sorted visible set: always filtered
+    if (FILTER || end > BL.mend) {
+      if (ok && (FILTER || pos >= BL.mend)) {
+        const short4 r = rcv[id];
+        ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
       }
-    }
-    unsigned bal[kRasterWarps];
-#pragma unroll
-    for (int s = 0; s < kRasterWarps; ++s) {
-      bal[s] = __ballot_sync(0xffffffffu, (m >> s) & 1u);
-      if (lane == 0) wcnt[s][w] = __popc(bal[s]);
-    }
-    __syncthreads();
-    int nb = 0;  // entries of this warp's strip
-#pragma unroll
-    for (int s = 0; s < kRasterWarps; ++s) {
-      int off = 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) wcnt[w] = __popc(bal);
+      __syncthreads();
+      int off = 0, tot = 0;
 #pragma unroll
       for (int k = 0; k < kRasterWarps; ++k) {
-        const int c = wcnt[s][k];
+        const int c = wcnt[k];
         off += k < w ? c : 0;
-        if (s == w) nb += c;
+        tot += c;
       }
-      if ((m >> s) & 1u) {
-        const int slot = off + __popc(bal[s] & lt);
-        spos[s][slot] = pos;
-        sa[s][slot] = ra;
-        sb[s][slot] = rb;
-        sc[s][slot] = rc;
-      }
+      slot = off + __popc(bal & lt);
+      nb = tot;
+    } else {
+      slot = threadIdx.x;
+      nb = min(kBatch, end - b0);
+    }
+    if (ok) {
+      spos[slot] = pos;
+      sa[slot] = rv[(int64_t)id * 3 + 0];
+      sb[slot] = rv[(int64_t)id * 3 + 1];
+      sc[slot] = rv[(int64_t)id * 3 + 2];
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     const int nb_w = __all_sync(0xffffffffu, all_done()) ? 0 : nb;  // warp already finished
-    const float4* saw = sa[w];
-    const float4* sbw = sb[w];
-    const float4* scw = sc[w];
-    const int32_t* sposw = spos[w];
     for (int j = 0; j < nb_w; ++j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      const float4 a = saw[j];
-      const float4 b = sbw[j];  // {C, hmax, o, inv_nu}
+      const float4 a = sa[j];
+      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
@@ -228,8 +200,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
         if (REC) cm |= 1ull << j;
-        const float4 c = scw[j];  // {e, r, g, b}
-        const int32_t pj1 = sposw[j] + 1;
+        const float4 c = sc[j];  // {e, r, g, b}
+        const int32_t pj1 = spos[j] + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
           for (int k = 0; k < kPairs; ++k) composite2<true>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
@@ -253,7 +225,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       for (int q = 0; q < kBatch / 32; ++q) {
         const unsigned cq = (unsigned)(cm >> (32 * q));
         const int slot = n_rec + __popc(cq & lt);
-        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = sposw[q * 32 + lane];
+        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
         n_rec += __popc(cq);
       }
     }

@@ -68,7 +68,8 @@ __device__ __forceinline__ void adam_plane(float* theta, const float* grad, floa
 // index in the [P] numbering (the ZeRO plane range).
 template <int U, bool EXPREG = false>
 __device__ __forceinline__ void adam_planes(float* theta, const float* grad, float* m, float* v, int64_t i,
-                                            int64_t n, int k0, int k1, int first, float lr, const HP& hp) {
+                                            int64_t n, int k0, int k1, int first, float lr, const HP& hp,
+                                            int64_t gn) {  // gn: the gradient's plane stride
   float t[U], g[U], mo[U], vo[U];
   bool on[U];
 #pragma unroll
@@ -78,7 +79,7 @@ __device__ __forceinline__ void adam_planes(float* theta, const float* grad, flo
     if (on[u]) {
       const int64_t idx = (int64_t)k * n + i;
       t[u] = theta[idx];
-      g[u] = grad[idx];
+      g[u] = grad[(int64_t)k * gn + i];
       mo[u] = m[idx];
       vo[u] = v[idx];
     }
@@ -104,6 +105,8 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (hp.skip_if && *hp.skip_if) return;  // e.g. the iteration's binning overflowed
+  int64_t gn;  // plane stride of the gradient (plain or component-blocked, sss.h)
+  Gr = block_view(Gr, i, gn);
   const int K = (P.sh_degree + 1) * (P.sh_degree + 1);
   // gate and (burn-in) covariance from the pre-update state
   const bool positive = P.variant & SSS_VARIANT_POSITIVE;
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     if (!onm[a]) continue;
     const int64_t idx = a * n + i;
     pm[a] = P.mean[idx];
-    gm[a] = Gr.mean[idx];
+    gm[a] = Gr.mean[a * gn + i];
     if (need_mv) {
       mo[a] = Mo.mean[idx];
       vo[a] = Vo.mean[idx];
@@ -187,8 +190,8 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     r[idx] = (1.f - eps * Cf) * ra - eps * g + (eta / eps) * xi[a];
   }
   // ---- Adam on the other groups
-  adam_planes<3, true>(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, i, n, 0, 3, 3, hp.lr_group[0], hp);
-  adam_planes<4>(P.rot, Gr.rot, Mo.rot, Vo.rot, i, n, 0, 4, 6, hp.lr_group[1], hp);
+  adam_planes<3, true>(P.log_scale, Gr.log_scale, Mo.log_scale, Vo.log_scale, i, n, 0, 3, 3, hp.lr_group[0], hp, gn);
+  adam_planes<4>(P.rot, Gr.rot, Mo.rot, Vo.rot, i, n, 0, 4, 6, hp.lr_group[1], hp, gn);
   {  // raw nu and raw opacity: both planes' loads before the stores
     const bool on_nu = mine(10), on_o = mine(11);
     float t2[2] = {0.f, 0.f}, g2[2] = {0.f, 0.f}, m2[2] = {0.f, 0.f}, v2[2] = {0.f, 0.f};
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr,
     if (on_o) step(1, reg_o, hp.lr_group[3], P.raw_opacity, Mo.raw_opacity, Vo.raw_opacity);
   }
   for (int k = 0; k < 3 * K; k += kShBatch)
-    adam_planes<kShBatch>(P.sh, Gr.sh, Mo.sh, Vo.sh, i, n, k, min(k + kShBatch, 3 * K), 12, hp.lr_group[4], hp);
+    adam_planes<kShBatch>(P.sh, Gr.sh, Mo.sh, Vo.sh, i, n, k, min(k + kShBatch, 3 * K), 12, hp.lr_group[4], hp, gn);
 }
 
 }  // namespace
@@ -220,7 +223,7 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
                                      void* stream) {
   sss_status st;
   if ((st = validate_params(p, "sss_sghmc_step")) != SSS_OK) return st;
-  if ((st = validate_params(grad, "sss_sghmc_step(grad)")) != SSS_OK) return st;
+  if ((st = validate_params(grad, "sss_sghmc_step(grad)", true)) != SSS_OK) return st;
   if ((st = validate_params(adam_m, "sss_sghmc_step(m)")) != SSS_OK) return st;
   if ((st = validate_params(adam_v, "sss_sghmc_step(v)")) != SSS_OK) return st;
   if (!h || (!momentum && p->n > 0)) { set_error("sss_sghmc_step: null hparams / momentum"); return SSS_ERR_ARG; }

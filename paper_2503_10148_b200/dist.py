@@ -11,8 +11,13 @@ fp32 [P][n] gradient buffer:
     update reads only the replicated pre-update parameters), and the ranks
     all-gather the parameter planes.  Same bytes on the wire as the
     all-reduce; the sampler's HBM work is divided by R.
-Either way replicas stay bit-identical.  torch.distributed is plumbing only
-(process group + NCCL); nothing here computes the method.
+Either way replicas stay bit-identical.  With the overlapped variant the
+gradient is component-blocked (api.BlockedParams): the projection backward
+runs block by block and each block's reduce-scatter is issued on a
+communication stream as soon as its components are done, so the exchange
+overlaps the remaining blocks' computation; the all-gather of the updated
+parameter planes follows the sampler step.  torch.distributed is plumbing
+only (process group + NCCL); nothing here computes the method.
 """
 from __future__ import annotations
 
@@ -85,6 +90,21 @@ def reduce_scatter_planes_(full: torch.Tensor, scratch: torch.Tensor, group=None
         mine.copy_(scratch)
     else:
         dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    return mine
+
+
+def reduce_scatter_block_(block: torch.Tensor, group=None) -> torch.Tensor:
+    """One block [R * Pr][B] of a component-blocked gradient: the sum over
+    ranks of this rank's planes [r Pr, (r + 1) Pr) lands in place (NCCL
+    in-place reduce-scatter: output = input + rank * Pr * B); gloo (CPU
+    tests) all-reduces the block, which leaves the same values there."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pr = block.shape[0] // world
+    mine = block[rank * pr:(rank + 1) * pr]
+    if _nccl(group):
+        dist.reduce_scatter_tensor(mine, block, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(block, op=dist.ReduceOp.SUM, group=group)
     return mine
 
 

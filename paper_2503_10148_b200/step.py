@@ -38,7 +38,7 @@ class TrainStep:
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
                  eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None,
-                 max_per_bin: int = 0, adaptive_bins: bool = False):
+                 max_per_bin: int = 0, adaptive_bins: bool = False, overlap_blocks: int = 0):
         dev = planes.device
         world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
         # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
@@ -61,9 +61,17 @@ class TrainStep:
             self.scratch = torch.empty((pr, planes.shape[1]), dtype=planes.dtype, device=dev)
             self.params = A.Params(pad[:P], sh_degree, variant)
             self.grad = A.Params(self.grad_pad[:P], sh_degree, variant)
+            # overlapped exchange: component-blocked gradient, one reduce-scatter
+            # per block as soon as the projection backward has finished it
+            self.blocks = int(overlap_blocks)
+            if self.blocks > 0:
+                self.grad_blk = A.BlockedParams.zeros(planes.shape[1], sh_degree, self.blocks, pr * world, dev,
+                                                      variant)
+                self.comm = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
         else:
             self.params = A.Params(planes, sh_degree, variant)
             self.grad = A.Params.zeros_like(self.params)
+            self.blocks = 0
         self.m = A.Params(adam_m if adam_m is not None else torch.zeros_like(planes), sh_degree, variant)
         self.v = A.Params(adam_v if adam_v is not None else torch.zeros_like(planes), sh_degree, variant)
         n = self.params.n
@@ -152,10 +160,17 @@ class TrainStep:
         return self.bins[0].view(nv)
 
     # -- the iteration -----------------------------------------------------
-    def forward_backward(self, targets: torch.Tensor) -> None:
+    def forward_backward(self, targets: torch.Tensor, exchange: bool = False) -> None:
         """Render this rank's views and accumulate grad (no optimizer step).
-        targets: [V_local][3][H][W] fp32 device tensor."""
-        self.grad.planes.zero_()
+        targets: [V_local][3][H][W] fp32 device tensor.  exchange (overlapped
+        ZeRO-1 mode): the last view batch's projection backward runs block by
+        block and each block's reduce-scatter is issued on the communication
+        stream right after it (step() waits for them)."""
+        blocked = self.blocks > 0
+        if blocked:
+            self.grad_blk.buf.zero_()
+        else:
+            self.grad.planes.zero_()
         self.loss.zero_()
         self._mark("start")
         for bi, b in enumerate(self.batches):
@@ -181,8 +196,21 @@ class TrainStep:
                                          loss=self.loss, ws=self.ws_loss)
                 self._mark("image_loss")
             kw = dict(bg=self.bg, target=None if d_rgb is not None else tg, d_rgb=d_rgb,
-                      grad=self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
-            if self.prof is None:
+                      grad=self.grad_blk if blocked else self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
+            if blocked and exchange and bi == len(self.batches) - 1:
+                A.sss_render_bwd(self.params, pv, bv, cams, fv, half="raster", **kw)
+                self._mark("render_bwd_raster")
+                comp = torch.cuda.current_stream()
+                for k in range(self.blocks):
+                    i0, i1 = self.grad_blk.block_range(k)
+                    A.sss_project_bwd_range(self.params, cams, self.ws_g2d, self.grad_blk, i0, i1, cams_c=cc)
+                    ev = torch.cuda.Event()
+                    ev.record(comp)
+                    self.comm.wait_event(ev)
+                    with torch.cuda.stream(self.comm):
+                        D.reduce_scatter_block_(self.grad_blk.buf[k], self.group)
+                self._mark("render_bwd_projection")
+            elif self.prof is None:
                 A.sss_render_bwd(self.params, pv, bv, cams, fv, **kw)
             else:  # same two kernels, split so each can be timed
                 A.sss_render_bwd(self.params, pv, bv, cams, fv, half="raster", **kw)
@@ -194,17 +222,27 @@ class TrainStep:
         """One full iteration; returns this rank's device loss sum (see the
         module docstring).  check=True: synchronise on the overflow flag and
         replay the iteration with grown bins until it fits."""
-        self.forward_backward(targets)
+        overlap = self.shard and self.blocks > 0
+        self.forward_backward(targets, exchange=overlap)
         while check and self.overflowed():
             self.grow()
-            self.forward_backward(targets)
+            self.forward_backward(targets, exchange=overlap)
         flag = self.bins[0].overflow
         if self.world > 1:  # any rank's overflow skips every rank's update
             D.allreduce_max_(flag, self.group)
         self.hp.skip_if = flag
         self.hp.step = self.t
         self.hp.grad_scale = 1.0 / self.total_views
-        if self.shard:
+        if overlap:  # the blocks' reduce-scatters were issued during the projection backward
+            torch.cuda.current_stream().wait_stream(self.comm)
+            self._mark("allreduce")
+            self.hp.plane_begin, self.hp.plane_end = self.p0, self.p1
+            if self.p1 > self.p0:
+                A.sss_sghmc_step(self.params, self.grad_blk, self.m, self.v, self.r, self.hp)
+            self._mark("sghmc")
+            D.all_gather_planes_(self.params_pad, self.scratch, self.group)
+            self._mark("allgather")
+        elif self.shard:
             D.reduce_scatter_planes_(self.grad_pad, self.scratch, self.group)
             self._mark("allreduce")
             self.hp.plane_begin, self.hp.plane_end = self.p0, self.p1

@@ -166,3 +166,58 @@ def test_plane_shard_partition():
             spans = [D.plane_shard(P, r, R)[1] for r in range(R)]
             covered = [p for a, b in spans for p in range(a, b)]
             assert covered == list(range(P))
+
+
+def _blocked_worker(rank, world, port, out_q):
+    """Overlapped exchange on gloo: the gradient in the component-blocked
+    layout (api.BlockedParams, sss.h sss_params.block), one reduce-scatter per
+    block issued as each block is finished, this rank's planes of every block
+    then hold the global sum -- the same values as the plain plane-sharded
+    reduce-scatter of the [P][n] buffer; the layout maps back exactly."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    from paper_2503_10148_b200 import api as A
+    from paper_2503_10148_b200 import dist as D
+
+    D.init(backend="gloo")
+    sh, n = 1, 1003  # ragged: the last block is partial
+    P = A.n_planes(sh)
+    pr, (p0, p1) = D.plane_shard(P, rank, world)
+    rng = np.random.default_rng(200 + rank)
+    g_local = rng.normal(size=(P, n))
+    g_all = sum(np.random.default_rng(200 + r).normal(size=(P, n)) for r in range(world))
+    ok = True
+    for n_blocks in (1, 3, 8):
+        blk = A.BlockedParams.zeros(n, sh, n_blocks, pr * world, "cpu")
+        blk.buf = blk.buf.double()
+        B = blk.block
+        for k in range(n_blocks):  # fill block k as the projection backward would, then exchange it
+            i0, i1 = blk.block_range(k)
+            blk.buf[k, :P, :i1 - i0] = torch.from_numpy(g_local[:, i0:i1])
+            D.reduce_scatter_block_(blk.buf[k])
+        got = blk.buf[:, p0:p1, :].permute(1, 0, 2).reshape(p1 - p0, -1)[:, :n].numpy()
+        ok = ok and bool(np.allclose(got, g_all[p0:p1], rtol=1e-14, atol=1e-14))
+        # to_planes() is the inverse of the block layout on the local data
+        fresh = A.BlockedParams.zeros(n, sh, n_blocks, pr * world, "cpu")
+        for k in range(n_blocks):
+            i0, i1 = fresh.block_range(k)
+            fresh.buf[k, :P, :i1 - i0] = torch.from_numpy(g_local[:, i0:i1]).float()
+        ok = ok and bool(np.array_equal(fresh.to_planes().numpy(), g_local.astype(np.float32)))
+        ok = ok and B * n_blocks >= n
+    out_q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_blocked_overlapped_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blocked_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)

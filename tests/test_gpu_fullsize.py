@@ -209,16 +209,19 @@ def test_sharded_step_nccl_single_rank(orc, sss):
         sc = make_custom_scene(3000, 1, 80, 64, n_views=2, seed=37, layout="blobs", nu_hi=16.0)
         tg = torch.from_numpy(make_targets(sc)).cuda()
         out = []
-        for shard in (False, True):
+        for shard, blocks in ((False, 0), (True, 0), (True, 3)):
             hp = _hp32(sghmc_params_for(sc, step=1, seed=3, noise=1e-4))
             ts = TrainStep(torch.from_numpy(sc.params).cuda(), 1, sc.cameras, hp, bin_shift=1,
-                           views_per_batch=2, shard_update=shard)
-            assert ts.shard == shard
+                           views_per_batch=2, shard_update=shard, overlap_blocks=blocks)
+            assert ts.shard == shard and ts.blocks == blocks
             for _ in range(2):
                 ts.step(tg)
             torch.cuda.synchronize()
             out.append(ts.params.planes.cpu().numpy())
         np.testing.assert_allclose(out[1], out[0], rtol=1e-6, atol=1e-7)
+        # the overlapped exchange (component-blocked gradient, per-block
+        # reduce-scatter during the projection backward) gives the same step
+        np.testing.assert_allclose(out[2], out[0], rtol=1e-6, atol=1e-7)
     finally:
         dist.destroy_process_group()
 

@@ -683,3 +683,44 @@ def test_adaptive_bin_caps(orc, sss, scenes):
             assert np.all(used >= 0)
         if name == "cfg2":
             assert (lens < lens0).any()  # round 3 truncated something
+
+
+def test_project_bwd_range_blocked_layout(orc, sss, scenes):
+    """sss_project_bwd_range over component blocks into a component-blocked
+    gradient (sss.h sss_params.block) equals the one-call backward into the
+    plain layout; sss_sghmc_step reads the blocked gradient identically."""
+    import torch
+
+    from gpu_helpers import gpu_forward
+    from paper_2503_10148_b200 import api as A
+    from sss_synth import sghmc_params_for
+
+    sc = scenes["blobs_d2_3v"]
+    V, cam = sc.n_views, sc.cameras[0]
+    params, pr, bins, fr = gpu_forward(sc, bin_shift=1)
+    d = torch.from_numpy(np.random.default_rng(6).normal(size=(V, 3, cam.height, cam.width))
+                         .astype(np.float32)).cuda()
+    ws = torch.zeros(A.render_bwd_workspace_bytes(sc.n, V), dtype=torch.uint8, device="cuda")
+    g_plain = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws)
+    P = A.n_planes(sc.sh_degree)
+    for n_blocks, planes in ((1, P), (4, P + 3), (7, 2 * P)):
+        gb = A.BlockedParams.zeros(sc.n, sc.sh_degree, n_blocks, planes, "cuda")
+        sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, ws=ws, half="raster", grad=gb)
+        for k in range(n_blocks):
+            i0, i1 = gb.block_range(k)
+            A.sss_project_bwd_range(params, sc.cameras, ws, gb, i0, i1)
+        torch.cuda.synchronize()
+        assert int(torch.count_nonzero(ws).item()) == 0  # consumed and cleared
+        assert rel_l2(gb.to_planes().cpu().numpy(), g_plain.planes.cpu().numpy()) <= 1e-5
+        if planes > P:
+            assert float(gb.buf[:, P:, :].abs().max()) == 0.0  # padding planes untouched
+        hp = _hp32(sghmc_params_for(sc, step=2, seed=5, noise=1e-4))
+        outs = []
+        for g in (A.Params(gb.to_planes(), sc.sh_degree), gb):
+            pp = sss.Params(params.planes.clone(), sc.sh_degree)
+            m, v = sss.Params.zeros_like(pp), sss.Params.zeros_like(pp)
+            r = torch.zeros((3, sc.n), device="cuda")
+            sss.sss_sghmc_step(pp, g, m, v, r, hp)
+            outs.append(pp.planes)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1])
