@@ -228,7 +228,21 @@ typedef struct {
    * binning overflowed -- its views rendered as background -- never moves
    * the parameters, moments or momentum; the caller grows and replays). */
   const int32_t* skip_if;
+  /* Device sss_step_state (nullable): if set, the 1-based step is read from
+   * step_state->step on the device (hp->step is ignored) and incremented by
+   * the call, so a CUDA graph that captured the call replays successive
+   * steps (host values are frozen in a captured launch). */
+  struct sss_step_state* step_state;
 } sss_sghmc_hparams;
+
+/* Device-resident step counter of a graph-captured sampler (see above).
+ * Initialise step to the first step (>= 1); the rest is scratch. */
+typedef struct sss_step_state {
+  int64_t step;
+  float inv_b1t, inv_b2t;  /* 1 / (1 - beta^t) of the step being applied */
+  uint32_t ctr2, ctr3;     /* Philox counter words (the step) */
+  int64_t reserved;
+} sss_step_state;
 
 /* flags for sss_render_bwd */
 #define SSS_BWD_NU_GRAD_PAPER 1 /* use the printed dT/dnu of PAPER.md:1301-1314 (R13) */

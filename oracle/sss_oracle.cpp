@@ -288,9 +288,11 @@ void project(const Comp& c, int deg, const orc_cam& cam, Proj& r, int variant = 
   r.depth_f = (float)pz;
   // R24: near-plane cull
   if (!(pz > cam.z_near)) { r.cull = 1; return; }
-  // Jacobian of the pinhole map at p (EWA affine approximation; Eq. 4, R4)
-  r.J[0] = cam.fx / pz; r.J[1] = 0.0; r.J[2] = -(cam.fx * px) / (pz * pz);
-  r.J[3] = 0.0; r.J[4] = cam.fy / pz; r.J[5] = -(cam.fy * py) / (pz * pz);
+  // Jacobian of the pinhole map at p (EWA affine approximation; Eq. 4, R4),
+  // through the one reciprocal iz = 1/pz (canonical order)
+  const double iz = 1.0 / pz;
+  r.J[0] = cam.fx * iz; r.J[1] = 0.0; r.J[2] = -(cam.fx * px) * (iz * iz);
+  r.J[3] = 0.0; r.J[4] = cam.fy * iz; r.J[5] = -(cam.fy * py) * (iz * iz);
   // Sigma_c = W Sigma W^T
   double T1[9];
   for (int i = 0; i < 3; ++i)
@@ -315,11 +317,12 @@ void project(const Comp& c, int deg, const orc_cam& cam, Proj& r, int variant = 
     r.cov[2] = r.cov[2] + kLowpass;
   }
   r.det = r.cov[0] * r.cov[2] - r.cov[1] * r.cov[1];
-  r.conic[0] = r.cov[2] / r.det;
-  r.conic[1] = -r.cov[1] / r.det;
-  r.conic[2] = r.cov[0] / r.det;
-  r.mean2d[0] = (cam.fx * px) / pz + cam.cx;
-  r.mean2d[1] = (cam.fy * py) / pz + cam.cy;
+  const double idet = 1.0 / r.det;  // conic = (Sigma2D)^-1 through one reciprocal
+  r.conic[0] = r.cov[2] * idet;
+  r.conic[1] = -r.cov[1] * idet;
+  r.conic[2] = r.cov[0] * idet;
+  r.mean2d[0] = (cam.fx * px) * iz + cam.cx;
+  r.mean2d[1] = (cam.fy * py) * iz + cam.cy;
   // L9 cutoff: pair included iff |o| T >= 1/255  <=>  h <= hmax  (R9)
   r.hmax = r.nu * std::expm1((2.0 / (r.nu + 2.0)) * std::log(255.0 * std::fabs(r.o)));
   if (variant & kVarGaussian) r.hmax = 2.0 * std::log(255.0 * std::fabs(r.o));  // |o| e^{-h/2} = 1/255

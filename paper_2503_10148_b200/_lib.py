@@ -71,7 +71,7 @@ class sss_sghmc_hparams(C.Structure):
                 ("grad_scale", C.c_float), ("step", C.c_int64), ("seed", C.c_uint64),
                 ("eps_o", C.c_float), ("eps_sigma", C.c_float), ("mu_mode", C.c_int32),
                 ("plane_begin", C.c_int32), ("plane_end", C.c_int32), ("reserved", C.c_int32),
-                ("skip_if", C.c_void_p)]
+                ("skip_if", C.c_void_p), ("step_state", C.c_void_p)]
 
 
 class sss_relocate_params(C.Structure):

@@ -244,7 +244,7 @@ def hparams_c(hp) -> L.sss_sghmc_hparams:
                                float(getattr(hp, "eps_o", 0.0)), float(getattr(hp, "eps_sigma", 0.0)),
                                int(getattr(hp, "mu_mode", 0)), int(getattr(hp, "plane_begin", 0)),
                                int(getattr(hp, "plane_end", 0)), 0,
-                               _ptr(getattr(hp, "skip_if", None)))
+                               _ptr(getattr(hp, "skip_if", None)), _ptr(getattr(hp, "step_state", None)))
 
 
 # ------------------------------------------------------------- entry points
@@ -428,6 +428,14 @@ def grow(planes: torch.Tensor, sh_degree: int, frac: float = 0.05) -> torch.Tens
     extra = torch.zeros((P, add), dtype=planes.dtype, device=planes.device)
     extra[6] = 1.0  # quaternion w
     return torch.cat([planes, extra], dim=1).contiguous()
+
+
+def step_state(first_step: int, device="cuda") -> torch.Tensor:
+    """A device sss_step_state (sss.h) starting at `first_step`: set it as
+    hp.step_state to make sss_sghmc_step graph-capturable."""
+    t = torch.zeros(4, dtype=torch.int64, device=device)  # 32 bytes
+    t[0] = int(first_step)
+    return t
 
 
 def sss_sghmc_step(params: Params, grad: Params, adam_m: Params, adam_v: Params,

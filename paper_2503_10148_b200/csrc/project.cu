@@ -175,9 +175,12 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
     if (vis) {
       const double px = p[0], py = p[1], pz = p[2];
       const double fx = cam.fx, fy = cam.fy;
+      // one fp64 reciprocal per view instead of six divisions (canonical
+      // order of DESIGN.md §2, mirrored by the oracle)
+      const double iz = 1.0 / pz;
       double J[6];
-      J[0] = fx / pz; J[1] = 0.0; J[2] = -(fx * px) / (pz * pz);
-      J[3] = 0.0; J[4] = fy / pz; J[5] = -(fy * py) / (pz * pz);
+      J[0] = fx * iz; J[1] = 0.0; J[2] = -(fx * px) * (iz * iz);
+      J[3] = 0.0; J[4] = fy * iz; J[5] = -(fy * py) * (iz * iz);
       double T1[9], Sc[9];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
@@ -187,21 +190,27 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
         for (int b = 0; b < 3; ++b)
           Sc[a * 3 + b] = (T1[a * 3 + 0] * cam.R[b * 3 + 0] + T1[a * 3 + 1] * cam.R[b * 3 + 1]) +
                           T1[a * 3 + 2] * cam.R[b * 3 + 2];
+      // K = J Sc and Sigma2D = K J^T in the canonical left-to-right order with
+      // the structural zeros of J (J01 = J10 = 0) dropped: a (finite) zero
+      // product added to a sum leaves it unchanged, so the values equal the
+      // full sums the oracle evaluates
       double K2[6];
-      for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 3; ++b)
-          K2[a * 3 + b] = (J[a * 3 + 0] * Sc[0 * 3 + b] + J[a * 3 + 1] * Sc[1 * 3 + b]) + J[a * 3 + 2] * Sc[2 * 3 + b];
-      double cxx = (K2[0] * J[0] + K2[1] * J[1]) + K2[2] * J[2];
-      const double cxy = (K2[0] * J[3] + K2[1] * J[4]) + K2[2] * J[5];
-      double cyy = (K2[3] * J[3] + K2[4] * J[4]) + K2[5] * J[5];
+      for (int b = 0; b < 3; ++b) {
+        K2[0 * 3 + b] = J[0] * Sc[0 * 3 + b] + J[2] * Sc[2 * 3 + b];
+        K2[1 * 3 + b] = J[4] * Sc[1 * 3 + b] + J[5] * Sc[2 * 3 + b];
+      }
+      double cxx = K2[0] * J[0] + K2[2] * J[2];
+      const double cxy = K2[1] * J[4] + K2[2] * J[5];
+      double cyy = K2[4] * J[4] + K2[5] * J[5];
       if (lowpass) {
         cxx = cxx + 0.3;
         cyy = cyy + 0.3;
       }
       const double det = cxx * cyy - cxy * cxy;
-      const double A = cyy / det, B = -cxy / det, C = cxx / det;
-      const double mx = (fx * px) / pz + cam.cx;
-      const double my = (fy * py) / pz + cam.cy;
+      const double idet = 1.0 / det;
+      const double A = cyy * idet, B = -cxy * idet, C = cxx * idet;
+      const double mx = (fx * px) * iz + cam.cx;
+      const double my = (fy * py) * iz + cam.cy;
       const float mx_f = (float)mx, my_f = (float)my;
       const float A_f = (float)A, B2_f = (float)(2.0 * B), C_f = (float)C;
       vis = ((float)det > 0.0f) && isfinite(mx_f) && isfinite(my_f) && isfinite(A_f) &&

@@ -45,7 +45,19 @@ struct HP {
   uint32_t ctr2, ctr3;     // step (lo, hi)
   uint32_t key0, key1;     // seed (lo, hi)
   const int32_t* skip_if;  // device flag: nonzero = write nothing
+  const sss_step_state* st;  // device step state (graph capture): overrides inv_b*t and ctr*
 };
+
+// Graph-capturable step: the step's constants from the device counter, with
+// the host formula (fp64 pow, rounded once), then the counter advances.
+__global__ void step_prep_kernel(sss_step_state* st, float beta1, float beta2) {
+  const int64_t t = st->step;
+  st->inv_b1t = (float)(1.0 / (1.0 - pow((double)beta1, (double)t)));
+  st->inv_b2t = (float)(1.0 / (1.0 - pow((double)beta2, (double)t)));
+  st->ctr2 = (uint32_t)t;
+  st->ctr3 = (uint32_t)((uint64_t)t >> 32);
+  st->step = t + 1;
+}
 
 __device__ __forceinline__ float adam_dir(float g, float* m, float* v, int64_t idx, const HP& hp) {
   const float mm = hp.beta1 * m[idx] + (1.f - hp.beta1) * g;
@@ -99,14 +111,21 @@ __device__ __forceinline__ void adam_planes(float* theta, const float* grad, flo
   }
 }
 
+template <bool BLOCKED>  // gradient in the component-blocked layout (sss.h sss_params.block)
 __global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr, sss_params Mo,
                                                     sss_params Vo, float* __restrict__ r, HP hp) {
   const int64_t n = P.n;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (hp.skip_if && *hp.skip_if) return;  // e.g. the iteration's binning overflowed
-  int64_t gn;  // plane stride of the gradient (plain or component-blocked, sss.h)
-  Gr = block_view(Gr, i, gn);
+  if (hp.st) {  // graph-captured step: this step's constants from the device
+    hp.inv_b1t = hp.st->inv_b1t;
+    hp.inv_b2t = hp.st->inv_b2t;
+    hp.ctr2 = hp.st->ctr2;
+    hp.ctr3 = hp.st->ctr3;
+  }
+  int64_t gn = n;  // plane stride of the gradient (plain or component-blocked, sss.h)
+  if (BLOCKED) Gr = block_view(Gr, i, gn);
   const int K = (P.sh_degree + 1) * (P.sh_degree + 1);
   // gate and (burn-in) covariance from the pre-update state
   const bool positive = P.variant & SSS_VARIANT_POSITIVE;
@@ -232,7 +251,7 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
     set_error("sss_sghmc_step: n / sh_degree mismatch");
     return SSS_ERR_ARG;
   }
-  if (h->step < 1 || !(h->lr > 0.f)) { set_error("sss_sghmc_step: step must be >= 1 and lr > 0"); return SSS_ERR_ARG; }
+  if ((!h->step_state && h->step < 1) || !(h->lr > 0.f)) { set_error("sss_sghmc_step: step must be >= 1 and lr > 0"); return SSS_ERR_ARG; }
   if (p->n == 0) return SSS_OK;
   HP hp;
   hp.lr = h->lr; hp.friction = h->friction; hp.noise = h->noise; hp.gate_k = h->gate_k; hp.gate_t = h->gate_t;
@@ -254,7 +273,15 @@ extern "C" sss_status sss_sghmc_step(sss_params* p, const sss_params* grad, sss_
   hp.ctr2 = (uint32_t)h->step; hp.ctr3 = (uint32_t)((uint64_t)h->step >> 32);
   hp.key0 = (uint32_t)h->seed; hp.key1 = (uint32_t)(h->seed >> 32);
   cudaStream_t s = (cudaStream_t)stream;
-  sghmc_kernel<<<div_up(p->n, 256), 256, 0, s>>>(*p, *grad, *adam_m, *adam_v, momentum, hp);
+  hp.st = h->step_state;
+  if (h->step_state) {
+    step_prep_kernel<<<1, 1, 0, s>>>(h->step_state, h->beta1, h->beta2);
+    count_launch();
+  }
+  if (grad->block > 0)
+    sghmc_kernel<true><<<div_up(p->n, 256), 256, 0, s>>>(*p, *grad, *adam_m, *adam_v, momentum, hp);
+  else
+    sghmc_kernel<false><<<div_up(p->n, 256), 256, 0, s>>>(*p, *grad, *adam_m, *adam_v, momentum, hp);
   count_launch();
   return check_launch("sss_sghmc_step");
 }

@@ -260,6 +260,36 @@ class TrainStep:
         self.t += 1
         return self.loss
 
+    # -- CUDA graph of one iteration (launch-bound small scenes, config 2) ---
+    def capture(self, targets: torch.Tensor) -> None:
+        """Capture one whole iteration (every view batch, the sampler step) in
+        a CUDA graph; replay() then runs an iteration with one launch.  The
+        step counter moves to the device (sss_step_state), the targets to a
+        static buffer.  One process (the NCCL exchange is not captured)."""
+        assert self.world == 1 and self.prof is None and self.stats is None
+        dev = self.params.planes.device
+        self.hp.step_state = A.step_state(self.t, dev)
+        self.g_targets = targets.clone()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up iteration (a real one) on the capture stream
+            self.step(self.g_targets)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.step(self.g_targets)
+        self.t -= 1  # the capture launched nothing
+
+    def replay(self, targets: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """One captured iteration; `targets` (if given and not the static
+        buffer) is copied into the static buffer first."""
+        if targets is not None and targets.data_ptr() != self.g_targets.data_ptr():
+            self.g_targets.copy_(targets, non_blocking=True)
+        self.graph.replay()
+        self.t += 1
+        return self.loss
+
     def phase_ms(self) -> dict:
         """Per-phase milliseconds of the recorded events (after a sync)."""
         out = {}

@@ -724,3 +724,66 @@ def test_project_bwd_range_blocked_layout(orc, sss, scenes):
             outs.append(pp.planes)
         torch.cuda.synchronize()
         assert torch.equal(outs[0], outs[1])
+
+
+def test_sghmc_device_step_state(sss):
+    """sss_sghmc_hparams.step_state (graph capture): the step read from the
+    device counter gives the host-step update bit for bit, and advances."""
+    import torch
+
+    from paper_2503_10148_b200 import api as A
+    from sss_synth import sghmc_params_for
+
+    sc = make_custom_scene(10000, 1, 32, 32, seed=13)
+    r, m, v = make_optimizer_state(sc, seed=2)
+    grad = (np.random.default_rng(3).normal(size=sc.params.shape) * 1e-2).astype(np.float32)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    outs = []
+    for use_state in (False, True):
+        hp = _hp32(sghmc_params_for(sc, step=7, seed=21, noise=1e-4))
+        st = None
+        if use_state:
+            st = A.step_state(6)
+            hp.step_state = st
+            hp.step = 999  # ignored
+        ps, ms, vs, rs = sss.Params(dev(sc.params), 1), sss.Params(dev(m), 1), sss.Params(dev(v), 1), dev(r)
+        g = sss.Params(dev(grad), 1)
+        if use_state:  # step 6 then step 7 from the device counter
+            sss.sss_sghmc_step(ps, g, ms, vs, rs, hp)
+            ps, ms, vs, rs = sss.Params(dev(sc.params), 1), sss.Params(dev(m), 1), sss.Params(dev(v), 1), dev(r)
+        sss.sss_sghmc_step(ps, g, ms, vs, rs, hp)
+        torch.cuda.synchronize()
+        outs.append((ps.planes.cpu(), ms.planes.cpu(), vs.planes.cpu(), rs.cpu()))
+        if use_state:
+            assert int(st[0].item()) == 8
+    for a_, b_ in zip(*outs):
+        assert torch.equal(a_, b_)
+
+
+def test_trainstep_cuda_graph_replay(sss):
+    """TrainStep.capture/replay: one whole iteration as a CUDA graph gives the
+    eager iterations' parameters (up to the order of the backward's float
+    atomics, which differs run to run)."""
+    import torch
+
+    from paper_2503_10148_b200.step import TrainStep
+    from sss_synth import make_targets, sghmc_params_for
+
+    sc = make_custom_scene(5000, 3, 96, 64, n_views=2, seed=19, layout="blobs", nu_hi=16.0)
+    tg = torch.from_numpy(make_targets(sc)).cuda()
+    outs = []
+    for graph in (False, True):
+        hp = _hp32(sghmc_params_for(sc, step=1, seed=4, noise=1e-4))
+        ts = TrainStep(torch.from_numpy(sc.params).cuda(), 3, sc.cameras, hp, bin_shift=2,
+                       views_per_batch=2, adaptive_bins=True)
+        if graph:
+            ts.capture(tg)  # one eager (warm-up) iteration inside
+            for _ in range(3):
+                ts.replay(tg)
+        else:
+            for _ in range(4):
+                ts.step(tg)
+        torch.cuda.synchronize()
+        assert not ts.overflowed() and ts.t == 5
+        outs.append(ts.params.planes.cpu().numpy())
+    np.testing.assert_allclose(outs[1], outs[0], rtol=1e-5, atol=1e-6)
