@@ -90,7 +90,7 @@ class SGHMCParams:
     gate_k: float = 100.0
     gate_t: float = 0.005
     burn_in: bool = False
-    g_adam: bool = False
+    g_adam: bool = True  # R17: "we employ the Adam gradient in SGHMC"
     lr_scale: float = 1e-3
     lr_rot: float = 1e-3
     lr_nu: float = 1e-3

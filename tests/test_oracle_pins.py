@@ -605,9 +605,12 @@ def test_sh_orthonormal(orc):
 
 # ------------------------------------------------------------------- SGHMC
 def _hp(**kw):
+    """Literal Eq. 10 (g = dL/dmu) unless g_adam is passed: these pins check
+    the equation's algebra; the Adam-direction default (R17) has its own pin."""
     from sss_synth import SGHMCParams
 
     p = SGHMCParams()
+    p.g_adam = False
     for k, v in kw.items():
         setattr(p, k, v)
     return p
@@ -670,6 +673,25 @@ def test_sghmc_degenerate_updates(orc):
     hp = _hp(noise=0.0, gate_t=1e9, burn_in=True)
     pl3, *_ = orc.sghmc_step(pl, 0, np.zeros_like(pl), m, v, r, hp)
     np.testing.assert_array_equal(pl3[0:3], pl[0:3])
+
+
+def test_sghmc_adam_direction_closed_form(orc):
+    """R17 (PAPER.md:1083 "we employ the Adam gradient in SGHMC"): g in Eq. 10
+    is Adam's direction m^/(sqrt(v^) + eps); on the first step from zero
+    moments that is g/|g| (up to eps) = sign(g), so with gate 0 and no noise
+    mu' = mu - eps^2 sign(g) and r' = (1 - eps C) r - eps sign(g)."""
+    rng = np.random.default_rng(7)
+    pl, m, v, r = _state(60, o=0.99)
+    g = rng.normal(size=pl.shape)
+    r[:] = rng.normal(size=r.shape)
+    hp = _hp(noise=0.0, g_adam=True, grad_scale=0.5)
+    pl2, m2, v2, r2 = orc.sghmc_step(pl, 0, g, m, v, r, hp)
+    eps, Cf = hp.lr, hp.friction
+    np.testing.assert_allclose(pl2[0:3], pl[0:3] - eps * eps * np.sign(g[0:3]), rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose(r2, (1 - eps * Cf) * r - eps * np.sign(g[0:3]), rtol=1e-9)
+    np.testing.assert_allclose(m2[0:3], 0.1 * 0.5 * g[0:3], rtol=1e-12)  # the mean moments move
+    from sss_synth import SGHMCParams
+    assert SGHMCParams().g_adam  # the default reading (R17)
 
 
 def test_adam_closed_forms(orc):

@@ -118,9 +118,11 @@ def test_variant_backward_matches_finite_differences(orc, variant):
 
 
 def _hp(**kw):
+    """Literal Eq. 10 (g = dL/dmu) unless g_adam is passed (R17)."""
     from sss_synth import SGHMCParams
 
     p = SGHMCParams()
+    p.g_adam = False
     for k, v in kw.items():
         setattr(p, k, v)
     return p
