@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--bin-shift", type=int, default=2)
+    ap.add_argument("--bin-shift", type=int, default=None,
+                    help="default per config (measured best): 0 for configs 1-2, 1 for 4, 2 for 3 and 5")
     ap.add_argument("--views-per-batch", type=int, default=64)
     ap.add_argument("--max-per-bin", type=int, default=0,
                     help="truncated bin lists (sss.h sss_bins.max_per_bin); 0 = complete lists")
@@ -63,7 +64,10 @@ def parse():
     ap.add_argument("--eps-dssim", type=float, default=0.0)
     ap.add_argument("--eps-o", type=float, default=0.0)
     ap.add_argument("--eps-sigma", type=float, default=0.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.bin_shift is None:
+        a.bin_shift = {1: 0, 2: 0, 3: 2, 4: 1, 5: 2}.get(a.config, 2)
+    return a
 
 
 def peaks():
