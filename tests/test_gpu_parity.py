@@ -523,8 +523,9 @@ def test_backward_tile_list_paths_agree(orc, sss, scenes):
                     seq = tl[v, t, s, :tc[v, t, s]]
                     assert np.all(np.diff(seq) > 0)
                     # the strip's last listed entry is its pixels' last composited one
-                    y0, x0 = (t // tiles_x) * 16 + 8 * s, (t % tiles_x) * 16
-                    assert seq[-1] + 1 == last[v, y0:y0 + 8, x0:x0 + 16].max()
+                    sh = 16 // sss._lib.SSS_TILE_LISTS  # rows per list
+                    y0, x0 = (t // tiles_x) * 16 + sh * s, (t % tiles_x) * 16
+                    assert seq[-1] + 1 == last[v, y0:y0 + sh, x0:x0 + 16].max()
         if cap == 4:
             assert (fr.tile_count.cpu().numpy() > 4).any()  # the fallback is exercised
     assert rel_l2(grads[0], grads[2]) <= 1e-5
