@@ -33,3 +33,12 @@ def ulp_diff(a, b):
     a = np.ascontiguousarray(a, np.float32).view(np.int32).astype(np.int64)
     b = np.ascontiguousarray(b, np.float32).view(np.int32).astype(np.int64)
     return np.abs(a - b)
+
+
+def update_ulp(p_ref, p_old):
+    """One fp32 ulp of the coarser of the old and new parameter binades: the
+    kernels form mu' from mu in two fp32 roundings (each <= 1/2 ulp of its
+    larger operand), so an update that crosses a power of two can be off by
+    half an ulp of the old binade plus half of the new one."""
+    big = np.maximum(np.abs(p_ref), np.abs(p_old)).astype(np.float32)
+    return np.spacing(big).astype(np.float64)

@@ -99,7 +99,9 @@ def test_sghmc_regularizers_parity(orc, sss):
     torch.cuda.synchronize()
     p_ref, m_ref, v_ref, _ = orc.sghmc_step(sc.params, 3, grad, m, v, r, hp)
     got = params.planes.cpu().numpy().astype(np.float64)
-    ulp = np.spacing(np.abs(p_ref).astype(np.float32)).astype(np.float64)
+    from gpu_helpers import update_ulp
+
+    ulp = update_ulp(p_ref, sc.params)
     bound = ulp + 1e-5 * np.abs(p_ref - sc.params)
     assert np.all(np.abs(got - p_ref) <= bound + 1e-30)
     assert rel_l2(mm.planes.cpu().numpy(), m_ref) <= 1e-5

@@ -328,9 +328,11 @@ def test_sghmc_parity(orc, sss, variant):
     got = params.planes.cpu().numpy().astype(np.float64)
     dref = p_ref - sc.params
     # fp32 state: the update can only be as exact as one ulp of the result
-    # (|d mu| ~ 1e-4 << |mu| ~ 1), so the bound per element is one fp32 ulp of
-    # the reference result plus 1e-5 of the reference update.
-    ulp = np.spacing(np.abs(p_ref).astype(np.float32)).astype(np.float64)
+    # (|d mu| ~ 1e-4 << |mu| ~ 1), so the bound per element is one fp32 ulp
+    # (of the coarser binade of mu and mu') plus 1e-5 of the reference update.
+    from gpu_helpers import update_ulp
+
+    ulp = update_ulp(p_ref, sc.params)
     bound = ulp + 1e-5 * np.abs(dref)
     assert np.all(np.abs(got - p_ref) <= bound + 1e-30), float((np.abs(got - p_ref) / bound).max())
     # and most elements are the correctly rounded fp64 result: a systematic
@@ -788,3 +790,114 @@ def test_trainstep_cuda_graph_replay(sss):
         assert not ts.overflowed() and ts.t == 5
         outs.append(ts.params.planes.cpu().numpy())
     np.testing.assert_allclose(outs[1], outs[0], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("shift", [1, 2])
+def test_tile_masks(orc, sss, scenes, shift):
+    """sss_bins.tmask: every bit a mask sets or clears is conservative -- the
+    forward and backward over masked bins give the unmasked result (image,
+    transmittance, counts bit for bit; gradients 1e-5) and the oracle's; every
+    pair the oracle composites has its tile's bit set; the masks drop a
+    large share of the rect's false positives; with adaptive truncation too."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    for name in ("blobs_d2_3v", "stress_d1", "cfg2"):
+        sc = scenes[name]
+        V, cam = sc.n_views, sc.cameras[0]
+        params = to_dev(sc)
+        pr = sss.sss_project(params, sc.cameras)
+        plain = sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift)
+        masked = sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift, tile_masks=True)
+        torch.cuda.synchronize()
+        assert torch.equal(plain.totals, masked.totals) and torch.equal(plain.ranges, masked.ranges)
+        for v in range(V):
+            M = int(plain.totals[v].item())
+            assert torch.equal(plain.ids[v, :M], masked.ids[v, :M])
+        frames = []
+        for b in (plain, masked):
+            f = sss.Frame.empty(V, cam.height, cam.width)
+            sss.sss_render_fwd(pr, b, sc.cameras, bg=(0.1, 0.2, 0.3), out=f)
+            frames.append(f)
+        torch.cuda.synchronize()
+        assert torch.equal(frames[0].rgb, frames[1].rgb) and torch.equal(frames[0].n_contrib, frames[1].n_contrib)
+        assert torch.equal(frames[0].final_T, frames[1].final_T)
+        for v in range(V):
+            ref = orc.render(sc.params, sc.sh_degree, sc.cameras[v], bg=(0.1, 0.2, 0.3), mode="tiled")
+            _check_frame(name, frames[1].rgb[v].cpu().numpy(), frames[1].final_T[v].cpu().numpy(),
+                         frames[1].n_contrib[v].cpu().numpy(), ref)
+        d = torch.from_numpy(np.random.default_rng(8).normal(size=(V, 3, cam.height, cam.width))
+                             .astype(np.float32)).cuda()
+        for cap in (1536, 3):  # tiny strip lists: the unlisted replay filters by the masks too
+            gs = []
+            for b in (plain, masked):
+                f = sss.Frame.empty(V, cam.height, cam.width, tile_cap=cap)
+                sss.sss_render_fwd(pr, b, sc.cameras, out=f)
+                gs.append(sss.sss_render_bwd(params, pr, b, sc.cameras, f, d_rgb=d).planes.cpu().numpy())
+            torch.cuda.synchronize()
+            assert rel_l2(gs[1], gs[0]) <= 1e-5, (name, cap)
+        # every cleared bit of a tile in the entry's rect is a tile none of whose
+        # 256 pixel centres passes the raster's fp32 inclusion test h <= hmax
+        # (brute force, view 0; outside the rect no pixel passes, whatever the
+        # bit); the masks drop a share of the rect's tiles
+        M0 = int(masked.totals[0].item())
+        tm = masked.tmask[0, :M0].cpu().numpy().view(np.uint16).astype(np.int64)
+        ids = masked.ids[0, :M0].cpu().numpy().astype(np.int64)
+        rg = masked.ranges[0].cpu().numpy()
+        rec = pr.rec[0].cpu().numpy().reshape(-1, 12)
+        rect = pr.rect[0].cpu().numpy().reshape(-1, 4).astype(np.int64)
+        tx_n = (cam.width + 15) // 16
+        S = 1 << shift
+        bx_n = ((tx_n + S - 1) // S)
+        kb = np.searchsorted(rg[:, 0], np.arange(M0), side="right") - 1
+        while True:  # empty bins share their successor's start: step to the bin holding k
+            adv = np.arange(M0) >= rg[kb, 1]
+            if not adv.any():
+                break
+            kb[adv] += 1
+        bx, by = (kb % bx_n) * S, (kb // bx_n) * S
+        r = rect[ids]
+        rect_bits = mask_bits = 0
+        f32 = np.float32
+        fma = lambda a, b, c: (a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)).astype(f32)  # noqa: E731
+        for ly in range(S):
+            for lx in range(S):
+                tx, ty = bx + lx, by + ly
+                inr = (tx >= r[:, 0]) & (tx <= r[:, 2]) & (ty >= r[:, 1]) & (ty <= r[:, 3])
+                bit = (tm >> ((ly << shift) | lx)) & 1
+                rect_bits += int(inr.sum())
+                mask_bits += int((bit.astype(bool) & inr).sum())
+                cl = np.nonzero(inr & (bit == 0))[0]
+                for c0 in range(0, len(cl), 4096):
+                    c = cl[c0:c0 + 4096]
+                    e = rec[ids[c]]
+                    mx, my, A, B2, C, hmax = (e[:, q:q + 1].astype(f32) for q in range(6))
+                    px = (tx[c, None] * 16 + np.arange(16)[None, :]).astype(f32) + f32(0.5)
+                    hmin = np.full(len(c), np.inf, dtype=f32)
+                    for yy in range(16):
+                        py = (ty[c, None] * 16 + yy).astype(f32) + f32(0.5)
+                        dx, dy = (px - mx).astype(f32), (py - my).astype(f32)
+                        bdy, cdy2 = (B2 * dy).astype(f32), ((C * dy).astype(f32) * dy).astype(f32)
+                        h = fma(dx, fma(A, dx, bdy), cdy2)
+                        hmin = np.minimum(hmin, h.min(axis=1))
+                    assert (hmin > hmax[:, 0]).all(), (name, shift, int((hmin <= hmax[:, 0]).sum()))
+        if name == "cfg2":
+            assert mask_bits < 0.9 * rect_bits, (mask_bits, rect_bits)
+    # adaptive truncation with masks: the tail (unmasked, rect-tested) joins seamlessly
+    from paper_2503_10148_b200 import api as A
+
+    sc = scenes["cfg2"]
+    params = to_dev(sc)
+    pr = sss.sss_project(params, sc.cameras)
+    full = sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift)
+    f0 = sss.Frame.empty(1, sc.cameras[0].height, sc.cameras[0].width)
+    sss.sss_render_fwd(pr, full, sc.cameras, out=f0)
+    ab = A.Bins.empty(1, full.ranges.shape[1], full.capacity, shift, False, "cuda", 0, sc.n, adaptive=True,
+                      tile_masks=True)
+    ab.used.zero_()  # caps of 1024: many tiles read the tail
+    sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift, out=ab)
+    f1 = sss.Frame.empty(1, sc.cameras[0].height, sc.cameras[0].width)
+    sss.sss_render_fwd(pr, ab, sc.cameras, out=f1)
+    torch.cuda.synchronize()
+    assert torch.equal(f0.rgb, f1.rgb) and torch.equal(f0.n_contrib, f1.n_contrib)
