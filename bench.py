@@ -53,6 +53,9 @@ def parse():
                          "projection backward (0 = one reduce-scatter after it)")
     ap.add_argument("--bins", default="adaptive", choices=["adaptive", "complete"],
                     help="adaptive: per-bin caps from the previous forward's consumption (sss.h sss_bins.used)")
+    ap.add_argument("--tile-masks", type=int, default=None,
+                    help="1: per-entry tile masks in the bin lists (sss.h sss_bins.tmask; default: on for "
+                         "bin_shift 1-2)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--graph", type=int, default=None,
                     help="1: replay each iteration as one CUDA graph (default: on for the launch-bound "
@@ -332,6 +335,7 @@ def arm_config(a, sc, world):
     return {"workload": CONFIG_NAMES[a.config], "n_components": sc.n, "views": sc.n_views,
             "width": cam.width, "height": cam.height, "sh_degree": sc.sh_degree,
             "bin_shift": a.bin_shift, "views_per_batch": a.views_per_batch, "max_per_bin": a.max_per_bin, "bins": a.bins,
+            "tile_masks": bool(a.tile_masks) if a.tile_masks is not None else 1 <= a.bin_shift <= 2,
             "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
                      if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
             "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
@@ -396,7 +400,8 @@ def main():
     hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
     ts = TrainStep(planes, sc.sh_degree, cams, hp, total_views=V, bin_shift=a.bin_shift,
                    views_per_batch=a.views_per_batch, eps_dssim=a.eps_dssim, max_per_bin=a.max_per_bin,
-                   adaptive_bins=a.bins == "adaptive", overlap_blocks=a.overlap_blocks if world > 1 else 0)
+                   adaptive_bins=a.bins == "adaptive", overlap_blocks=a.overlap_blocks if world > 1 else 0,
+                   tile_masks=None if a.tile_masks is None else bool(a.tile_masks))
     for _ in range(a.warmup):
         ts.step(targets)
         if ts.overflowed():

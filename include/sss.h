@@ -148,6 +148,13 @@ typedef struct {
  *           used to 0 for the forward that follows.  Truncation (either
  *           kind) never changes the raster's results; a tile that needs
  *           more than its bin kept reads the tail (slower).
+ *  tmask    [V][capacity] nullable (bin_shift <= 2): per materialised entry,
+ *           the tiles of its bin (bit ly * 2^bin_shift + lx) whose 16x16
+ *           block of pixel centres the component's h <= hmax ellipse may
+ *           reach (a conservative fp32 ellipse-box test); the raster then
+ *           filters a bin's entries by this bit instead of by the tile rect,
+ *           which drops the rect's false positives (~43 % of the entries a
+ *           config-5 forward tile visits) before they are staged.
  *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
  *           scattered for that view and its ranges are empty; grow and
  *           retry).  Sticky: sss_bin_sort only ever sets it; the caller
@@ -168,6 +175,7 @@ typedef struct {
   int32_t* n_vis;
   int32_t* resume;
   int32_t* used;
+  uint16_t* tmask;
 } sss_bins;
 
 /* Rendered frames (output of sss_render_fwd; all views share one size).

@@ -53,7 +53,7 @@ class sss_bins(C.Structure):
                 ("ids", C.c_void_p), ("keys", C.c_void_p), ("ranges", C.c_void_p),
                 ("totals", C.c_void_p), ("overflow", C.c_void_p), ("max_per_bin", C.c_int32),
                 ("reserved", C.c_int32), ("sorted", C.c_void_p), ("n_vis", C.c_void_p),
-                ("resume", C.c_void_p), ("used", C.c_void_p)]
+                ("resume", C.c_void_p), ("used", C.c_void_p), ("tmask", C.c_void_p)]
 
 
 class sss_frame(C.Structure):

@@ -168,10 +168,12 @@ class Bins:
     n_vis: Optional[torch.Tensor] = None   # [V] i32
     resume: Optional[torch.Tensor] = None  # [V][n_bins] i32
     used: Optional[torch.Tensor] = None    # [V][n_bins] i32: adaptive truncation (sss.h)
+    tmask: Optional[torch.Tensor] = None   # [V][capacity] i16: per-entry tile masks (sss.h)
 
     @classmethod
     def empty(cls, V: int, n_bins: int, capacity: int, bin_shift: int, keys: bool,
-              device="cuda", max_per_bin: int = 0, n: int = 0, adaptive: bool = False) -> "Bins":
+              device="cuda", max_per_bin: int = 0, n: int = 0, adaptive: bool = False,
+              tile_masks: bool = False) -> "Bins":
         """n: components (needed for the sorted array when truncating).
         adaptive: per-bin caps from the previous forward's consumption (the
         first call, with used = -1, builds complete lists)."""
@@ -187,13 +189,14 @@ class Bins:
                    torch.empty((V, max(int(n), 1)), dtype=torch.int32, device=device) if trunc else None,
                    torch.zeros((V,), dtype=torch.int32, device=device) if trunc else None,
                    torch.empty((V, n_bins), dtype=torch.int32, device=device) if trunc else None,
-                   torch.full((V, n_bins), -1, dtype=torch.int32, device=device) if adaptive else None)
+                   torch.full((V, n_bins), -1, dtype=torch.int32, device=device) if adaptive else None,
+                   torch.empty((V, cap), dtype=torch.int16, device=device) if tile_masks else None)
 
     def c(self) -> L.sss_bins:
         return L.sss_bins(self.bin_shift, int(self.totals.shape[0]), self.capacity, _ptr(self.ids),
                           _ptr(self.keys), _ptr(self.ranges), _ptr(self.totals),
                           _ptr(self.overflow), int(self.max_per_bin), 0, _ptr(self.sorted),
-                          _ptr(self.n_vis), _ptr(self.resume), _ptr(self.used))
+                          _ptr(self.n_vis), _ptr(self.resume), _ptr(self.used), _ptr(self.tmask))
 
     def view(self, nv: int) -> "Bins":
         """The first nv views (shared storage)."""
@@ -203,7 +206,8 @@ class Bins:
                     self.sorted[:nv] if self.sorted is not None else None,
                     self.n_vis[:nv] if self.n_vis is not None else None,
                     self.resume[:nv] if self.resume is not None else None,
-                    self.used[:nv] if self.used is not None else None)
+                    self.used[:nv] if self.used is not None else None,
+                    self.tmask[:nv] if self.tmask is not None else None)
 
 
 TILE_CAP = 1536  # composited entries per 16x8 strip the forward records for the backward
@@ -268,7 +272,8 @@ def bin_sort_workspace_bytes(n: int, cams: Sequence, bin_shift: int, cams_c=None
 def sss_bin_sort(proj: Projected, cams: Sequence, bin_shift: int = 0,
                  capacity: Optional[int] = None, keys: bool = False,
                  ws: Optional[torch.Tensor] = None, out: Optional[Bins] = None, stream=None,
-                 cams_c=None, headroom: float = 1.25, max_per_bin: int = 0) -> Bins:
+                 cams_c=None, headroom: float = 1.25, max_per_bin: int = 0,
+                 tile_masks: bool = False) -> Bins:
     """Bin and depth-sort.  With capacity=None the instance count is measured
     first (one host sync) and the output sized with `headroom`.
     max_per_bin > 0: truncated lists (sss.h sss_bins)."""
@@ -288,7 +293,7 @@ def sss_bin_sort(proj: Projected, cams: Sequence, bin_shift: int = 0,
             L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(pc),
                                      _stream_ptr(stream)), "sss_bin_sort(probe)")
             capacity = int(int(probe.totals.max().item()) * headroom) + 1024
-        out = Bins.empty(V, nb, capacity, bin_shift, keys, dev, max_per_bin, proj.n)
+        out = Bins.empty(V, nb, capacity, bin_shift, keys, dev, max_per_bin, proj.n, tile_masks=tile_masks)
     bc, prc = out.c(), proj.c()
     L.check(lib.sss_bin_sort(C.byref(prc), cc, V, _ptr(ws), ws.numel(), C.byref(bc),
                              _stream_ptr(stream)), "sss_bin_sort")

@@ -694,6 +694,161 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
   }
 }
 
+
+// Tile mask of a bin-list entry (sss_bins.tmask): bit ly * 2^shift + lx
+// for each tile (bx + lx, by + ly) of the bin whose 16x16 block of pixel
+// centres the ellipse h(dx, dy) = A dx^2 + B2 dx dy + C dy^2 <= hmax may
+// reach.  The rect is not read: it is a conservative bound of the same
+// ellipse, so a bit outside it marks a tile where no pixel passes anyway and
+// the raster's results cannot change.  Row by row: the ellipse's x-extent
+// over the row's band of pixel-centre y, then the tile columns that interval
+// meets.  Conservative by construction (fp32 throughout, every rounding
+// covered by a margin):
+//  * the raster's fp32 h carries a rounding error of a few ulp of
+//    M = A|dx|^2 + |B2||dx||dy| + C|dy|^2 (M over the bin box), so the
+//    ellipse is taken at hm = hmax + 1e-5 M;
+//  * det = A C - (B2/2)^2 by Kahan's 2x2 determinant (fma residuals), a
+//    few ulp relative even for thin ellipses;
+//  * for a band [d0, d1] (relative to my) the leftmost point is
+//    x = (-hB dy - sqrt(A hm - det dy^2)) / A, convex in dy with its minimum
+//    at dyL = hB xe / C (xe = sqrt(C hm / det), the ellipse's half-width):
+//    -xe whenever dyL lies in the band (with a tolerance), else the value at
+//    the band end nearest dyL; the right end mirrors it;
+//  * the discriminant's absolute error (~1e-7 A hm) moves x by <= 5e-4 xe:
+//    the interval is widened by 1e-3 xe + 1e-5 of its terms + 1e-3 px, the
+//    half-extents by 1e-5 + 1e-3 px and the bands by 1e-3 px.
+// A degenerate record (det <= 0, A or C <= 0, NaN, overflow) keeps every bit.
+// MUFU approximations (relative error <= 2^-22), covered by the margins below.
+__device__ __forceinline__ float sqrt_apx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t entry_tile_mask(float mx, float my, float A, float B2, float C, float hmax,
+                                                    int bx, int by, int sft) {
+  const int S = 1 << sft;
+  const uint32_t rowbits = (1u << S) - 1u;
+  const float X0 = (float)(bx * kTile) + 0.5f, X1 = (float)((bx + S) * kTile) - 0.5f;
+  const float Y0 = (float)(by * kTile) + 0.5f, Y1 = (float)((by + S) * kTile) - 0.5f;
+  const float mdx = fmaxf(fabsf(X0 - mx), fabsf(X1 - mx)), mdy = fmaxf(fabsf(Y0 - my), fabsf(Y1 - my));
+  const float M = fmaf(A * mdx, mdx, fmaf(fabsf(B2) * mdx, mdy, C * mdy * mdy));
+  const float hm = fmaf(1e-5f, M, hmax);
+  const float hB = 0.5f * B2;
+  const float p1 = A * C, p2 = hB * hB;
+  const float det = (p1 - p2) + (fmaf(A, C, -p1) - fmaf(hB, hB, -p2));
+  if (!(det > 1e-30f) || !(A > 0.f) || !(C > 0.f) || !(hm >= 0.f) || !(M < 1e30f)) {
+    uint32_t m = 0u;
+    for (int ly = 0; ly < S; ++ly) m |= rowbits << (ly << sft);
+    return m;
+  }
+  const float idet = rcp_apx(det);
+  const float Ah = A * hm;
+  const float ym = sqrt_apx(Ah * idet);  // the ellipse's dy half-extent
+  const float ymw = fmaf(ym, 1e-5f, ym) + 1e-3f;
+  const float xe = sqrt_apx(C * hm * idet);  // its dx half-extent
+  const float xew = fmaf(xe, 1e-5f, xe) + 1e-3f;
+  const float dyL = hB * xe * rcp_apx(C);  // the leftmost point's dy (the rightmost's is -dyL)
+  const float tol = fmaf(1e-4f, fabsf(dyL), 1e-3f);
+  const float iA = rcp_apx(A);
+  const float marg = fmaf(1e-3f, xe, 1e-3f);
+  uint32_t m = 0u;
+  for (int ly = 0; ly < S; ++ly) {
+    const float b0 = (float)((by + ly) * kTile) + 0.5f - my - 1e-3f;
+    const float b1 = (float)((by + ly) * kTile) + (kTile - 0.5f) - my + 1e-3f;
+    if (b0 > ymw || b1 < -ymw) continue;
+    float d0 = fmaxf(b0, -ym), d1 = fminf(b1, ym);
+    if (d0 > d1) d0 = d1 = (b0 > 0.f ? ym : -ym);  // the band only grazes a tip
+    float L, R;
+    if (dyL >= d0 - tol && dyL <= d1 + tol) {
+      L = -xew;
+    } else {
+      const float dl = fminf(fmaxf(dyL, d0), d1);
+      const float sl = sqrt_apx(fmaxf(fmaf(-det * dl, dl, Ah), 0.f));
+      const float t = -hB * dl;
+      L = (t - sl) * iA - fmaf(1e-5f, (fabsf(t) + sl) * iA, marg);
+    }
+    if (-dyL >= d0 - tol && -dyL <= d1 + tol) {
+      R = xew;
+    } else {
+      const float dr = fminf(fmaxf(-dyL, d0), d1);
+      const float sr = sqrt_apx(fmaxf(fmaf(-det * dr, dr, Ah), 0.f));
+      const float t = -hB * dr;
+      R = (t + sr) * iA + fmaf(1e-5f, (fabsf(t) + sr) * iA, marg);
+    }
+    // tile column bx + lx (pixel centres [16 (bx+lx) + 0.5, + 15.5]) meets [mx + L, mx + R]
+    const float lo_f = ceilf((mx + L - (kTile - 0.5f)) * (1.f / kTile)) - (float)bx;
+    const float hi_f = floorf((mx + R - 0.5f) * (1.f / kTile)) - (float)bx;
+    const int lo = lo_f > 0.f ? (int)lo_f : 0;
+    const int hi = hi_f < (float)(S - 1) ? (int)hi_f : S - 1;
+    if (lo <= hi) m |= ((2u << hi) - (1u << lo)) << (ly << sft);
+  }
+  return m;
+}
+
+#ifndef SSS_MASK_PER
+#define SSS_MASK_PER 4
+#endif
+constexpr int kMaskPer = SSS_MASK_PER;  // entries per lane per step, all gathers in flight together
+// sss_bins.tmask for every materialised entry: grid (G, V); CTA c owns a
+// contiguous slice of its view's entries [0, totals[v]) (the bins'
+// materialised ranges are contiguous from 0), its warps take 32 kMaskPer entries
+// at a time.  The bin of an entry
+// is found once per warp by binary search over the range starts, then by
+// walking forward.
+__global__ void __launch_bounds__(256) tile_mask_kernel(const int32_t* __restrict__ ids,
+                                                        const int32_t* __restrict__ ranges,
+                                                        const int64_t* __restrict__ totals, int64_t capacity,
+                                                        const float4* __restrict__ rec, int64_t n, BinGeom g,
+                                                        uint16_t* __restrict__ tmask) {
+  const int v = blockIdx.y;
+  const int64_t tot = totals[v];
+  if (tot > capacity) return;  // overflowed: nothing scattered
+  const int64_t per = ((tot + gridDim.x - 1) / gridDim.x + 32 * kMaskPer - 1) & ~(int64_t)(32 * kMaskPer - 1);
+  const int64_t c0 = (int64_t)blockIdx.x * per, c1 = min(tot, c0 + per);
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  int64_t base = c0 + (int64_t)w * 32 * kMaskPer;
+  if (base >= c1) return;
+  const int2* rg = reinterpret_cast<const int2*>(ranges) + (size_t)v * g.n_bins;
+  const int32_t* idv = ids + (int64_t)v * capacity;
+  uint16_t* tmv = tmask + (int64_t)v * capacity;
+  const float4* recv = rec + (int64_t)v * n * 3;
+  int bw = 0;  // last bin whose start <= base (empty bins share their successor's start)
+  {
+    int hi = g.n_bins - 1;
+    while (bw < hi) {
+      const int mid = (bw + hi + 1) >> 1;
+      if (__ldg(&rg[mid].x) <= base) bw = mid; else hi = mid - 1;
+    }
+  }
+  for (; base < c1; base += kMaskPer * 32 * (int64_t)(blockDim.x >> 5)) {
+    while (base >= __ldg(&rg[bw].y)) ++bw;  // warp-uniform
+    int id[kMaskPer];
+#pragma unroll
+    for (int q = 0; q < kMaskPer; ++q) id[q] = base + q * 32 + lane < c1 ? __ldg(idv + base + q * 32 + lane) : 0;
+    float4 a[kMaskPer];
+    float2 e[kMaskPer];
+#pragma unroll
+    for (int q = 0; q < kMaskPer; ++q) {
+      a[q] = __ldg(recv + (int64_t)id[q] * 3);
+      e[q] = __ldg(reinterpret_cast<const float2*>(recv + (int64_t)id[q] * 3 + 1));
+    }
+    int b = bw;
+#pragma unroll
+    for (int q = 0; q < kMaskPer; ++q) {
+      const int64_t p = base + q * 32 + lane;
+      while (p >= __ldg(&rg[b].y) && b < g.n_bins - 1) ++b;
+      if (p < c1)
+        tmv[p] = (uint16_t)entry_tile_mask(a[q].x, a[q].y, a[q].z, a[q].w, e[q].x, e[q].y, (b % g.bins_x) << g.shift,
+                                           (b / g.bins_x) << g.shift, g.shift);
+    }
+  }
+}
+
 }  // namespace
 }  // namespace sss
 
@@ -733,6 +888,11 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     set_error("sss_bin_sort: truncated lists (max_per_bin > 0 or used) need sorted, n_vis and resume");
     return SSS_ERR_ARG;
   }
+  if (out->tmask && out->bin_shift > 2) {
+    set_error("sss_bin_sort: tile masks (tmask) need bin_shift <= 2 (16 tiles per bin)");
+    return SSS_ERR_ARG;
+  }
+  if (out->tmask && !pr->rec) { set_error("sss_bin_sort: tile masks need the projected records"); return SSS_ERR_ARG; }
   if (n > 0x7fffffffLL - out->capacity) {  // virtual list positions (start + n) must fit int32
     set_error("sss_bin_sort: n + capacity must be < 2^31");
     return SSS_ERR_SHAPE;
@@ -822,6 +982,12 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
         out->totals,
         out->capacity, bcap, stage_cap, out->ids, out->keys, resume);
     count_launch();
+    if (out->tmask) {
+      const int gx = std::max(1, std::min(1024, 148 * 8 / n_views));
+      tile_mask_kernel<<<dim3(gx, n_views), 256, 0, s>>>(out->ids, out->ranges, out->totals, out->capacity,
+                                                               (const float4*)pr->rec, n, g, out->tmask);
+      count_launch();
+    }
   }
   return check_launch("sss_bin_sort");
 }

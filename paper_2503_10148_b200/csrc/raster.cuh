@@ -105,7 +105,23 @@ struct RasterGeom {
   const int32_t* n_vis;
   const int32_t* resume;
   int32_t* used;  // adaptive truncation: per-bin consumption written by the forward (nullable)
+  const uint16_t* tmask;  // per-entry tile masks of the bin lists (nullable, sss.h)
 };
+
+// Does bin-list entry `pos` (component id) belong to tile (tx, ty)?  The
+// entry's tile mask bit when the bins carry masks (listed entries only),
+// else its tile rect (a truncated list's tail is always rect-tested).
+__device__ __forceinline__ bool entry_in_tile(const RasterGeom& G, const uint16_t* __restrict__ tmv, int32_t pos,
+                                              int32_t mend, int id, const short4* __restrict__ rcv, int tx,
+                                              int ty) {
+  if (G.tmask && pos < mend) {
+    const int m = G.shift;
+    const int bit = ((ty & ((1 << m) - 1)) << m) | (tx & ((1 << m) - 1));
+    return (__ldg(tmv + pos) >> bit) & 1;
+  }
+  const short4 r = rcv[id];
+  return tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
+}
 
 // The list of the tile's bin as the raster walks it: positions [start, end)
 // with end = mend + tail length; position p maps to a component through

@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
 
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
+  const uint16_t* tmv = G.tmask ? G.tmask + (int64_t)v * G.capacity : nullptr;
   float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
@@ -265,10 +266,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     bool ok = id >= 0;
     // unlisted replay: filter by the tile rect with bins, and always in the
     // truncated list's tail (the depth-sorted visible set)
-    if (!use_list && ok && (FILTER || p >= BL.mend)) {
-      const short4 r = rcv[id];
-      ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
-    }
+    if (!use_list && ok && (FILTER || p >= BL.mend)) ok = entry_in_tile(G, tmv, p, BL.mend, id, rcv, tx, ty);
     // tag: the entry's g2d record offset (uint32: n < 2^32 / SSS_G2D_FLOATS, checked by the API)
     return stage_batch(S, buf, ok, p, id, rv, lt, (int32_t)((uint32_t)id * SSS_G2D_FLOATS));
   };

@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
 
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
+  const uint16_t* tmv = G.tmask ? G.tmask + (int64_t)v * G.capacity : nullptr;
 
   if (threadIdx.x == 0) SSS_COUNT(7, end - start);
   PixF2 p[kPairs];
@@ -140,10 +141,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int slot, nb;
     // the truncated list's tail is the depth-sorted visible set: always filtered
     if (FILTER || end > BL.mend) {
-      if (ok && (FILTER || pos >= BL.mend)) {
-        const short4 r = rcv[id];
-        ok = tx >= r.x && tx <= r.z && ty >= r.y && ty <= r.w;
-      }
+      if (ok && (FILTER || pos >= BL.mend)) ok = entry_in_tile(G, tmv, pos, BL.mend, id, rcv, tx, ty);
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       if (lane == 0) wcnt[w] = __popc(bal);
       __syncthreads();
@@ -275,6 +273,7 @@ bool raster_geom(const sss_projected* pr, const sss_bins* bins, const sss_camera
   G.n_vis = trunc ? bins->n_vis : nullptr;
   G.resume = trunc ? bins->resume : nullptr;
   G.used = bins->used;
+  G.tmask = (bins->tmask && bins->bin_shift <= 2) ? bins->tmask : nullptr;
   if (trunc && (!bins->sorted || !bins->n_vis || !bins->resume)) return false;
   return G.n_bins <= SSS_MAX_BINS && pr->n_views == n_views && bins->n_views == n_views;
 }

@@ -38,7 +38,8 @@ class TrainStep:
                  group=None, momentum: Optional[torch.Tensor] = None,
                  adam_m: Optional[torch.Tensor] = None, adam_v: Optional[torch.Tensor] = None,
                  eps_dssim: float = 0.0, variant: int = 0, shard_update: Optional[bool] = None,
-                 max_per_bin: int = 0, adaptive_bins: bool = False, overlap_blocks: int = 0):
+                 max_per_bin: int = 0, adaptive_bins: bool = False, overlap_blocks: int = 0,
+                 tile_masks: Optional[bool] = None):
         dev = planes.device
         world = D.dist.get_world_size(group) if D.dist.is_initialized() else 1
         # ZeRO-1 sharded sampler step for R > 1 (dist.py): plane buffers padded
@@ -84,6 +85,8 @@ class TrainStep:
         # adaptive truncation: each view batch keeps its bins' consumption from
         # the previous iteration's forward (sss.h sss_bins.used; -1 = complete)
         self.adaptive_bins = bool(adaptive_bins)
+        # per-entry tile masks (sss.h sss_bins.tmask): on by default for bins of 2x2 / 4x4 tiles
+        self.tile_masks = (1 <= self.bin_shift <= 2) if tile_masks is None else bool(tile_masks)
         self.bg = tuple(float(x) for x in bg)
         self.headroom = headroom
         self.group = group
@@ -141,7 +144,7 @@ class TrainStep:
         vb = len(self.batches[0])
         self.bins = [A.Bins.empty(vb, self.n_bins, cap, self.bin_shift, False,
                                   self.params.planes.device, self.max_per_bin, self.params.n,
-                                  adaptive=self.adaptive_bins)]
+                                  adaptive=self.adaptive_bins, tile_masks=self.tile_masks)]
         self.capacity = cap
 
     def _proj_view(self, nv: int) -> A.Projected:

@@ -1,4 +1,2 @@
-for rep in 1 2; do
-SSS_TILE_LISTS_DEV=2 SSS_LIB=variants/libsss_2warp.so python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive >> gpurun_out/ab_2w.jsonl 2>&1
-python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive >> gpurun_out/ab_2w.jsonl 2>&1
-done
+rm -f gpurun_out/ab_tm.jsonl
+for rep in 1 2; do for lib in paper_2503_10148_b200/build_SSS_MASK_PER2/libsss.so paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_MASK_PER8/libsss.so; do echo $lib >> gpurun_out/ab_tm.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab_tm.jsonl 2>&1; done; done

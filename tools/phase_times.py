@@ -14,6 +14,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-count", action="store_true", help="forward without the n_contrib diagnostic")
 ap.add_argument("--tile-cap", type=int, default=None)
 ap.add_argument("--adaptive", action="store_true", help="adaptive bin caps (sss_bins.used), after one warm round")
+ap.add_argument("--tmask", type=int, default=1, help="per-entry tile masks (sss_bins.tmask)")
 a = ap.parse_args()
 sc = make_scene(a.config, n_views=a.views)
 cams = sc.cameras
@@ -23,7 +24,8 @@ tgt = torch.from_numpy(make_targets(sc)).cuda()
 pr = P.sss_project(params, cams)
 bins = P.sss_bin_sort(pr, cams, bin_shift=a.shift)
 if a.adaptive:
-    bins = A.Bins.empty(V, bins.ranges.shape[1], bins.capacity, a.shift, False, "cuda", 0, params.n, adaptive=True)
+    bins = A.Bins.empty(V, bins.ranges.shape[1], bins.capacity, a.shift, False, "cuda", 0, params.n, adaptive=True,
+                        tile_masks=bool(a.tmask) and 1 <= a.shift <= 2)
     P.sss_bin_sort(pr, cams, bin_shift=a.shift, out=bins)
     P.sss_render_fwd(pr, bins, cams, out=P.Frame.empty(V, cams[0].height, cams[0].width))
     used0 = bins.used.clone()  # every timed bin_sort starts from the warm round's consumption
