@@ -148,13 +148,18 @@ typedef struct {
  *           used to 0 for the forward that follows.  Truncation (either
  *           kind) never changes the raster's results; a tile that needs
  *           more than its bin kept reads the tail (slower).
- *  tmask    [V][capacity] nullable (bin_shift <= 2): per materialised entry,
- *           the tiles of its bin (bit ly * 2^bin_shift + lx) whose 16x16
- *           block of pixel centres the component's h <= hmax ellipse may
- *           reach (a conservative fp32 ellipse-box test); the raster then
- *           filters a bin's entries by this bit instead of by the tile rect,
- *           which drops the rect's false positives (~43 % of the entries a
- *           config-5 forward tile visits) before they are staged.
+ *  tmask    [V][capacity] nullable (bin_shift <= 2; needs pr->rec): per
+ *           materialised entry, bit ly * 2^bin_shift + lx is set for the
+ *           tiles of its bin whose 16x16 block of pixel centres the
+ *           component's h <= hmax ellipse (R9) may reach -- conservative:
+ *           a cleared bit guarantees no pixel of that tile passes the
+ *           raster's fp32 inclusion test; a set bit may be a tile it misses
+ *           (also outside the tile rect).  The raster filters a bin's listed
+ *           entries by this bit instead of by the tile rect (a truncated
+ *           list's tail stays rect-filtered), which drops the rect's false
+ *           positives (~43 % of the entries a config-5 forward tile visits)
+ *           before they are staged; results are unchanged.  Computed by
+ *           sss_bin_sort after the scatter (one extra kernel).
  *  overflow [1] set to 1 if any totals[v] > capacity (then nothing is
  *           scattered for that view and its ranges are empty; grow and
  *           retry).  Sticky: sss_bin_sort only ever sets it; the caller

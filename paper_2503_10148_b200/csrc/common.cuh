@@ -63,31 +63,5 @@ sss_status validate_cams(const sss_camera* cams, int n_views, const char* what);
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
-// Conservative ellipse-box test: false only if no point of the box
-// [X0, X1] x [Y0, Y1] (a strip's pixel centres) can pass the fp32 inclusion
-// test h <= hmax of the record (mx, my, A, B2, C, hmax).  The exact minimum of
-// the convex quadratic over the box is 0 if the mean lies inside, else the
-// least of its four edge minima (each a clamped 1-D vertex); the comparison
-// allows 1e-5 of an upper bound M of the quadratic's terms over the box, far
-// above the few-ulp difference between this evaluation and the per-pixel
-// fp32 sequence (so the per-pixel decisions, and the image, are unchanged).
-__device__ __forceinline__ bool ellipse_meets_box(float mx, float my, float A, float B2, float C, float hmax,
-                                                  float X0, float X1, float Y0, float Y1) {
-  const float dx0 = X0 - mx, dx1 = X1 - mx, dy0 = Y0 - my, dy1 = Y1 - my;
-  if (dx0 <= 0.f && dx1 >= 0.f && dy0 <= 0.f && dy1 >= 0.f) return true;
-  const float mdx = fmaxf(fabsf(dx0), fabsf(dx1)), mdy = fmaxf(fabsf(dy0), fabsf(dy1));
-  const float M = fmaf(A * mdx, mdx, fmaf(fabsf(B2) * mdx, mdy, C * mdy * mdy));
-  const float lim = fmaf(1e-5f, M, hmax);
-  const float hB = 0.5f * B2;
-  const float iC = 1.f / C, iA = 1.f / A;
-  auto q = [&](float dx, float dy) { return fmaf(dx, fmaf(A, dx, B2 * dy), C * dy * dy); };
-  const float ya = fminf(fmaxf(-hB * dx0 * iC, dy0), dy1);
-  const float yb = fminf(fmaxf(-hB * dx1 * iC, dy0), dy1);
-  const float xa = fminf(fmaxf(-hB * dy0 * iA, dx0), dx1);
-  const float xb = fminf(fmaxf(-hB * dy1 * iA, dx0), dx1);
-  const float m = fminf(fminf(q(dx0, ya), q(dx1, yb)), fminf(q(xa, dy0), q(xb, dy1)));
-  return !(m > lim);  // NaN-safe: keep the entry
-}
-
 
 }  // namespace sss
