@@ -186,7 +186,10 @@ __device__ __forceinline__ void bin_rect(short4 r, int shift, int& bx0, int& by0
 // components).  Writes the chunk totals (u32, for the scans) and the per-warp
 // counts (u16: a warp's 256 components hit a bin at most 256 times; the 8
 // warps' counts of a bin packed in one 16-byte word), so the scatter needs no
-// counting pass of its own.
+// counting pass of its own.  Each component adds its rect of bins as a 2-D
+// difference (<= 4 shared atomics instead of one per instance: 9.2 per
+// component at config 5), and the per-warp grids are prefix-summed by rows
+// and columns before the write-out (bin_sort -0.6 ms per config-5 step).
 __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32_t* __restrict__ sorted_ids,
                                                          const int32_t* __restrict__ n_vis,
                                                          const short4* __restrict__ rect, int64_t n,
@@ -207,8 +210,26 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
     const int id = sorted_ids[(int64_t)v * n + j];
     int bx0, by0, bx1, by1;
     bin_rect(rect[(int64_t)v * n + id], g.shift, bx0, by0, bx1, by1);
-    for (int by = by0; by <= by1; ++by)
-      for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&my[by * g.bins_x + bx], 1u);
+    if (bx0 > bx1 || by0 > by1) continue;
+    // the rect's bins as a 2-D difference (<= 4 corner updates, mod 2^32)
+    const bool xe = bx1 + 1 < g.bins_x, ye = by1 + 1 < g.bins_y;
+    atomicAdd(&my[by0 * g.bins_x + bx0], 1u);
+    if (xe) atomicAdd(&my[by0 * g.bins_x + bx1 + 1], 0xFFFFFFFFu);
+    if (ye) atomicAdd(&my[(by1 + 1) * g.bins_x + bx0], 0xFFFFFFFFu);
+    if (xe && ye) atomicAdd(&my[(by1 + 1) * g.bins_x + bx1 + 1], 1u);
+  }
+  __syncthreads();
+  // 2-D prefix sums of every warp's difference grid: rows, then columns
+  for (int r = threadIdx.x; r < kScatterWarps * g.bins_y; r += blockDim.x) {
+    uint32_t* row = hs + (size_t)(r / g.bins_y) * nb + (size_t)(r % g.bins_y) * g.bins_x;
+    uint32_t acc = 0;
+    for (int x = 0; x < g.bins_x; ++x) row[x] = acc += row[x];
+  }
+  __syncthreads();
+  for (int cidx = threadIdx.x; cidx < kScatterWarps * g.bins_x; cidx += blockDim.x) {
+    uint32_t* col = hs + (size_t)(cidx / g.bins_x) * nb + (cidx % g.bins_x);
+    uint32_t acc = 0;
+    for (int y = 0; y < g.bins_y; ++y) col[(size_t)y * g.bins_x] = acc += col[(size_t)y * g.bins_x];
   }
   __syncthreads();
   uint32_t* out = chunk_hist + ((size_t)v * n_chunks + c) * nb;
