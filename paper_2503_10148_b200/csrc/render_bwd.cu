@@ -30,6 +30,8 @@
 // and finally the chain Sigma -> (R(q), S) -> (q, log_scale) and the
 // reparameterisations o = tanh(raw), nu = 1 + softplus(raw) once for all
 // views.  grad += result (one read-modify-write of the 240 B per component).
+#include <cstdlib>
+
 #include "raster.cuh"
 
 namespace sss {
@@ -165,9 +167,13 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
     float* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
-    int32_t tile_cap) {
+    int32_t tile_cap, int v0) {
   __shared__ WarpStage stage[kRasterWarps];
-  const int v = blockIdx.y;
+  // views v0 + blockIdx.y; g2d points at view v0's records and the entry
+  // tags are 32-bit record offsets from it (the host sizes the view groups
+  // so that they fit), so the RED address is one 32-bit add + one wide IMAD
+  const int v = v0 + (int)blockIdx.y;
+  const uint32_t vtag = (uint32_t)blockIdx.y * (uint32_t)G.n * (uint32_t)SSS_G2D_FLOATS;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int bin = (ty >> G.shift) * G.bins_x + (tx >> G.shift);
@@ -231,7 +237,6 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const float4* rv = rec + (int64_t)v * G.n * 3;
   const short4* rcv = rect + (int64_t)v * G.n;
   const uint16_t* tmv = G.tmask ? G.tmask + (int64_t)v * G.capacity : nullptr;
-  float* gvf = g2d + (int64_t)v * G.n * SSS_G2D_FLOATS;
   WarpStage& S = stage[w];
   const int ridx = reduce10_index(lane);
   // opaque copies of the lane and of the lane's slot in the 10-float record
@@ -267,8 +272,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     // unlisted replay: filter by the tile rect with bins, and always in the
     // truncated list's tail (the depth-sorted visible set)
     if (!use_list && ok && (FILTER || p >= BL.mend)) ok = entry_in_tile(G, tmv, p, BL.mend, id, rcv, tx, ty);
-    // tag: the entry's g2d record offset (uint32: n < 2^32 / SSS_G2D_FLOATS, checked by the API)
-    return stage_batch(S, buf, ok, p, id, rv, lt, (int32_t)((uint32_t)id * SSS_G2D_FLOATS));
+    // tag: the entry's g2d record offset from view v0's (uint32, see above)
+    return stage_batch(S, buf, ok, p, id, rv, lt, (int32_t)(vtag + (uint32_t)id * SSS_G2D_FLOATS));
   };
 
   int32_t hi = lend;
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       const float r = warp_reduce10(vals, lane_o);
       // one RED per warp and entry: lanes 0, 2, .. hold the 10 sums of the
       // 40-byte screen-space gradient record g2d[v][id]
-      if (roff >= 0 && r != 0.f) atomicAdd(gvf + ((uint32_t)S.id[buf][j] + (uint32_t)roff), r);
+      if (roff >= 0 && r != 0.f) atomicAdd(g2d + ((uint32_t)S.id[buf][j] + (uint32_t)roff), r);
     }
     __syncwarp();  // this buffer is refilled two batches on
     nb = nb_next;
@@ -758,13 +763,19 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   if (!fwd->rgb || !fwd->final_T || !fwd->last) { set_error("sss_render_bwd: null frame buffer"); return SSS_ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   float* g2d = (float*)ws;
-  const dim3 grid(G.tiles_x * G.tiles_y, n_views);
+  // view groups whose g2d records (n * 10 floats each) span < 2^32 floats:
+  // the raster's 32-bit record tags (one group at config 5: 64 x 3M x 10)
+  int vg = (int)std::max<int64_t>(1, std::min<int64_t>(n_views, (int64_t)0xffffffffu /
+                                                                    std::max<int64_t>(1, p->n * SSS_G2D_FLOATS)));
+  if (const char* e = getenv("SSS_BWD_VIEW_GROUP")) vg = std::max(1, std::min(vg, atoi(e)));  // tests: force groups
   const float4* rec = (const float4*)pr->rec;
   const short4* rect = (const short4*)pr->rect;
-#define SSS_BWD_LAUNCH(F, L, N)                                                                     \
-  render_bwd_kernel<F, L, N><<<grid, kRasterThreads, 0, s>>>(                              \
-      rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last, \
-      d_rgb, target, loss_out, g2d, fwd->tile_list, fwd->tile_count, fwd->tile_cap)
+#define SSS_BWD_LAUNCH(F, L, N)                                                                           \
+  for (int gv0 = 0; gv0 < n_views; gv0 += vg)                                                              \
+  render_bwd_kernel<F, L, N><<<dim3(G.tiles_x * G.tiles_y, std::min(vg, n_views - gv0)), kRasterThreads, 0, s>>>( \
+      rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last,       \
+      d_rgb, target, loss_out, g2d + (int64_t)gv0 * p->n * SSS_G2D_FLOATS, fwd->tile_list, fwd->tile_count, \
+      fwd->tile_cap, gv0)
 #define SSS_BWD_LAUNCH_N(F, L)              \
   do {                                      \
     if (nup) SSS_BWD_LAUNCH(F, L, true);    \
@@ -778,7 +789,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
     } else {
       if (l1) SSS_BWD_LAUNCH_N(false, true); else SSS_BWD_LAUNCH_N(false, false);
     }
-    count_launch();
+    count_launch((n_views + vg - 1) / vg);
     if ((st = check_launch("sss_render_bwd(raster)")) != SSS_OK) return st;
   }
 #undef SSS_BWD_LAUNCH_N

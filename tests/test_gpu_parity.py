@@ -901,3 +901,41 @@ def test_tile_masks(orc, sss, scenes, shift):
     sss.sss_render_fwd(pr, ab, sc.cameras, out=f1)
     torch.cuda.synchronize()
     assert torch.equal(f0.rgb, f1.rgb) and torch.equal(f0.n_contrib, f1.n_contrib)
+
+
+def test_backward_view_groups(orc, sss, scenes, monkeypatch):
+    """The raster backward tags entries with 32-bit g2d record offsets from
+    the first view of a launch group; a launch spanning >= 2^32 record floats
+    is split into view groups (SSS_BWD_VIEW_GROUP forces small groups here).
+    Groups of 1 and 2 views give the single-launch gradients (up to the
+    order of the float atomics) and the L1 loss, on the bin-list and on the
+    unlisted replay paths."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    sc = scenes["blobs_d2_3v"]
+    V, cam = sc.n_views, sc.cameras[0]
+    assert V >= 3
+    tgt = torch.from_numpy(np.random.default_rng(2).uniform(size=(V, 3, cam.height, cam.width))
+                           .astype(np.float32)).cuda()
+    for cap in (2048, 0):
+        res = []
+        for group in (None, "1", "2"):
+            if group is None:
+                monkeypatch.delenv("SSS_BWD_VIEW_GROUP", raising=False)
+            else:
+                monkeypatch.setenv("SSS_BWD_VIEW_GROUP", group)
+            params = to_dev(sc)
+            pr = sss.sss_project(params, sc.cameras)
+            bins = sss.sss_bin_sort(pr, sc.cameras, bin_shift=1)
+            fr = sss.Frame.empty(V, cam.height, cam.width, tile_cap=cap)
+            sss.sss_render_fwd(pr, bins, sc.cameras, out=fr)
+            loss = torch.zeros(1, device="cuda")
+            g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, target=tgt, loss=loss)
+            torch.cuda.synchronize()
+            res.append((g.planes.cpu().numpy().astype(np.float64), float(loss.item())))
+        monkeypatch.delenv("SSS_BWD_VIEW_GROUP", raising=False)
+        for gk, lk in res[1:]:
+            assert rel_l2(gk, res[0][0]) <= 1e-5, cap
+            assert abs(lk - res[0][1]) <= 1e-6 * abs(res[0][1]), cap
