@@ -184,8 +184,11 @@ def roofline_for(phase_ms, counts, n, views, pk, steps, views_per_launch=16, ker
     P = counts["planes"]
     # projection: params read once per launch (<=views_per_batch views) + 60 B/view written
     table["project"] = ("hbm", counts["launches_per_step"] * n * 4 * P + views * n * 60, hbm_peak, "GB/s")
-    # bin/sort: lower bound = 4 B id written per instance + 4 B depth key read per comp-view
-    table["bin_sort"] = ("hbm", counts["instances"] * 4 + views * n * 4, hbm_peak, "GB/s")
+    # bin/sort: 16 B per comp-view (4 B depth + 8 B rect read, 4 B sorted id written)
+    # + 4 B id written per materialised instance (+ 4 B id and 24 B record read, 2 B mask written
+    # with tile masks)
+    table["bin_sort"] = ("hbm", views * n * 16 + counts["instances"] * (34 if counts.get("tile_masks") else 4),
+                         hbm_peak, "GB/s")
     # projection backward: g2d 40 B read per comp-view + params 240 B + grad RMW 480 B per launch
     table["render_bwd_projection"] = ("hbm", views * n * 40 + counts["launches_per_step"] * n * 4 * P * 3,
                                       hbm_peak, "GB/s")
@@ -490,6 +493,7 @@ def main():
     pairs, inst = 0.5 * (p_first + p_last), 0.5 * (i_first + i_last)
     counts = {"steps": a.steps, "sghmc_planes": (ts.p1 - ts.p0) if ts.shard else sc.params.shape[0],
               "pairs": pairs * a.steps, "instances": inst * a.steps, "planes": sc.params.shape[0],
+              "tile_masks": bool(ts.tile_masks),
               "launches_per_step": len(ts.batches) * a.steps,
               "pixels": len(mine) * a.steps * sc.cameras[0].width * sc.cameras[0].height}
     pk = peaks()
