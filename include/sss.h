@@ -50,7 +50,8 @@ typedef enum {
 
 #define SSS_TILE 16          /* tile edge in pixels */
 #define SSS_MAX_BINS 5632    /* bins per view (tiles >> bin_shift); bounded by the scatter CTA's shared memory */
-#define SSS_REC_FLOATS 12    /* floats per projected record (48 B) */
+#define SSS_REC_FLOATS 8     /* floats per projected geometry record (32 B) */
+#define SSS_COL_FLOATS 4     /* floats per projected colour record (16 B) */
 #define SSS_G2D_FLOATS 10    /* floats per screen-space gradient record (40 B) */
 #define SSS_TILE_LISTS 2     /* composited-entry lists per tile (one per 16x8 strip) */
 
@@ -102,9 +103,11 @@ typedef struct {
 } sss_params;
 
 /* Per-(view, component) projection (output of sss_project).
- *  rec   [V][n][12] floats: {mx, my, A, B2}, {C, hmax, o, inv_nu},
- *        {e, r, g, b} with (A, B2/2, C) the conic (Sigma2D)^-1, hmax the L9
- *        cutoff, e = -(nu+2)/2 and (r,g,b) the clamped SH colour.
+ *  rec   [V][n][8] floats: {mx, my, A, B2}, {C, hmax, o, inv_nu} with
+ *        (A, B2/2, C) the conic (Sigma2D)^-1 and hmax the L9 cutoff --
+ *        32-byte records, so the geometry of a component is one sector
+ *  col   [V][n][4] floats: {e, r, g, b}, e = -(nu+2)/2 and (r,g,b) the
+ *        clamped SH colour (the compositors' third record)
  *  depth [V][n] camera-space z of the mean, fp32 (the sort key source, R8).
  *  rect  [V][n][4] int16 inclusive tile rect x0,y0,x1,y1; x0 > x1 = culled.
  * Memory: 60 B per (view, component). */
@@ -115,6 +118,7 @@ typedef struct {
   float* rec;
   float* depth;
   int16_t* rect;
+  float* col;
 } sss_projected;
 
 /* Depth-ordered bin lists (output of sss_bin_sort).  A bin is a square of

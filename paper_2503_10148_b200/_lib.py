@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(PKG, "libsss.so")
 SSS_OK, SSS_ERR_ARG, SSS_ERR_SHAPE, SSS_ERR_CAPACITY, SSS_ERR_CUDA = range(5)
 SSS_TILE = 16
 SSS_MAX_BINS = 5632
-SSS_REC_FLOATS = 12
+SSS_REC_FLOATS = 8
+SSS_COL_FLOATS = 4
 SSS_G2D_FLOATS = 10
 SSS_TILE_LISTS = 2
 SSS_VARIANT_POSITIVE, SSS_VARIANT_GAUSSIAN, SSS_VARIANT_LOWPASS = 1, 2, 4
@@ -45,7 +46,7 @@ class sss_params(C.Structure):
 
 class sss_projected(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_views", C.c_int32), ("reserved", C.c_int32),
-                ("rec", C.c_void_p), ("depth", C.c_void_p), ("rect", C.c_void_p)]
+                ("rec", C.c_void_p), ("depth", C.c_void_p), ("rect", C.c_void_p), ("col", C.c_void_p)]
 
 
 class sss_bins(C.Structure):

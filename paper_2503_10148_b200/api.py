@@ -131,15 +131,17 @@ def n_bins_of(width: int, height: int, bin_shift: int) -> int:
 # ----------------------------------------------------------------- outputs
 @dataclass
 class Projected:
-    rec: torch.Tensor    # [V][n][12] f32
+    rec: torch.Tensor    # [V][n][8] f32 {mx, my, A, B2, C, hmax, o, inv_nu}
     depth: torch.Tensor  # [V][n] f32
     rect: torch.Tensor   # [V][n][4] i16
+    col: torch.Tensor    # [V][n][4] f32 {e, r, g, b}
 
     @classmethod
     def empty(cls, n: int, V: int, device="cuda") -> "Projected":
         return cls(torch.empty((V, n, L.SSS_REC_FLOATS), dtype=torch.float32, device=device),
                    torch.empty((V, n), dtype=torch.float32, device=device),
-                   torch.empty((V, n, 4), dtype=torch.int16, device=device))
+                   torch.empty((V, n, 4), dtype=torch.int16, device=device),
+                   torch.empty((V, n, L.SSS_COL_FLOATS), dtype=torch.float32, device=device))
 
     @property
     def n(self):
@@ -151,7 +153,7 @@ class Projected:
 
     def c(self) -> L.sss_projected:
         return L.sss_projected(self.n, self.n_views, 0, _ptr(self.rec), _ptr(self.depth),
-                               _ptr(self.rect))
+                               _ptr(self.rect), _ptr(self.col))
 
 
 @dataclass

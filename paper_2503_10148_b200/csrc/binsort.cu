@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(256) tile_mask_kernel(const int32_t* __restric
   const int2* rg = reinterpret_cast<const int2*>(ranges) + (size_t)v * g.n_bins;
   const int32_t* idv = ids + (int64_t)v * capacity;
   uint16_t* tmv = tmask + (int64_t)v * capacity;
-  const float4* recv = rec + (int64_t)v * n * 3;
+  const float4* recv = rec + (int64_t)v * n * 2;  // 32-byte geometry records: one sector each
   int bw = 0;  // last bin whose start <= base (empty bins share their successor's start)
   {
     int hi = g.n_bins - 1;
@@ -855,8 +855,8 @@ __global__ void __launch_bounds__(256) tile_mask_kernel(const int32_t* __restric
     float2 e[kMaskPer];
 #pragma unroll
     for (int q = 0; q < kMaskPer; ++q) {
-      a[q] = __ldg(recv + (int64_t)id[q] * 3);
-      e[q] = __ldg(reinterpret_cast<const float2*>(recv + (int64_t)id[q] * 3 + 1));
+      a[q] = __ldg(recv + (int64_t)id[q] * 2);
+      e[q] = __ldg(reinterpret_cast<const float2*>(recv + (int64_t)id[q] * 2 + 1));
     }
     int b = bw;
 #pragma unroll

@@ -8,8 +8,8 @@
 // Design (B200): one thread per component, looping over up to 128 views of
 // the launch, so the 60 parameter floats (240 B at SH degree 3) are read from
 // HBM once per launch instead of once per view.  Loads are coalesced SoA
-// plane reads; the per-view outputs (48 B record + 4 B depth + 8 B rect) are
-// written contiguously.  HBM-bound: 240 B + 60 B/view per component.
+// plane reads; the per-view outputs (32 B geometry record + 16 B colour record
+// + 4 B depth + 8 B rect) are written contiguously.  HBM-bound: 240 B + 60 B/view per component.
 //
 // Precision: every quantity that feeds a discrete decision (depth key, tile
 // rect, the fp32 inclusion test of the compositor) is computed in fp64 in the
@@ -105,6 +105,7 @@ template <int DEG>
 #endif
 __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params P, const __grid_constant__ CamPackD cp,
                                                        int nv, int v0, float4* __restrict__ rec,
+                                                       float4* __restrict__ col,
                                                        float* __restrict__ depth,
                                                        short4* __restrict__ rect) {
   constexpr int K = (DEG + 1) * (DEG + 1);
@@ -236,9 +237,9 @@ __global__ void __launch_bounds__(128, SSS_PROJ_MINB) project_kernel(sss_params 
         }
       }
     }
-    rec[o_idx * 3 + 0] = r0;
-    rec[o_idx * 3 + 1] = r1;
-    rec[o_idx * 3 + 2] = r2;
+    rec[o_idx * 2 + 0] = r0;
+    rec[o_idx * 2 + 1] = r1;
+    col[o_idx] = r2;
     rect[o_idx] = rr;
   }
 }
@@ -253,7 +254,7 @@ extern "C" sss_status sss_project(const sss_params* p, const sss_camera* cams, i
   sss_status st = validate_params(p, "sss_project");
   if (st != SSS_OK) return st;
   if ((st = validate_cams(cams, n_views, "sss_project")) != SSS_OK) return st;
-  if (!out || !out->rec || !out->depth || !out->rect) {
+  if (!out || !out->rec || !out->depth || !out->rect || !out->col) {
     if (p->n > 0) { set_error("sss_project: null output"); return SSS_ERR_ARG; }
   }
   if (out->n != p->n || out->n_views != n_views) {
@@ -274,12 +275,13 @@ extern "C" sss_status sss_project(const sss_params* p, const sss_camera* cams, i
     static thread_local CamPackD cp;  // ~19 KB: kept off the stack
     fill_campack_d(cpf, nv, cp);
     float4* rec = (float4*)out->rec;
+    float4* col = (float4*)out->col;
     short4* rect = (short4*)out->rect;
     switch (p->sh_degree) {
-      case 0: project_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, out->depth, rect); break;
-      case 1: project_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, out->depth, rect); break;
-      case 2: project_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, out->depth, rect); break;
-      default: project_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, out->depth, rect); break;
+      case 0: project_kernel<0><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, col, out->depth, rect); break;
+      case 1: project_kernel<1><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, col, out->depth, rect); break;
+      case 2: project_kernel<2><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, col, out->depth, rect); break;
+      default: project_kernel<3><<<blocks, threads, 0, s>>>(*p, cp, nv, v0, rec, col, out->depth, rect); break;
     }
     count_launch();
     if ((st = check_launch("sss_project")) != SSS_OK) return st;

@@ -38,7 +38,8 @@ constexpr int kWarpsPerRow = 16 / kWarpW;
 static_assert(kRasterWarps == SSS_TILE_LISTS, "one composited-entry list per warp strip");
 
 // Per-warp staging of the bin-list entries: batches of 32 entries, double
-// buffered, the 48-byte records gathered with cp.async (LDGSTS) one batch
+// buffered, the 48-byte records (32-byte geometry + 16-byte colour) gathered
+// with cp.async (LDGSTS) one batch
 // ahead of the compute.
 constexpr int kWB = 32;
 struct WarpStage {
@@ -55,18 +56,19 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Stages one batch: the lanes with `ok` are compacted in lane order (ballot)
-// into slots of buffer `buf` (position and tag), their 48-byte records
+// into slots of buffer `buf` (position and tag), their geometry and colour records
 // gathered by cp.async;
 // commits one async group (also when empty) and returns the entry count.
 __device__ __forceinline__ int stage_batch(WarpStage& S, int buf, bool ok, int32_t pos, int32_t id,
-                                           const float4* __restrict__ rv, unsigned lt, int32_t tag) {
+                                           const float4* __restrict__ rv, const float4* __restrict__ cv,
+                                           unsigned lt, int32_t tag) {
   const unsigned bal = __ballot_sync(0xffffffffu, ok);
   if (ok) {
     const int slot = __popc(bal & lt);
-    const float4* src = rv + (int64_t)id * 3;
+    const float4* src = rv + (int64_t)id * 2;
     cp_async16(&S.r[buf][0][slot], src);
     cp_async16(&S.r[buf][1][slot], src + 1);
-    cp_async16(&S.r[buf][2][slot], src + 2);
+    cp_async16(&S.r[buf][2][slot], cv + id);
     S.pos[buf][slot] = pos;
     S.id[buf][slot] = tag;
   }

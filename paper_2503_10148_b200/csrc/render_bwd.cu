@@ -162,7 +162,8 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
 
 template <bool FILTER, bool L1, bool NUP>
 __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kernel(
-    const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
+    const float4* __restrict__ rec, const float4* __restrict__ col, const short4* __restrict__ rect,
+    const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
     const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
@@ -234,7 +235,8 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const int32_t wlast = m;
   if (lane == 0) SSS_COUNT(7, wlast - start);
 
-  const float4* rv = rec + (int64_t)v * G.n * 3;
+  const float4* rv = rec + (int64_t)v * G.n * 2;  // geometry records (2 x float4)
+  const float4* cv = col + (int64_t)v * G.n;      // colour records
   const short4* rcv = rect + (int64_t)v * G.n;
   const uint16_t* tmv = G.tmask ? G.tmask + (int64_t)v * G.capacity : nullptr;
   WarpStage& S = stage[w];
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     // truncated list's tail (the depth-sorted visible set)
     if (!use_list && ok && (FILTER || p >= BL.mend)) ok = entry_in_tile(G, tmv, p, BL.mend, id, rcv, tx, ty);
     // tag: the entry's g2d record offset from view v0's (uint32, see above)
-    return stage_batch(S, buf, ok, p, id, rv, lt, (int32_t)(vtag + (uint32_t)id * SSS_G2D_FLOATS));
+    return stage_batch(S, buf, ok, p, id, rv, cv, lt, (int32_t)(vtag + (uint32_t)id * SSS_G2D_FLOATS));
   };
 
   int32_t hi = lend;
@@ -761,6 +763,10 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
     return SSS_ERR_ARG;
   }
   if (!fwd->rgb || !fwd->final_T || !fwd->last) { set_error("sss_render_bwd: null frame buffer"); return SSS_ERR_ARG; }
+  if (!(flags & SSS_BWD_PROJECTION_ONLY) && p->n > 0 && (!pr->rec || !pr->col || !pr->rect)) {
+    set_error("sss_render_bwd: null projection buffer");
+    return SSS_ERR_ARG;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   float* g2d = (float*)ws;
   // view groups whose g2d records (n * 10 floats each) span < 2^32 floats:
@@ -769,11 +775,12 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
                                                                     std::max<int64_t>(1, p->n * SSS_G2D_FLOATS)));
   if (const char* e = getenv("SSS_BWD_VIEW_GROUP")) vg = std::max(1, std::min(vg, atoi(e)));  // tests: force groups
   const float4* rec = (const float4*)pr->rec;
+  const float4* col = (const float4*)pr->col;
   const short4* rect = (const short4*)pr->rect;
 #define SSS_BWD_LAUNCH(F, L, N)                                                                           \
   for (int gv0 = 0; gv0 < n_views; gv0 += vg)                                                              \
   render_bwd_kernel<F, L, N><<<dim3(G.tiles_x * G.tiles_y, std::min(vg, n_views - gv0)), kRasterThreads, 0, s>>>( \
-      rec, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last,       \
+      rec, col, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last,  \
       d_rgb, target, loss_out, g2d + (int64_t)gv0 * p->n * SSS_G2D_FLOATS, fwd->tile_list, fwd->tile_count, \
       fwd->tile_cap, gv0)
 #define SSS_BWD_LAUNCH_N(F, L)              \

@@ -75,7 +75,8 @@ __device__ __forceinline__ float& lane_of(float2& v, int k) { return (k & 1) ? v
 
 template <bool FILTER, bool COUNT, bool REC>
 __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kernel(
-    const float4* __restrict__ rec, const short4* __restrict__ rect, const int32_t* __restrict__ ids,
+    const float4* __restrict__ rec, const float4* __restrict__ col, const short4* __restrict__ rect,
+    const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     float* __restrict__ rgb, float* __restrict__ final_T, int32_t* __restrict__ n_contrib,
     int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   const int w = threadIdx.x >> 5, lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
 
-  const float4* rv = rec + (int64_t)v * G.n * 3;
+  const float4* rv = rec + (int64_t)v * G.n * 2;  // geometry records (2 x float4)
+  const float4* cv = col + (int64_t)v * G.n;      // colour records
   const short4* rcv = rect + (int64_t)v * G.n;
   const uint16_t* tmv = G.tmask ? G.tmask + (int64_t)v * G.capacity : nullptr;
 
@@ -160,9 +162,9 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     }
     if (ok) {
       spos[slot] = pos;
-      sa[slot] = rv[(int64_t)id * 3 + 0];
-      sb[slot] = rv[(int64_t)id * 3 + 1];
-      sc[slot] = rv[(int64_t)id * 3 + 2];
+      sa[slot] = rv[(int64_t)id * 2 + 0];
+      sb[slot] = rv[(int64_t)id * 2 + 1];
+      sc[slot] = cv[id];
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
@@ -292,7 +294,7 @@ extern "C" sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bi
   RasterGeom G;
   if (!raster_geom(pr, bins, cams, n_views, G)) { set_error("sss_render_fwd: geometry mismatch"); return SSS_ERR_SHAPE; }
   if (!out->rgb || !out->final_T || !out->last || !bins->ranges ||
-      (pr->n > 0 && (!pr->rec || !pr->rect)) || (bins->capacity > 0 && !bins->ids)) {
+      (pr->n > 0 && (!pr->rec || !pr->col || !pr->rect)) || (bins->capacity > 0 && !bins->ids)) {
     set_error("sss_render_fwd: null buffer");
     return SSS_ERR_ARG;
   }
@@ -300,7 +302,8 @@ extern "C" sss_status sss_render_fwd(const sss_projected* pr, const sss_bins* bi
   const dim3 grid(G.tiles_x * G.tiles_y, n_views);
 #define SSS_FWD_LAUNCH(F, N, R)                                                                         \
   render_fwd_kernel<F, N, R><<<grid, kRasterThreads, 0, s>>>(                                             \
-      (const float4*)pr->rec, (const short4*)pr->rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2],   \
+      (const float4*)pr->rec, (const float4*)pr->col, (const short4*)pr->rect, bins->ids, bins->ranges, G,  \
+      bg[0], bg[1], bg[2],                                                                                 \
       out->rgb, out->final_T, out->n_contrib, out->last, out->tile_list, out->tile_count, out->tile_cap)
 #define SSS_FWD_LAUNCH_R(F, N)                 \
   do {                                         \

@@ -148,7 +148,7 @@ class TrainStep:
         self.capacity = cap
 
     def _proj_view(self, nv: int) -> A.Projected:
-        return A.Projected(self.proj.rec[:nv], self.proj.depth[:nv], self.proj.rect[:nv])
+        return A.Projected(self.proj.rec[:nv], self.proj.depth[:nv], self.proj.rect[:nv], self.proj.col[:nv])
 
     def _frame_view(self, nv: int) -> A.Frame:
         # n_contrib is a diagnostic the backward does not read: counted only

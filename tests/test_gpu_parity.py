@@ -39,6 +39,7 @@ def _check_projection(orc, scene, pr_gpu, v):
     o = orc.project(scene.params, scene.sh_degree, cam)
     rect = pr_gpu.rect[v].cpu().numpy().astype(np.int32)
     rec = pr_gpu.rec[v].cpu().numpy()
+    col = pr_gpu.col[v].cpu().numpy()
     depth = pr_gpu.depth[v].cpu().numpy()
     vis_o = o.n_tiles > 0
     vis_g = rect[:, 0] <= rect[:, 2]
@@ -59,8 +60,8 @@ def _check_projection(orc, scene, pr_gpu, v):
             assert ulp_diff(g[bad], ref[bad]).max() <= 1, name
     np.testing.assert_allclose(rec[vis, 6], o.o[vis], rtol=1e-6, atol=1e-7)
     np.testing.assert_allclose(rec[vis, 7], 1.0 / o.nu[vis], rtol=1e-6)
-    np.testing.assert_allclose(rec[vis, 8], -(o.nu[vis] + 2) / 2, rtol=1e-6)
-    np.testing.assert_allclose(rec[vis, 9:12], o.color[vis], atol=2e-6, rtol=1e-5)
+    np.testing.assert_allclose(col[vis, 0], -(o.nu[vis] + 2) / 2, rtol=1e-6)
+    np.testing.assert_allclose(col[vis, 1:4], o.color[vis], atol=2e-6, rtol=1e-5)
     return o
 
 
@@ -845,7 +846,7 @@ def test_tile_masks(orc, sss, scenes, shift):
         tm = masked.tmask[0, :M0].cpu().numpy().view(np.uint16).astype(np.int64)
         ids = masked.ids[0, :M0].cpu().numpy().astype(np.int64)
         rg = masked.ranges[0].cpu().numpy()
-        rec = pr.rec[0].cpu().numpy().reshape(-1, 12)
+        rec = pr.rec[0].cpu().numpy().reshape(-1, 8)
         rect = pr.rect[0].cpu().numpy().reshape(-1, 4).astype(np.int64)
         tx_n = (cam.width + 15) // 16
         S = 1 << shift
