@@ -18,9 +18,10 @@ full = P.sss_bin_sort(pr, cams, bin_shift=2)
 b = A.Bins.empty(V, full.ranges.shape[1], full.capacity, 2, False, "cuda", 0, params.n, adaptive=True)
 P.sss_bin_sort(pr, cams, bin_shift=2, out=b)
 P.sss_render_fwd(pr, b, cams, out=P.Frame.empty(V, cams[0].height, cams[0].width))
-P.sss_bin_sort(pr, cams, bin_shift=2, out=b)
+P.sss_bin_sort(pr, cams, bin_shift=2, out=b)  # steady-state caps from the warm forward
+P.sss_render_fwd(pr, b, cams, out=P.Frame.empty(V, cams[0].height, cams[0].width))
 torch.cuda.synchronize()
-used = b.used
+used = b.used.clone()  # this forward's consumption (bin_sort resets it)
 lens_full = (full.ranges[..., 1] - full.ranges[..., 0]).long()
 kept = (b.ranges[..., 1] - b.ranges[..., 0]).long()
 complete = used >= (1 << 30)
