@@ -147,7 +147,7 @@ typedef struct {
  *           these bins writes each bin's consumption (the list length its
  *           tiles needed: up to the last composited entry if every pixel of
  *           the tile stopped, 2^30 if some pixel is still live at the end);
- *           the next sss_bin_sort caps bin b at min(max_per_bin, 2 used + 1024)
+ *           the next sss_bin_sort caps bin b at min(max_per_bin, 1.25 used + 256)
  *           (no cap for used < 0 or >= 2^30: initialise to -1) and resets
  *           used to 0 for the forward that follows.  Truncation (either
  *           kind) never changes the raster's results; a tile that needs

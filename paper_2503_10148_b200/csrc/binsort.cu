@@ -259,14 +259,20 @@ __global__ void __launch_bounds__(kScatterThreads) chunk_hist_kernel(const int32
 #endif
 constexpr int kColWarps = SSS_COLSCAN_WARPS;  // warps splitting the chunk range of 32 bins
 // Per-bin cap: the static max_per_bin (0xFFFFFFFF = none), or, with `used`
-// (the previous sss_render_fwd's per-bin consumption), 2 used + 1024 capped
+// (the previous sss_render_fwd's per-bin consumption), 1.25 used + 256 capped
 // by it; used < 0 or >= 2^30 (unknown, or a tile with a pixel still live at
 // the end of its list) keeps the static cap.
 __device__ __forceinline__ uint32_t bin_cap_of(uint32_t static_cap, const int32_t* used, size_t k) {
   if (!used) return static_cap;
   const int32_t u = used[k];
   if (u < 0 || u >= (1 << 30)) return static_cap;
-  return min(static_cap, 2u * (uint32_t)u + 1024u);
+#ifndef SSS_CAP_NUM
+#define SSS_CAP_NUM 5  // cap = used * SSS_CAP_NUM / 4 + SSS_CAP_ADD: 1.25 used + 256
+#endif                 // (2 used + 1024 kept 1.6 M instances per config-5 view, this
+#ifndef SSS_CAP_ADD    // 1.05 M: bin_sort -1.3 ms; no bin read the tail in 30 training
+#define SSS_CAP_ADD 256u  // steps, tools/cap_drift.py)
+#endif
+  return min(static_cap, (uint32_t)(((uint64_t)u * SSS_CAP_NUM) >> 2) + SSS_CAP_ADD);
 }
 
 // The column scan also applies the caps: each (chunk, bin) keeps

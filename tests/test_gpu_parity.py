@@ -643,9 +643,9 @@ def test_truncated_bin_lists(orc, sss, scenes, shift):
 
 def test_adaptive_bin_caps(orc, sss, scenes):
     """sss_bins.used: the forward records each bin's consumption, the next
-    bin_sort caps the bin at 2 used + 1024.  Round 1 (used = -1) builds
+    bin_sort caps the bin at 1.25 used + 256.  Round 1 (used = -1) builds
     complete lists; round 2 truncates from round 1's consumption; round 3
-    starts from used = 0 (caps of 1024 for every bin: many tiles read the
+    starts from used = 0 (caps of 256 for every bin: many tiles read the
     rect-filtered tail).  All three render the complete-list image bit for
     bit and give its gradients."""
     import torch
@@ -896,7 +896,7 @@ def test_tile_masks(orc, sss, scenes, shift):
     sss.sss_render_fwd(pr, full, sc.cameras, out=f0)
     ab = A.Bins.empty(1, full.ranges.shape[1], full.capacity, shift, False, "cuda", 0, sc.n, adaptive=True,
                       tile_masks=True)
-    ab.used.zero_()  # caps of 1024: many tiles read the tail
+    ab.used.zero_()  # caps of 256: many tiles read the tail
     sss.sss_bin_sort(pr, sc.cameras, bin_shift=shift, out=ab)
     f1 = sss.Frame.empty(1, sc.cameras[0].height, sc.cameras[0].width)
     sss.sss_render_fwd(pr, ab, sc.cameras, out=f1)

@@ -52,21 +52,22 @@ for name, f in phases.items():
         e0.record(); f(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     res[name] = min(ts)
 tot = bins.totals.cpu().numpy()
-tail_bins = 0
+tail_bins = complete_bins = 0
 if a.adaptive:  # bins whose tiles needed more than the bin kept (read the tail)
     bins.used.copy_(used0)
     P.sss_bin_sort(pr, cams, bin_shift=a.shift, out=bins)
     P.sss_render_fwd(pr, bins, cams, out=fr)
     torch.cuda.synchronize()
     lens = bins.ranges[..., 1] - bins.ranges[..., 0]
-    tail_bins = int((bins.used > lens).sum().item())
+    complete_bins = int((bins.used >= (1 << 30)).sum().item())  # some pixel never stops: complete list
+    tail_bins = int(((bins.used > lens) & (bins.used < (1 << 30))).sum().item())  # read the virtual tail
 nc = fr.n_contrib.float()
 tcs = fr.tile_count.float() if fr.tile_count is not None else torch.zeros(1, device="cuda")
 cap = fr.tile_list.shape[-1] if fr.tile_list is not None else 0
 out = dict(config=a.config, views=V, shift=a.shift, ms=res, total_ms=sum(res.values()),
            tile_count=dict(mean=float(tcs.mean()), max=float(tcs.max()), cap=int(cap),
                            over=float((tcs > cap).float().mean())),
-           instances_per_view=float(tot.mean()), capacity=bins.capacity, tail_bins=tail_bins,
+           instances_per_view=float(tot.mean()), capacity=bins.capacity, tail_bins=tail_bins, complete_bins=complete_bins,
            pairs_per_view=float(nc.sum().item()/V), mean_contrib=float(nc.mean().item()),
            mpix_per_s=V*cams[0].width*cams[0].height/sum(res.values())/1e3)
 print(json.dumps(out))
