@@ -135,7 +135,11 @@ __global__ void __launch_bounds__(kRadixThreads, SSS_RADIX_MINB) radix_onesweep_
   __shared__ uint32_t skey[kRadixTile];
   __shared__ int32_t sval[kRadixTile];
   __shared__ int s_tile;
-  const int v = blockIdx.y;
+  // segments interleaved in launch order (block b: segment b % n_segs): a
+  // tile's predecessor in its segment started n_segs blocks earlier, so its
+  // published counts are usually there when the look-back reads them
+  const int n_segs = (int)(gridDim.x / (unsigned)tiles);
+  const int v = (int)(blockIdx.x % (unsigned)n_segs);
   const int shift = 8 * pass;
   const int w = threadIdx.x >> 5, lane = lane_id();
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(&tickets[v * 4 + pass], 1u);  // launch order
@@ -260,7 +264,8 @@ void radix_sort_pairs(uint32_t* keys_a, int32_t* vals_a, uint32_t* keys_b, int32
   int32_t *vin = vals_a, *vout = vals_b;
   for (int pass = 0; pass < 4; ++pass) {
     if (pass == 3 && vals_final) vout = vals_final;
-    radix_onesweep_kernel<<<gr, kRadixThreads, 0, s>>>(kin, vin, n, pass, tiles, status, goff, tickets, kout, vout);
+    radix_onesweep_kernel<<<dim3(tiles * n_segs), kRadixThreads, 0, s>>>(kin, vin, n, pass, tiles, status, goff,
+                                                                       tickets, kout, vout);
     count_launch();
     uint32_t* tk = kin; kin = kout; kout = tk;
     int32_t* tv = vin; vin = vout; vout = tv;
