@@ -1010,7 +1010,14 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
         out->capacity, bcap, stage_cap, out->ids, out->keys, resume);
     count_launch();
     if (out->tmask) {
-      const int gx = std::max(1, std::min(1024, 148 * 8 / n_views));
+#ifndef SSS_MASK_GX
+#define SSS_MASK_GX 148
+#endif
+      // 148 CTAs per view, launched view-major: ~8 views in flight, so a
+      // record line fetched for one bin is often still in L2 for the
+      // component's other bins (config 5: -0.26 ms vs all 64 views at once
+      // with 18 CTAs each; 296 / 592 / 1184 per view: -0.22 / -0.13 / 0)
+      const int gx = SSS_MASK_GX;
       tile_mask_kernel<<<dim3(gx, n_views), 256, 0, s>>>(out->ids, out->ranges, out->totals, out->capacity,
                                                                (const float4*)pr->rec, n, g, out->tmask);
       count_launch();
