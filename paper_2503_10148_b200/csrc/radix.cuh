@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) radix_digit_offsets_kernel(const uint32_t
 // One onesweep pass: stable scatter of one 4096-key tile by the digit at
 // 8 * pass (see the header).
 #ifndef SSS_RADIX_MINB
-#define SSS_RADIX_MINB 5  // 5 CTAs/SM (measured -4% vs 3; the per-tile ranking is latency-bound)
+#define SSS_RADIX_MINB 4  // 64 registers, no spills: with interleaved views -0.05 ms vs 5 (48 registers + 40 B of stack), +0.45 ms at 6
 #endif
 __global__ void __launch_bounds__(kRadixThreads, SSS_RADIX_MINB) radix_onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in, int64_t n, int pass,
