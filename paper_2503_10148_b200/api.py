@@ -336,10 +336,11 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
                    target: Optional[torch.Tensor] = None, grad: Optional[Params] = None,
                    loss: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
                    nu_grad_paper: bool = False, stream=None, cams_c=None,
-                   half: Optional[str] = None) -> Params:
-    """grad += d(L)/d(params).  `ws` (zeroed, reusable) holds the screen-space
-    gradient records; it is left zero by the call.  half = "raster" /
-    "projection" runs one of the two kernels (timing instrumentation)."""
+                   half: Optional[str] = None, assign: bool = False) -> Params:
+    """grad += d(L)/d(params) (assign: grad = d(L)/d(params), the old contents
+    unread).  `ws` (zeroed, reusable) holds the screen-space gradient records;
+    it is left zero by the call.  half = "raster" / "projection" runs one of
+    the two kernels (timing instrumentation)."""
     lib = L.load()
     V = len(cams)
     cc = cams_c if cams_c is not None else cameras_c(cams)
@@ -353,7 +354,7 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
             assert t.is_contiguous() and t.dtype == torch.float32
     bgc = (C.c_float * 3)(*[float(x) for x in bg])
     pc, prc, bc, fc, gc = params.c(), proj.c(), bins.c(), frame.c(), grad.c()
-    flags = L.SSS_BWD_NU_GRAD_PAPER if nu_grad_paper else 0
+    flags = (L.SSS_BWD_NU_GRAD_PAPER if nu_grad_paper else 0) | (L.SSS_BWD_GRAD_ASSIGN if assign else 0)
     if half == "raster":
         flags |= L.SSS_BWD_RASTER_ONLY
     elif half == "projection":

@@ -441,7 +441,7 @@ template <int DEG>
 #endif
 __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_params P, const __grid_constant__ CamPack cp,
                                                            int nv, int v0, float2* __restrict__ g2d,
-                                                           sss_params Gd, int64_t i0, int64_t i1) {
+                                                           sss_params Gd, int64_t i0, int64_t i1, bool assign) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const int64_t n = P.n;
   const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -614,7 +614,20 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
     g_o += G2.x;
     g_nu += G2.y;
   }
-  if (!any) return;
+  if (!any) {
+    if (assign) {  // grad = 0 for a component no view touched
+      int64_t gz;
+      const sss_params Gz = block_view(Gd, i, gz);
+      for (int a = 0; a < 3; ++a) Gz.mean[a * gz + i] = 0.f;
+      for (int a = 0; a < 3; ++a) Gz.log_scale[a * gz + i] = 0.f;
+      for (int a = 0; a < 4; ++a) Gz.rot[a * gz + i] = 0.f;
+      Gz.raw_nu[i] = 0.f;
+      Gz.raw_opacity[i] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 3 * K; ++k) Gz.sh[k * gz + i] = 0.f;
+    }
+    return;
+  }
   // Sigma = M M^T, M = R S
   float GM[9];
   for (int a = 0; a < 3; ++a)
@@ -647,14 +660,19 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
   Gd = block_view(Gd, i, gn);
   {
     float cur[12];
+    if (assign) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cur[a] = Gd.mean[a * gn + i];
+      for (int a = 0; a < 12; ++a) cur[a] = 0.f;
+    } else {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cur[3 + a] = Gd.log_scale[a * gn + i];
+      for (int a = 0; a < 3; ++a) cur[a] = Gd.mean[a * gn + i];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) cur[6 + a] = Gd.rot[a * gn + i];
-    cur[10] = Gd.raw_nu[i];
-    cur[11] = Gd.raw_opacity[i];
+      for (int a = 0; a < 3; ++a) cur[3 + a] = Gd.log_scale[a * gn + i];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) cur[6 + a] = Gd.rot[a * gn + i];
+      cur[10] = Gd.raw_nu[i];
+      cur[11] = Gd.raw_opacity[i];
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) Gd.mean[a * gn + i] = cur[a] + gmu[a];
 #pragma unroll
@@ -669,7 +687,7 @@ __global__ void __launch_bounds__(128, SSS_PROJB_MINB) project_bwd_kernel(sss_pa
     float cur[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (k0 + u < 3 * K) cur[u] = Gd.sh[(k0 + u) * gn + i];
+      if (k0 + u < 3 * K) cur[u] = assign ? 0.f : Gd.sh[(k0 + u) * gn + i];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (k0 + u < 3 * K) Gd.sh[(k0 + u) * gn + i] = cur[u] + gsh[k0 + u];
@@ -686,7 +704,8 @@ SSS_COUNTER_ACCESSOR(sss_dev_counters_bwd)
 namespace sss {
 // the a5 kernel over components [i0, i1), views in launches of <= 128
 static sss_status project_bwd_launch(const sss_params& p, const sss_camera* cams, int n_views, float* g2d,
-                                     const sss_params& grad, int64_t i0, int64_t i1, cudaStream_t s) {
+                                     const sss_params& grad, int64_t i0, int64_t i1, cudaStream_t s,
+                                     bool assign = false) {
   if (i1 <= i0) return SSS_OK;
   const int threads = 128;
   const int blocks = div_up(i1 - i0, threads);
@@ -696,10 +715,14 @@ static sss_status project_bwd_launch(const sss_params& p, const sss_camera* cams
     CamPack cp;
     fill_campack(cams, v0, nv, cp);
     switch (p.sh_degree) {
-      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
-      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
-      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
-      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1); break;
+      case 0: project_bwd_kernel<0><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1,
+                                                                 assign && v0 == 0); break;
+      case 1: project_bwd_kernel<1><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1,
+                                                                 assign && v0 == 0); break;
+      case 2: project_bwd_kernel<2><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1,
+                                                                 assign && v0 == 0); break;
+      default: project_bwd_kernel<3><<<blocks, threads, 0, s>>>(p, cp, nv, v0, (float2*)g2d, grad, i0, i1,
+                                                                 assign && v0 == 0); break;
     }
     count_launch();
     if ((st = check_launch("sss_render_bwd(projection)")) != SSS_OK) return st;
@@ -802,6 +825,6 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
 #undef SSS_BWD_LAUNCH_N
 #undef SSS_BWD_LAUNCH
   if (p->n == 0 || (flags & SSS_BWD_RASTER_ONLY)) return SSS_OK;
-  return project_bwd_launch(*p, cams, n_views, g2d, *grad, 0, p->n, s);
+  return project_bwd_launch(*p, cams, n_views, g2d, *grad, 0, p->n, s, (flags & SSS_BWD_GRAD_ASSIGN) != 0);
   return SSS_OK;
 }

@@ -172,8 +172,8 @@ class TrainStep:
         blocked = self.blocks > 0
         if blocked:
             self.grad_blk.buf.zero_()
-        else:
-            self.grad.planes.zero_()
+        # plain layout: the first batch's backward assigns the gradient
+        # (SSS_BWD_GRAD_ASSIGN), later batches accumulate -- no zeroing pass
         self.loss.zero_()
         self._mark("start")
         for bi, b in enumerate(self.batches):
@@ -199,7 +199,8 @@ class TrainStep:
                                          loss=self.loss, ws=self.ws_loss)
                 self._mark("image_loss")
             kw = dict(bg=self.bg, target=None if d_rgb is not None else tg, d_rgb=d_rgb,
-                      grad=self.grad_blk if blocked else self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc)
+                      grad=self.grad_blk if blocked else self.grad, loss=self.loss, ws=self.ws_g2d, cams_c=cc,
+                      assign=not blocked and bi == 0)
             if blocked and exchange and bi == len(self.batches) - 1:
                 A.sss_render_bwd(self.params, pv, bv, cams, fv, half="raster", **kw)
                 self._mark("render_bwd_raster")

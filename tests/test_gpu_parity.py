@@ -940,3 +940,31 @@ def test_backward_view_groups(orc, sss, scenes, monkeypatch):
         for gk, lk in res[1:]:
             assert rel_l2(gk, res[0][0]) <= 1e-5, cap
             assert abs(lk - res[0][1]) <= 1e-6 * abs(res[0][1]), cap
+
+
+def test_backward_grad_assign(orc, sss, scenes):
+    """SSS_BWD_GRAD_ASSIGN (sss.h): grad = result, the old contents unread --
+    on a NaN-filled gradient it gives bit for bit what += gives on zeros,
+    including the zero rows of components no view touched."""
+    import torch
+
+    from gpu_helpers import to_dev
+
+    sc = scenes["blobs_d2_3v"]
+    V, cam = sc.n_views, sc.cameras[0]
+    params = to_dev(sc)
+    pr = sss.sss_project(params, sc.cameras)
+    bins = sss.sss_bin_sort(pr, sc.cameras, bin_shift=1)
+    fr = sss.sss_render_fwd(pr, bins, sc.cameras)
+    d = torch.from_numpy(np.random.default_rng(6).normal(size=(V, 3, cam.height, cam.width))
+                         .astype(np.float32)).cuda()
+    g_add = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d)
+    g_nan = sss.Params(torch.full_like(params.planes, float("nan")), params.sh_degree)
+    g_set = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, d_rgb=d, grad=g_nan, assign=True)
+    torch.cuda.synchronize()
+    a, b = g_add.planes.cpu().numpy(), g_set.planes.cpu().numpy()
+    assert not np.isnan(b).any()
+    # the raster's float atomics may order the per-record sums differently
+    assert rel_l2(b, a) <= 1e-6
+    untouched = np.all(a == 0, axis=0)
+    assert untouched.any() and np.all(b[:, untouched] == 0)
