@@ -82,8 +82,26 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
+#ifndef SSS_FWD_AOS
+#define SSS_FWD_AOS 1
+#endif
+#if SSS_FWD_AOS
+  // one 64-byte slot per staged entry: the composite loop addresses all four
+  // fields from one base (immediate offsets) instead of four array bases
+  struct alignas(16) StageSlot { float4 a, b, c; int32_t pos, pad0, pad1, pad2; };
+  __shared__ StageSlot stg[kBatch];
+#define SA(j) stg[j].a
+#define SB(j) stg[j].b
+#define SC(j) stg[j].c
+#define SPOS(j) stg[j].pos
+#else
   __shared__ float4 sa[kBatch], sb[kBatch], sc[kBatch];
   __shared__ int32_t spos[kBatch];
+#define SA(j) sa[j]
+#define SB(j) sb[j]
+#define SC(j) sc[j]
+#define SPOS(j) spos[j]
+#endif
   __shared__ int32_t wcnt[kRasterWarps];
   const int v = blockIdx.y;
   const int tile = blockIdx.x;
@@ -161,18 +179,18 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       nb = min(kBatch, end - b0);
     }
     if (ok) {
-      spos[slot] = pos;
-      sa[slot] = rv[(int64_t)id * 2 + 0];
-      sb[slot] = rv[(int64_t)id * 2 + 1];
-      sc[slot] = cv[id];
+      SPOS(slot) = pos;
+      SA(slot) = rv[(int64_t)id * 2 + 0];
+      SB(slot) = rv[(int64_t)id * 2 + 1];
+      SC(slot) = cv[id];
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
     const int nb_w = __all_sync(0xffffffffu, all_done()) ? 0 : nb;  // warp already finished
     for (int j = 0; j < nb_w; ++j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      const float4 a = sa[j];
-      const float4 b = sb[j];  // {C, hmax, o, inv_nu}
+      const float4 a = SA(j);
+      const float4 b = SB(j);  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
@@ -200,8 +218,8 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
 #endif
       if (__any_sync(0xffffffffu, any)) {  // warp-uniform; pixels predicated
         if (REC) cm |= 1ull << j;
-        const float4 c = sc[j];  // {e, r, g, b}
-        const int32_t pj1 = spos[j] + 1;
+        const float4 c = SC(j);  // {e, r, g, b}
+        const int32_t pj1 = SPOS(j) + 1;
         if (fabsf(b.z) > 0.989f || b.w < (1.f / 32.f)) {  // warp-uniform, rare
 #pragma unroll
           for (int k = 0; k < kPairs; ++k) composite2<true>(p[k], h[k], b, c, inc[2 * k], inc[2 * k + 1]);
@@ -225,7 +243,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       for (int q = 0; q < kBatch / 32; ++q) {
         const unsigned cq = (unsigned)(cm >> (32 * q));
         const int slot = n_rec + __popc(cq & lt);
-        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = spos[q * 32 + lane];
+        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = SPOS(q * 32 + lane);
         n_rec += __popc(cq);
       }
     }
