@@ -42,10 +42,31 @@ static_assert(kRasterWarps == SSS_TILE_LISTS, "one composited-entry list per war
 // with cp.async (LDGSTS) one batch
 // ahead of the compute.
 constexpr int kWB = 32;
-struct WarpStage {
-  float4 r[2][3][kWB];  // [buffer][record float4][slot]
-  int32_t pos[2][kWB], id[2][kWB];  // id: the caller's tag of the entry
+#ifndef SSS_BWD_AOS
+#define SSS_BWD_AOS 1
+#endif
+#if SSS_BWD_AOS
+// one 64-byte slot per staged entry (the replay loop addresses its fields
+// from one base with immediate offsets)
+struct alignas(16) StageSlot {
+  float4 r[3];
+  int32_t pos, id, pad0, pad1;  // id: the caller's tag of the entry
 };
+struct WarpStage {
+  StageSlot s[2][kWB];  // [buffer][slot]
+  __device__ __forceinline__ float4& rec(int buf, int k, int j) { return s[buf][j].r[k]; }
+  __device__ __forceinline__ int32_t& pos(int buf, int j) { return s[buf][j].pos; }
+  __device__ __forceinline__ int32_t& id(int buf, int j) { return s[buf][j].id; }
+};
+#else
+struct WarpStage {
+  float4 r_[2][3][kWB];  // [buffer][record float4][slot]
+  int32_t pos_[2][kWB], id_[2][kWB];  // id: the caller's tag of the entry
+  __device__ __forceinline__ float4& rec(int buf, int k, int j) { return r_[buf][k][j]; }
+  __device__ __forceinline__ int32_t& pos(int buf, int j) { return pos_[buf][j]; }
+  __device__ __forceinline__ int32_t& id(int buf, int j) { return id_[buf][j]; }
+};
+#endif
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -66,11 +87,11 @@ __device__ __forceinline__ int stage_batch(WarpStage& S, int buf, bool ok, int32
   if (ok) {
     const int slot = __popc(bal & lt);
     const float4* src = rv + (int64_t)id * 2;
-    cp_async16(&S.r[buf][0][slot], src);
-    cp_async16(&S.r[buf][1][slot], src + 1);
-    cp_async16(&S.r[buf][2][slot], cv + id);
-    S.pos[buf][slot] = pos;
-    S.id[buf][slot] = tag;
+    cp_async16(&S.rec(buf, 0, slot), src);
+    cp_async16(&S.rec(buf, 1, slot), src + 1);
+    cp_async16(&S.rec(buf, 2, slot), cv + id);
+    S.pos(buf, slot) = pos;
+    S.id(buf, slot) = tag;
   }
   cp_async_commit();
   return __popc(bal);

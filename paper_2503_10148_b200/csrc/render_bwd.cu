@@ -299,9 +299,9 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     if (lane == 0) { SSS_COUNT(0, 1); SSS_COUNT(6, nb); }
     for (int j = nb - 1; j >= 0; --j) {
       if (lane == 0) SSS_COUNT(1, 1);
-      const int32_t pj = S.pos[buf][j];
-      const float4 a = S.r[buf][0][j];
-      const float4 b = S.r[buf][1][j];  // {C, hmax, o, inv_nu}
+      const int32_t pj = S.pos(buf, j);
+      const float4 a = S.rec(buf, 0, j);
+      const float4 b = S.rec(buf, 1, j);  // {C, hmax, o, inv_nu}
       const float dy = __fsub_rn(py, a.y);
       const float bdy = __fmul_rn(a.w, dy);
       const float cdy2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       }
 #endif
       if (!__any_sync(0xffffffffu, any)) continue;
-      const float4 c = S.r[buf][2][j];  // {e, r, g, b}
+      const float4 c = S.rec(buf, 2, j);  // {e, r, g, b}
       // e / nu = -(nu+2)/(2 nu): dT/dh = einu T/(1 + h/nu); -1/2 for the Gaussian variant
       const float einu = b.w == 0.f ? -0.5f : c.x * b.w;
       static_assert(kPairs == 2, "two pixel pairs per thread");
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
       const float r = warp_reduce10(vals, lane_o);
       // one RED per warp and entry: lanes 0, 2, .. hold the 10 sums of the
       // 40-byte screen-space gradient record g2d[v][id]
-      if (roff >= 0 && r != 0.f) atomicAdd(g2d + ((uint32_t)S.id[buf][j] + (uint32_t)roff), r);
+      if (roff >= 0 && r != 0.f) atomicAdd(g2d + ((uint32_t)S.id(buf, j) + (uint32_t)roff), r);
     }
     __syncwarp();  // this buffer is refilled two batches on
     nb = nb_next;
