@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   // (-1: not a writer): otherwise the compiler re-derives them from %tid in
   // every entry (an S2R and ~15 integer ops)
   int lane_o, roff;
-  asm volatile("mov.b32 %0, %1;" : "=r"(lane_o) : "r"(lane));
+  lane_o = __shfl_sync(0xffffffffu, lane, lane);  // opaque to ptxas too (an asm mov is not: -0.3 ms)
   asm volatile("mov.b32 %0, %1;" : "=r"(roff) : "r"(!(lane & 1) && ridx >= 0 ? ridx : -1));
 
   // The forward's list of the entries this warp's strip composited: replay
