@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "render_bwd or backward or grad" 2>&1 | tail -3 > gpurun_out/ab_tests.log
-rm -f gpurun_out/ab.jsonl
-for rep in 1 2; do for lib in paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_*/libsss.so; do echo $lib >> gpurun_out/ab.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab.jsonl 2>&1; done; done
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-next --e2e-steps 1"
+K='regex:project_kernel|keys_init4_kernel|radix_hist_kernel|radix_onesweep_kernel|chunk_hist_kernel|column_scan_kernel|bin_scan_kernel|scatter_kernel|tile_mask_kernel|render_fwd_kernel|render_bwd_kernel|project_bwd_kernel|sghmc_kernel'
+$CMD > gpurun_out/r02_plain2.log 2>&1 && \
+ncu -f --set full --clock-control none --import-source on -k "$K" -s 32 -c 16 -o /tmp/r02_full $CMD > gpurun_out/r02_ncu_full.log 2>&1
+ncu -i /tmp/r02_full.ncu-rep --page raw --csv > gpurun_out/r02_full_raw.csv
+ncu -i /tmp/r02_full.ncu-rep --page details --csv > gpurun_out/r02_full_details.csv
