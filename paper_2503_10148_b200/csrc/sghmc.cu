@@ -112,7 +112,11 @@ __device__ __forceinline__ void adam_planes(float* theta, const float* grad, flo
 }
 
 template <bool BLOCKED>  // gradient in the component-blocked layout (sss.h sss_params.block)
-__global__ void __launch_bounds__(256) sghmc_kernel(sss_params P, sss_params Gr, sss_params Mo,
+#ifndef SSS_SGHMC_MINB
+#define SSS_SGHMC_MINB 4  // 62 registers, 32 warps/SM: 5.9 TB/s vs 5.6 at 80 registers (tools/sghmc_time.py)
+#endif
+#define SSS_SGHMC_LB __launch_bounds__(256, SSS_SGHMC_MINB)
+__global__ void SSS_SGHMC_LB sghmc_kernel(sss_params P, sss_params Gr, sss_params Mo,
                                                     sss_params Vo, float* __restrict__ r, HP hp) {
   const int64_t n = P.n;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
