@@ -827,7 +827,12 @@ constexpr int kMaskPer = SSS_MASK_PER;  // entries per lane per step, all gather
 // at a time.  The bin of an entry
 // is found once per warp by binary search over the range starts, then by
 // walking forward.
-__global__ void __launch_bounds__(256) tile_mask_kernel(const int32_t* __restrict__ ids,
+#ifdef SSS_MASK_MINB
+#define SSS_MASK_LB __launch_bounds__(256, SSS_MASK_MINB)
+#else
+#define SSS_MASK_LB __launch_bounds__(256)
+#endif
+__global__ void SSS_MASK_LB tile_mask_kernel(const int32_t* __restrict__ ids,
                                                         const int32_t* __restrict__ ranges,
                                                         const int64_t* __restrict__ totals, int64_t capacity,
                                                         const float4* __restrict__ rec, int64_t n, BinGeom g,

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "sghmc or step or graph or variants or loss or relocat or torus or multi" 2>&1 | tail -3 > gpurun_out/ab_tests.log
-python bench.py --no-cpu-baseline > gpurun_out/bench_new.jsonl 2> gpurun_out/bench_new.err
+rm -f gpurun_out/ab.jsonl
+for rep in 1 2; do for lib in paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_*/libsss.so; do echo $lib >> gpurun_out/ab.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab.jsonl 2>&1; done; done
