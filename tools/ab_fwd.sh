@@ -1,2 +1,4 @@
-rm -f gpurun_out/ab.jsonl
-for rep in 1 2; do for lib in paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_*/libsss.so; do echo $lib >> gpurun_out/ab.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab.jsonl 2>&1; done; done
+for c in 4 3 2; do python bench.py --config $c > gpurun_out/bench_c${c}_v4.jsonl 2> gpurun_out/bench_c${c}_v4.err; done
+python bench.py --impl reference > gpurun_out/bench_ref_v3.jsonl 2> gpurun_out/bench_ref_v3.err
+python bench.py > gpurun_out/bench_c5_v6.jsonl 2> gpurun_out/bench_c5_v6.err
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
