@@ -237,6 +237,8 @@ def time_next_rows(ts, targets, pk):
     nv = len(ts.batches[-1])
     fr = ts.frame.rgb[:nv]
     tg = targets[ts.batches[-1][0]:ts.batches[-1][-1] + 1]
+    if tg.dtype != torch.float32:  # the D-SSIM kernel reads fp32 targets (conversion untimed)
+        tg = tg.float() / 255.0
     V, _, H, W = fr.shape
     d = torch.empty_like(fr)
     ws = torch.empty(max(A.image_loss_workspace_bytes(V, H, W), 4), dtype=torch.uint8, device=fr.device)
@@ -342,6 +344,7 @@ def arm_config(a, sc, world):
             "loss": ("eq8: (1-eps_D) L1 + eps_D D-SSIM + eps_o sum|o| + eps_S sum sqrt(lambda)"
                      if (a.eps_dssim or a.eps_o or a.eps_sigma) else "L1"),
             "eps_dssim": a.eps_dssim, "eps_o": a.eps_o, "eps_sigma": a.eps_sigma,
+            "targets": "fp32" if a.eps_dssim > 0.0 else "uint8 images, read as u/255 (SSS_BWD_TARGET_U8)",
             "parallelism": f"view-dp{world}",
             "l2": ("flushed between timed iterations (512 MB write outside the per-iteration events)"
                    if l2_flush_needed(a.config) else
@@ -384,7 +387,7 @@ def main():
     import paper_2503_10148_b200 as P
     from paper_2503_10148_b200 import dist as D
     from paper_2503_10148_b200.step import TrainStep
-    from sss_synth import CONFIG_NAMES, make_scene, make_targets, sghmc_params_for
+    from sss_synth import CONFIG_NAMES, make_scene, make_targets, make_targets_u8, sghmc_params_for
 
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:  # communicator lines (comm_nranks) on stderr
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -397,7 +400,10 @@ def main():
     V = sc.n_views
     mine = D.shard_views(V, rank, world)
     cams = [sc.cameras[v] for v in mine]
-    tg_np = make_targets(sc, mine)
+    # 8-bit target images (as the paper's datasets), read by the fused-L1
+    # backward as u / 255 (sss.h SSS_BWD_TARGET_U8); the D-SSIM loss reads fp32
+    tg_np = make_targets(sc, mine) if a.eps_dssim > 0.0 else make_targets_u8(sc, mine)
+    tg_f32 = tg_np if tg_np.dtype == np.float32 else tg_np.astype(np.float32) / np.float32(255.0)
     targets = torch.from_numpy(tg_np).cuda()
     planes = torch.from_numpy(sc.params).cuda()
     hp = sghmc_params_for(sc, eps_o=a.eps_o, eps_sigma=a.eps_sigma)
@@ -573,7 +579,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = D.allreduce_max(s0.elapsed_time(s1), device=torch.device("cuda", local))
     e2e = {"value": round(e2e_steps / (e2e_ms / 1e3), 4), "unit": "it/s",
-           "h2d_bytes_per_step": int(host_t.numel() * 4), "d2h_bytes_per_step": 4,
+           "h2d_bytes_per_step": int(host_t.numel() * host_t.element_size()), "d2h_bytes_per_step": 4,
            "pipeline": ("next step's targets copied (pinned H2D) on a second stream during the current step; "
                         "each step's loss copied D2H (pinned) and read by the host while the next step runs"),
            "losses_read": len(losses_e2e)}
@@ -586,7 +592,7 @@ def main():
         cb = None
         if world == 1 and not a.no_cpu_baseline:
             try:
-                cb = cpu_baseline_sample(sc, tg_np[0], a.cpu_budget_s, V)
+                cb = cpu_baseline_sample(sc, tg_f32[0], a.cpu_budget_s, V)
             except Exception as ex:  # noqa: BLE001
                 cb = {"error": str(ex)}
         line = {

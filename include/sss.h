@@ -265,6 +265,9 @@ typedef struct sss_step_state {
 #define SSS_BWD_NU_GRAD_PAPER 1 /* use the printed dT/dnu of PAPER.md:1301-1314 (R13) */
 #define SSS_BWD_RASTER_ONLY 2   /* run only the a4 raster half (fills the workspace) */
 #define SSS_BWD_PROJECTION_ONLY 4 /* run only the a5 projection half (consumes it) */
+#define SSS_BWD_TARGET_U8 16    /* target is uint8 [V][3][H][W] (8-bit images, as the
+                                   paper's datasets): value u / 255 (fp32, correctly
+                                   rounded division) -- a quarter of the bytes */
 #define SSS_BWD_GRAD_ASSIGN 8   /* grad = result instead of grad += result: every
                                    component's gradient is written (zeros where no
                                    view touched it) and the old contents are not
@@ -319,13 +322,14 @@ SSS_API size_t sss_render_bwd_workspace(int64_t n, int32_t n_views);
 /* a4 + a5 (+ a6) — closed-form backward of
  * sss_render_fwd with gating frozen (R22), accumulated (+=) into grad over all
  * views.  Image gradient: d_rgb [V][3][H][W] if non-NULL, else the fused L1
- * loss against target [V][3][H][W]: dL/dC = sign(C - target) / (3 H W) per
+ * loss against target [V][3][H][W] (fp32, or uint8 with SSS_BWD_TARGET_U8):
+ * dL/dC = sign(C - target) / (3 H W) per
  * view (Eq. 8's L1 term, R20); in that case loss_out (device float[1],
  * nullable) is incremented by sum_v mean|C - target|.  fwd must be the
  * output of sss_render_fwd for the same inputs.  flags: SSS_BWD_*. */
 SSS_API sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, const sss_bins* bins,
                           const sss_camera* cams, int32_t n_views, const float* bg,
-                          const sss_frame* fwd, const float* d_rgb, const float* target,
+                          const sss_frame* fwd, const float* d_rgb, const void* target,
                           float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
                           int32_t flags, void* stream);
 

@@ -24,6 +24,7 @@ SSS_BWD_NU_GRAD_PAPER = 1
 SSS_BWD_RASTER_ONLY = 2
 SSS_BWD_PROJECTION_ONLY = 4
 SSS_BWD_GRAD_ASSIGN = 8
+SSS_BWD_TARGET_U8 = 16
 
 EXPORTS = ["sss_project", "sss_bin_sort_workspace", "sss_bin_sort", "sss_check_overflow",
            "sss_render_fwd", "sss_render_bwd_workspace", "sss_render_bwd", "sss_sghmc_step",

@@ -349,12 +349,15 @@ def sss_render_bwd(params: Params, proj: Projected, bins: Bins, cams: Sequence, 
     if ws is None:
         ws = torch.zeros(max(need, 4), dtype=torch.uint8, device=params.planes.device)
     assert ws.numel() >= need
-    for t in (d_rgb, target):
-        if t is not None:
-            assert t.is_contiguous() and t.dtype == torch.float32
+    if d_rgb is not None:
+        assert d_rgb.is_contiguous() and d_rgb.dtype == torch.float32
+    if target is not None:  # fp32, or uint8 images (value u / 255, sss.h SSS_BWD_TARGET_U8)
+        assert target.is_contiguous() and target.dtype in (torch.float32, torch.uint8)
     bgc = (C.c_float * 3)(*[float(x) for x in bg])
     pc, prc, bc, fc, gc = params.c(), proj.c(), bins.c(), frame.c(), grad.c()
     flags = (L.SSS_BWD_NU_GRAD_PAPER if nu_grad_paper else 0) | (L.SSS_BWD_GRAD_ASSIGN if assign else 0)
+    if target is not None and target.dtype == torch.uint8:
+        flags |= L.SSS_BWD_TARGET_U8
     if half == "raster":
         flags |= L.SSS_BWD_RASTER_ONLY
     elif half == "projection":

@@ -166,9 +166,9 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     const int32_t* __restrict__ ids,
     const int32_t* __restrict__ ranges, RasterGeom G, float bg0, float bg1, float bg2,
     const float* __restrict__ rgb, const float* __restrict__ final_T, const int32_t* __restrict__ last,
-    const float* __restrict__ d_rgb, const float* __restrict__ target, float* __restrict__ loss_out,
+    const float* __restrict__ d_rgb, const void* __restrict__ target, float* __restrict__ loss_out,
     float* __restrict__ g2d, const int32_t* __restrict__ tile_list, const int32_t* __restrict__ tile_count,
-    int32_t tile_cap, int v0) {
+    int32_t tile_cap, int v0, bool tu8) {
   __shared__ WarpStage stage[kRasterWarps];
   // views v0 + blockIdx.y; g2d points at view v0's records and the entry
   // tags are 32-bit record offsets from it (the host sizes the view groups
@@ -210,8 +210,19 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
     m = max(m, qlast[k]);
     if (L1) {
       const float* cimg = rgb + (int64_t)v * 3 * HW + pix;
-      const float* timg = target + (int64_t)v * 3 * HW + pix;
-      const float d0 = cimg[0] - timg[0], d1 = cimg[HW] - timg[HW], d2 = cimg[2 * HW] - timg[2 * HW];
+      float t0, t1, t2;
+      if (tu8) {  // 8-bit targets: u / 255, correctly rounded (SSS_BWD_TARGET_U8)
+        const uint8_t* t8 = static_cast<const uint8_t*>(target) + (int64_t)v * 3 * HW + pix;
+        t0 = __fdiv_rn((float)t8[0], 255.f);
+        t1 = __fdiv_rn((float)t8[HW], 255.f);
+        t2 = __fdiv_rn((float)t8[2 * HW], 255.f);
+      } else {
+        const float* timg = static_cast<const float*>(target) + (int64_t)v * 3 * HW + pix;
+        t0 = timg[0];
+        t1 = timg[HW];
+        t2 = timg[2 * HW];
+      }
+      const float d0 = cimg[0] - t0, d1 = cimg[HW] - t1, d2 = cimg[2 * HW] - t2;
       g0 = d0 > 0.f ? inv3P : (d0 < 0.f ? -inv3P : 0.f);
       g1 = d1 > 0.f ? inv3P : (d1 < 0.f ? -inv3P : 0.f);
       g2 = d2 > 0.f ? inv3P : (d2 < 0.f ? -inv3P : 0.f);
@@ -758,7 +769,7 @@ extern "C" size_t sss_render_bwd_workspace(int64_t n, int32_t n_views) {
 
 extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* pr, const sss_bins* bins,
                                      const sss_camera* cams, int32_t n_views, const float* bg,
-                                     const sss_frame* fwd, const float* d_rgb, const float* target,
+                                     const sss_frame* fwd, const float* d_rgb, const void* target,
                                      float* loss_out, sss_params* grad, void* ws, size_t ws_bytes,
                                      int32_t flags, void* stream) {
   sss_status st;
@@ -805,7 +816,7 @@ extern "C" sss_status sss_render_bwd(const sss_params* p, const sss_projected* p
   render_bwd_kernel<F, L, N><<<dim3(G.tiles_x * G.tiles_y, std::min(vg, n_views - gv0)), kRasterThreads, 0, s>>>( \
       rec, col, rect, bins->ids, bins->ranges, G, bg[0], bg[1], bg[2], fwd->rgb, fwd->final_T, fwd->last,  \
       d_rgb, target, loss_out, g2d + (int64_t)gv0 * p->n * SSS_G2D_FLOATS, fwd->tile_list, fwd->tile_count, \
-      fwd->tile_cap, gv0)
+      fwd->tile_cap, gv0, (flags & SSS_BWD_TARGET_U8) != 0)
 #define SSS_BWD_LAUNCH_N(F, L)              \
   do {                                      \
     if (nup) SSS_BWD_LAUNCH(F, L, true);    \

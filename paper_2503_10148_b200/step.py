@@ -195,6 +195,7 @@ class TrainStep:
                 self.stats["instances"] += bv.totals.sum()
             d_rgb = None
             if self.eps_dssim > 0.0:
+                assert tg.dtype == torch.float32, "the D-SSIM loss reads fp32 targets"
                 d_rgb = A.sss_image_loss(fv.rgb, tg, self.eps_dssim, d_rgb=self.d_rgb[:nv],
                                          loss=self.loss, ws=self.ws_loss)
                 self._mark("image_loss")

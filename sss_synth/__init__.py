@@ -17,6 +17,7 @@ from .scenes import (  # noqa: F401
     make_optimizer_state,
     sghmc_params_for,
     make_targets,
+    make_targets_u8,
     make_cameras,
     look_at,
     sh_coeff_count,

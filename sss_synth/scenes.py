@@ -369,6 +369,20 @@ def make_targets(scene: Scene, views=None, seed_offset: int = 0) -> np.ndarray:
     return out
 
 
+def make_targets_u8(scene: Scene, views=None, seed_offset: int = 0) -> np.ndarray:
+    """8-bit target images [len(views)][3][H][W] uint8 (uniform 0..255),
+    seeded per view: the form of the paper's datasets (8-bit PNG/JPEG); the
+    losses read them as u / 255 (sss.h SSS_BWD_TARGET_U8)."""
+    views = range(scene.n_views) if views is None else views
+    views = list(views)
+    cam = scene.cameras[0]
+    out = np.empty((len(views), 3, cam.height, cam.width), np.uint8)
+    for i, v in enumerate(views):
+        rng = np.random.Generator(np.random.PCG64(scene.seed * 1000 + 17 + v + seed_offset))
+        out[i] = rng.integers(0, 256, (3, cam.height, cam.width), dtype=np.uint8)
+    return out
+
+
 def make_optimizer_state(scene: Scene, seed: int = 99, zero: bool = False):
     """(momentum r [3][n], adam m [P][n], adam v [P][n]) float32.
 

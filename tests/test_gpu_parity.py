@@ -968,3 +968,36 @@ def test_backward_grad_assign(orc, sss, scenes):
     assert rel_l2(b, a) <= 1e-6
     untouched = np.all(a == 0, axis=0)
     assert untouched.any() and np.all(b[:, untouched] == 0)
+
+
+def test_backward_u8_targets(orc, sss, scenes):
+    """SSS_BWD_TARGET_U8: 8-bit targets read as u / 255 give the gradients
+    and the L1 loss of the fp32 targets u / 255 (correctly rounded) bit for
+    bit (up to the float atomics' order), and match the oracle's backward."""
+    import torch
+
+    from gpu_helpers import to_dev
+    from sss_synth import make_targets_u8
+
+    sc = scenes["blobs_d2_3v"]
+    V, cam = sc.n_views, sc.cameras[0]
+    t8 = make_targets_u8(sc)
+    tf = t8.astype(np.float32) / np.float32(255.0)
+    params = to_dev(sc)
+    pr = sss.sss_project(params, sc.cameras)
+    bins = sss.sss_bin_sort(pr, sc.cameras, bin_shift=1)
+    fr = sss.sss_render_fwd(pr, bins, sc.cameras)
+    res = []
+    for t in (torch.from_numpy(tf).cuda(), torch.from_numpy(t8).cuda()):
+        loss = torch.zeros(1, device="cuda")
+        g = sss.sss_render_bwd(params, pr, bins, sc.cameras, fr, target=t, loss=loss)
+        torch.cuda.synchronize()
+        res.append((g.planes.cpu().numpy().astype(np.float64), float(loss.item())))
+    assert rel_l2(res[1][0], res[0][0]) <= 1e-6
+    assert abs(res[1][1] - res[0][1]) <= 1e-6 * abs(res[0][1])
+    # and the oracle's loss over the same fp32 targets
+    ref = 0.0
+    for v in range(V):
+        img = orc.render(sc.params, sc.sh_degree, sc.cameras[v], mode="tiled")
+        ref += float(np.mean(np.abs(img.rgb.astype(np.float64) - tf[v])))
+    assert abs(res[1][1] - ref) <= 1e-4 * abs(ref), (res[1][1], ref)

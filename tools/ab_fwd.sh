@@ -1,4 +1,2 @@
-for c in 4 3 2; do python bench.py --config $c > gpurun_out/bench_c${c}_v4.jsonl 2> gpurun_out/bench_c${c}_v4.err; done
-python bench.py --impl reference > gpurun_out/bench_ref_v3.jsonl 2> gpurun_out/bench_ref_v3.err
-python bench.py > gpurun_out/bench_c5_v6.jsonl 2> gpurun_out/bench_c5_v6.err
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/ab_tests.log
+python bench.py > gpurun_out/bench_c5_v7.jsonl 2> gpurun_out/bench_c5_v7.err
