@@ -148,7 +148,11 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   // REC: this warp's list of the entries some pixel of its 16x8 strip
   // composited, appended after each batch from warp-uniform bit masks
   const int64_t lslot = ((int64_t)v * G.tiles_x * G.tiles_y + tile) * kRasterWarps + w;
-  int32_t* tl = REC ? tile_list + lslot * tile_cap : nullptr;
+  // the warp's list base lives in shared memory: recomputing the 64-bit
+  // address from the block indices at every batch's write-out cost ~40
+  // instructions (the registers are all taken by the pixel state)
+  __shared__ int32_t* s_tl[kRasterWarps];
+  if (REC && lane == 0) s_tl[w] = tile_list + lslot * tile_cap;
   int32_t n_rec = 0;
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
     if (__syncthreads_count(!all_done()) == 0) break;
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       for (int q = 0; q < kBatch / 32; ++q) {
         const unsigned cq = (unsigned)(cm >> (32 * q));
         const int slot = n_rec + __popc(cq & lt);
-        if (((cq >> lane) & 1u) && slot < tile_cap) tl[slot] = SPOS(q * 32 + lane);
+        if (((cq >> lane) & 1u) && slot < tile_cap) s_tl[w][slot] = SPOS(q * 32 + lane);
         n_rec += __popc(cq);
       }
     }
