@@ -82,6 +82,9 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     int32_t* __restrict__ last, int32_t* __restrict__ tile_list, int32_t* __restrict__ tile_count,
     int32_t tile_cap) {
   static_assert(kBatch == kRasterThreads, "one staged entry per thread");
+#ifndef SSS_FWD_SMEM_PTRS
+#define SSS_FWD_SMEM_PTRS 1
+#endif
 #ifndef SSS_FWD_AOS
 #define SSS_FWD_AOS 1
 #endif
@@ -153,6 +156,17 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
   // instructions (the registers are all taken by the pixel state)
   __shared__ int32_t* s_tl[kRasterWarps];
   if (REC && lane == 0) s_tl[w] = tile_list + lslot * tile_cap;
+#if SSS_FWD_SMEM_PTRS
+  // the same for the staging's per-view bases (ids, tail, records, masks)
+  __shared__ const void* s_ptr[5];
+  if (threadIdx.x == 0) {
+    s_ptr[0] = BL.ids;
+    s_ptr[1] = BL.tail ? BL.tail + BL.tail0 - BL.mend : nullptr;  // index by the list position
+    s_ptr[2] = rv;
+    s_ptr[3] = cv;
+    s_ptr[4] = tmv;
+  }
+#endif
   int32_t n_rec = 0;
   for (int32_t b0 = start; b0 < end; b0 += kBatch) {
     if (__syncthreads_count(!all_done()) == 0) break;
@@ -161,11 +175,18 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
     unsigned long long cm = 0ull;  // REC: this warp's composited entries (warp-uniform bits)
     const int32_t pos = b0 + (int32_t)threadIdx.x;
     bool ok = (int)threadIdx.x < kBatch && pos < end;
+#if SSS_FWD_SMEM_PTRS
+    const int32_t id = !ok ? 0 : pos < BL.mend ? __ldg(static_cast<const int32_t*>(s_ptr[0]) + pos)
+                                               : __ldg(static_cast<const int32_t*>(s_ptr[1]) + pos);
+    const uint16_t* tmv_s = static_cast<const uint16_t*>(s_ptr[4]);
+#else
     const int32_t id = ok ? BL.id(pos) : 0;
+    const uint16_t* tmv_s = tmv;
+#endif
     int slot, nb;
     // the truncated list's tail is the depth-sorted visible set: always filtered
     if (FILTER || end > BL.mend) {
-      if (ok && (FILTER || pos >= BL.mend)) ok = entry_in_tile(G, tmv, pos, BL.mend, id, rcv, tx, ty);
+      if (ok && (FILTER || pos >= BL.mend)) ok = entry_in_tile(G, tmv_s, pos, BL.mend, id, rcv, tx, ty);
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       if (lane == 0) wcnt[w] = __popc(bal);
       __syncthreads();
@@ -183,10 +204,17 @@ __global__ void __launch_bounds__(kRasterThreads, kFwdMinBlocks) render_fwd_kern
       nb = min(kBatch, end - b0);
     }
     if (ok) {
+#if SSS_FWD_SMEM_PTRS
+      const float4* rvs = static_cast<const float4*>(s_ptr[2]);
+      const float4* cvs = static_cast<const float4*>(s_ptr[3]);
+#else
+      const float4* rvs = rv;
+      const float4* cvs = cv;
+#endif
       SPOS(slot) = pos;
-      SA(slot) = rv[(int64_t)id * 2 + 0];
-      SB(slot) = rv[(int64_t)id * 2 + 1];
-      SC(slot) = cv[id];
+      SA(slot) = rvs[(int64_t)id * 2 + 0];
+      SB(slot) = rvs[(int64_t)id * 2 + 1];
+      SC(slot) = cvs[id];
     }
     __syncthreads();
     if (threadIdx.x == 0) SSS_COUNT(6, nb);
