@@ -160,6 +160,9 @@ __device__ __forceinline__ void pair_grad2(PixB2& p, float2 dx, float2 h, float4
   e.sdhdx2 = FIRST ? mul2(dhdx, dx) : fma2(dhdx, dx, e.sdhdx2);
 }
 
+#ifndef SSS_BWD_SMEM_PTRS
+#define SSS_BWD_SMEM_PTRS 1
+#endif
 template <bool FILTER, bool L1, bool NUP>
 __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kernel(
     const float4* __restrict__ rec, const float4* __restrict__ col, const short4* __restrict__ rect,
@@ -274,19 +277,48 @@ __global__ void __launch_bounds__(kRasterThreads, kBwdMinBlocks) render_bwd_kern
   const int32_t* tl = use_list ? tile_list + lslot * tile_cap : nullptr;
   const int32_t lbeg = use_list ? 0 : start;
   const int32_t lend = use_list ? tcount : wlast;
+#if SSS_BWD_SMEM_PTRS
+  // the warp's per-batch bases live in shared memory (the compiler would
+  // otherwise rebuild the 64-bit addresses from the block indices at every
+  // batch: the registers are all taken by the pixel state)
+  __shared__ const void* s_bp[kRasterWarps][5];
+  if (lane == 0) {
+    s_bp[w][0] = tl;
+    s_bp[w][1] = BL.ids;
+    s_bp[w][2] = BL.tail ? BL.tail + BL.tail0 - BL.mend : nullptr;  // index by the list position
+    s_bp[w][3] = rv;
+    s_bp[w][4] = cv;
+  }
+  __syncwarp();
+  auto pos_at = [&](int32_t h) -> int32_t {  // lane's entry of the batch [max(lbeg, h - 32), h)
+    const int32_t li = h - kWB + lane;
+    if (h <= lbeg || li < lbeg) return INT32_MAX;
+    return use_list ? __ldg(static_cast<const int32_t*>(s_bp[w][0]) + li) : li;
+  };
+  auto id_at = [&](int32_t p) -> int32_t {
+    return p >= wlast ? -1 : p < BL.mend ? __ldg(static_cast<const int32_t*>(s_bp[w][1]) + p)
+                                         : __ldg(static_cast<const int32_t*>(s_bp[w][2]) + p);
+  };
+#else
   auto pos_at = [&](int32_t h) -> int32_t {  // lane's entry of the batch [max(lbeg, h - 32), h)
     const int32_t li = h - kWB + lane;
     if (h <= lbeg || li < lbeg) return INT32_MAX;
     return use_list ? __ldg(tl + li) : li;
   };
   auto id_at = [&](int32_t p) -> int32_t { return p < wlast ? BL.id(p) : -1; };
+#endif
   auto issue = [&](int buf, int32_t p, int32_t id) -> int {
     bool ok = id >= 0;
     // unlisted replay: filter by the tile rect with bins, and always in the
     // truncated list's tail (the depth-sorted visible set)
     if (!use_list && ok && (FILTER || p >= BL.mend)) ok = entry_in_tile(G, tmv, p, BL.mend, id, rcv, tx, ty);
     // tag: the entry's g2d record offset from view v0's (uint32, see above)
+#if SSS_BWD_SMEM_PTRS
+    return stage_batch(S, buf, ok, p, id, static_cast<const float4*>(s_bp[w][3]),
+                       static_cast<const float4*>(s_bp[w][4]), lt, (int32_t)(vtag + (uint32_t)id * SSS_G2D_FLOATS));
+#else
     return stage_batch(S, buf, ok, p, id, rv, cv, lt, (int32_t)(vtag + (uint32_t)id * SSS_G2D_FLOATS));
+#endif
   };
 
   int32_t hi = lend;
