@@ -1,3 +1,4 @@
-rm -f gpurun_out/ab.jsonl
-timeout 900 python -m pytest tests -m gpu -x -q -k "tile_list or render_bwd or backward or tile_masks or truncated or adaptive" 2>&1 | tail -3 > gpurun_out/ab_tests.log
-for rep in 1 2; do for lib in paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_*/libsss.so; do echo $lib >> gpurun_out/ab.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab.jsonl 2>&1; done; done
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+python bench.py > gpurun_out/bench_c5_v8.jsonl 2> gpurun_out/bench_c5_v8.err
+for c in 4 3 2; do python bench.py --config $c > gpurun_out/bench_c${c}_v6.jsonl 2> gpurun_out/bench_c${c}_v6.err; done
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
