@@ -1004,7 +1004,10 @@ extern "C" sss_status sss_bin_sort(const sss_projected* pr, const sss_camera* ca
     // truncated lists: most chunks keep little, and the walk is latency-bound,
     // so a small stage (more CTAs per SM) wins; the few front chunks that keep
     // more than it take the direct path
-    if (trunc) want = std::min<int64_t>(want, 4096);
+#ifndef SSS_SCATTER_TRUNC_STAGE
+#define SSS_SCATTER_TRUNC_STAGE 4096
+#endif
+    if (trunc) want = std::min<int64_t>(want, SSS_SCATTER_TRUNC_STAGE);
     const int64_t room = ((int64_t)kScatterSmemMax - (int64_t)fixed) / 4;
     const int stage_cap = (int)std::max<int64_t>(0, std::min<int64_t>((want + 31) & ~31, room));
     const size_t ssm = fixed + (size_t)stage_cap * 4;
