@@ -1,2 +1,3 @@
-rm -f gpurun_out/ab.jsonl
-for rep in 1 2; do for lib in paper_2503_10148_b200/libsss.so paper_2503_10148_b200/build_SSS_*/libsss.so; do echo $lib >> gpurun_out/ab.jsonl; SSS_LIB=$lib python tools/phase_times.py --config 5 --views 64 --shift 2 --no-count --reps 3 --adaptive --tmask 1 >> gpurun_out/ab.jsonl 2>&1; done; done
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+python bench.py > gpurun_out/bench_final.jsonl 2> gpurun_out/bench_final.err; tail -c 300 gpurun_out/bench_final.jsonl
